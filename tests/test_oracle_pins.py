@@ -1,0 +1,384 @@
+"""Pins of the CPU oracle to what the paper and mathematics fix (no GPU).
+
+Every check here relates oracle/ to something other than itself: a value the
+paper (or SPEC.md's worked examples derived from it) prints, a hand-derived
+golden fixture, a closed form, an invariant of the method, or the separately
+written untiled brute force in tests/untiled_reference.py.  Citations are
+PAPER.md lines (P:Lnnn) / SPEC.md lines (S:Lnnn); R# = DESIGN.md readings.
+"""
+from __future__ import annotations
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+from paper_2604_25306_b200.inputs import gen_int8_qkv, gen_workload
+from tests.untiled_reference import untiled_attention
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+# ----------------------------------------------------------------- Eq. 1-2
+def test_quantize_worked_example(orc):
+    # [-1, 0.5, 1] -> s = 1/127, [-127, 64, 127] (Eq. 2 + R1).
+    xq, s = orc.quantize(np.array([-1.0, 0.5, 1.0], np.float32))
+    assert s == np.float32(1.0) / np.float32(127.0)
+    assert xq.tolist() == [-127, 64, 127]
+
+
+def test_quantize_round_half_away(orc):
+    # R1: ties round away from zero (2.5 -> 3, -2.5 -> -3, 0.5 -> 1); half-even
+    # would give 2, -2, 0.  amax = 127 makes s = 1 exactly.
+    xq, s = orc.quantize(np.array([127.0, 2.5, -2.5, 0.5, -0.5, 1.5], np.float32))
+    assert s == 1.0
+    assert xq.tolist() == [127, 3, -3, 1, -1, 2]
+
+
+def test_quantize_zero_tensor(orc):
+    # R3: all-zero tensor -> s = 1/127 (inside the attention's scale range).
+    xq, s = orc.quantize(np.zeros(17, np.float32))
+    assert s == np.float32(1.0) / np.float32(127.0)
+    assert not xq.any()
+
+
+def test_quantize_error_bound_and_idempotence(orc):
+    rng = np.random.default_rng(1)
+    x = (rng.standard_normal(100_000) * 3).astype(np.float32)
+    xq, s = orc.quantize(x)
+    # Eq. 2: amax maps to +-127, |x - s x^| <= s/2 (no element is clamped).
+    assert np.abs(xq).max() == 127
+    assert np.all(np.abs(x.astype(np.float64) - s * xq.astype(np.float64)) <= s / 2 * (1 + 1e-6))
+    assert xq.min() >= -127  # symmetric scale never reaches -128
+    # quantize o dequantize o quantize = quantize
+    y = orc.dequantize(xq, s)
+    xq2, s2 = orc.quantize(y)
+    assert np.array_equal(xq, xq2) and s2 == s
+
+
+def test_quantize_bf16_is_widened_f32(orc):
+    rng = np.random.default_rng(2)
+    x = (rng.standard_normal(4096) * 2).astype(np.float32)
+    bits = (x.view(np.uint32) >> 16).astype(np.uint16)       # truncate to bf16
+    widened = (bits.astype(np.uint32) << 16).view(np.float32)
+    a, sa = orc.quantize(bits)
+    b, sb = orc.quantize(widened)
+    assert sa == sb and np.array_equal(a, b)
+
+
+def test_dequantize_exact(orc):
+    xq = np.array([-128, -1, 0, 1, 127], np.int8)
+    y = orc.dequantize(xq, 0.5)
+    assert y.tolist() == [-64.0, -0.5, 0.0, 0.5, 63.5]
+
+
+# ----------------------------------------------------------- constants
+def _golden_params():
+    rows = []
+    with open(os.path.join(HERE, "golden", "params_hand.txt")) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            lhs, rhs = line.split("|")
+            sq, sk, d = lhs.split()
+            rows.append((float(sq), float(sk), int(d), tuple(int(t) for t in rhs.split())))
+    return rows
+
+
+@pytest.mark.parametrize("sq,sk,d,expect", _golden_params())
+def test_params_hand_derived(orc, sq, sk, d, expect):
+    p = orc.derive_params(sq, sk, d)
+    assert (p["s_inv"], p["n"], p["r_p"], p["m_p"]) == expect
+
+
+def test_params_scale_range(orc):
+    # s outside [2^-24, 0.5] is rejected (R6 range).
+    with pytest.raises(ValueError):
+        orc.derive_params(1.0, 1.0, 1)       # s = 1.44 > 0.5
+    with pytest.raises(ValueError):
+        orc.derive_params(1e-5, 1e-5, 64)    # s ~ 1.8e-11 < 2^-24
+    with pytest.raises(ValueError):
+        orc.derive_params(0.0, 0.1, 64)
+
+
+# ----------------------------------------------------------- Eq. 9-10
+def test_make_multiplier_worked_examples(orc):
+    # S:L163-165 (direct evaluation of Eq. 9-10 with b = 8).
+    assert orc.make_multiplier(1.0) == (0, 8, 256)
+    assert orc.make_multiplier(2.0) == (1, 7, 256)
+    assert orc.make_multiplier(0.003) == (-9, 17, 393)
+    # S:L174 prints 99 for 1000 x 0.1; evaluating Eq. 9-10 by hand gives
+    # n = floor(log2 0.1) = -4, r = 12, M = round(409.6) = 410, 410000 >> 12 = 100.
+    assert orc.make_multiplier(0.1) == (-4, 12, 410)
+    assert orc.requantize(1000, 410, 12) == 100
+
+
+def test_requantize_bound(orc):
+    # Eq. 10 realises x * ratio within 1 + x*ratio*2^-9 (M has 9 significant bits).
+    rng = np.random.default_rng(3)
+    for ratio in [0.003, 0.07, 0.5, 0.99]:
+        n, r, m = orc.make_multiplier(ratio)
+        assert 256 <= m <= 512
+        for x in rng.integers(0, 20000, 200):
+            y = orc.requantize(int(x), m, r)
+            exact = math.floor(x * ratio)
+            if exact <= 127:
+                assert abs(y - exact) <= 1 + x * ratio * 2 ** -9
+    # R8 clamp: P^ never exceeds 127
+    assert orc.requantize(10**6, 300, 8) == 127
+
+
+# ----------------------------------------------------------- Alg. 2
+S_INVS = [2, 3, 22, 127, 251, 1287, 1420, 2293, 8030, 11769, 65537, 1 << 20, (1 << 24) - 3]
+
+
+@pytest.mark.parametrize("s_inv", S_INVS)
+def test_shift_exp2_hand_traces(orc, s_inv):
+    # Alg. 2 traced by hand: x = 0 -> q = 0, r = 0, y = s_inv;
+    # x = -s_inv -> q = 1, r = 0, y = s_inv >> 1.
+    assert orc.shift_exp2(0, s_inv) == s_inv
+    assert orc.shift_exp2(-s_inv, s_inv) == s_inv // 2
+    # knot identity: x = -k s_inv -> r = 0, y = s_inv >> k
+    for k in range(0, 31):
+        if k * s_inv <= 1 << 23:
+            assert orc.shift_exp2(-k * s_inv, s_inv) == s_inv >> k
+
+
+@pytest.mark.parametrize("s_inv", [22, 251, 1420, 2293, 8030])
+def test_shift_exp2_exhaustive_range_monotone_chord(orc, s_inv):
+    # Exhaustive over the live input range x in [-2^22, 0] (R18 bound).
+    x = np.arange(-(1 << 22), 1, dtype=np.int64)
+    y = orc.shift_exp2_array(x, s_inv)
+    # range invariant: y in [0, s_inv]
+    assert y.min() >= 0 and y.max() == s_inv
+    # exact monotonicity (R6: holds because q is the exact quotient)
+    assert np.all(np.diff(y) >= 0)
+    # Eq. 6-8 integer chord: with q = floor(-x/s_inv), r = x + q s_inv (Eq. 6),
+    # y = floor((r/2 + s_inv) / 2^q) exactly (Eq. 7-8 on the integer grid).
+    q = (-x) // s_inv
+    r = x + q * s_inv
+    assert np.all((r > -s_inv) & (r <= 0))
+    live = q < 40
+    chord = (r[live] / 2.0 + s_inv) / np.exp2(q[live].astype(np.float64))
+    err = chord - y[live]
+    assert np.all(err >= 0) and np.all(err < 1)
+
+
+@pytest.mark.parametrize("s_inv", [251, 1420, 2293, 8030])
+def test_shift_exp2_vs_true_exponential(orc, s_inv):
+    # Eq. 5-8: s*y approximates 2^(s x) (here s := 1/s_inv exactly).  The linear
+    # fraction approximation 1 + t/2 of 2^t on t in (-1, 0] (Eq. 7) overestimates
+    # by at most max((1+t/2)/2^t) = 1.06148 at t = 2(1/(2 ln2) - 1); the floor
+    # loses < 1 unit of y.
+    s = 1.0 / s_inv
+    x = -np.arange(0, 12 * s_inv, 7, dtype=np.int64)
+    y = orc.shift_exp2_array(x, s_inv).astype(np.float64)
+    true = np.exp2(s * x)
+    ok = y >= 8
+    ratio = s * y[ok] / true[ok]
+    assert np.all(ratio <= 1.06149)
+    assert np.all(ratio >= 1.0 - 1.0 / y[ok] - 1e-12)
+    # the bound is attained near t = -0.5573 (Eq. 7's worst point)
+    assert ratio.max() > 1.06
+
+
+@pytest.mark.parametrize("s_inv", [251, 1420, 2293, 8030])
+def test_quotient_div_vs_paper_mulshift(orc, s_inv):
+    # eq:q_mulshift: M = round(s 2^N), q = (|x| M) >> N -- the
+    # paper's fast form of eq:q_div.  With N = 32 it agrees with the oracle's
+    # exact quotient within +-1 wherever the shift result matters (q < 32).
+    s = 1.0 / s_inv
+    M = int(math.floor(s * 2 ** 32 + 0.5))
+    for x in list(range(0, -32 * s_inv, -max(1, s_inv // 97))):
+        qd = orc.quotient_div(x, s_inv)
+        qm = ((-x) * M) >> 32
+        assert abs(qm - qd) <= 1
+
+
+# ----------------------------------------------------------- Eq. 14, step 11
+def test_scale_release_special_cases(orc):
+    s_inv = 1420
+    for x in [-(1 << 30), -12345, -1, 0, 1, 999, (1 << 30)]:
+        assert orc.scale_release(x, s_inv, s_inv) == x     # alpha = s_inv: identity
+        assert orc.scale_release(x, 0, s_inv) == 0         # alpha = 0
+    assert orc.scale_release(-1, 1, 2) == -1               # floor(-0.5) (R10)
+    assert orc.scale_release(5, 710, 1420) == 2            # floor(2.5)
+    assert orc.scale_release(-5, 710, 1420) == -3          # floor(-2.5)
+
+
+def test_normalize_worked_examples(orc):
+    # [254]/[2] -> 127; [-255]/[2] -> -128 (floor of -127.5)
+    assert orc.normalize(254, 2) == 127
+    assert orc.normalize(-255, 2) == -128
+    assert orc.normalize(-1, 3) == -1
+    assert orc.normalize(1000, 2) == 127     # R14 saturation
+    assert orc.normalize(-1000, 2) == -128
+
+
+# ----------------------------------------------------------- Alg. 1
+@pytest.mark.parametrize("N,d", [(1, 32), (5, 32), (17, 64), (49, 32), (64, 64), (130, 64), (33, 128)])
+@pytest.mark.parametrize("kind", ["uniform", "one_hot", "ties", "constant_rows", "all_min"])
+def test_untiled_matches_bruteforce(orc, N, d, kind):
+    # T_c = 1 (block_kv >= N): Algorithm 1 == untiled integer softmax attention
+    q, k, v = gen_int8_qkv(3, N, d, seed=N * 7 + d, kind=kind)
+    sq, sk = 0.055, 0.055
+    bkv = 256 if N <= 256 else N
+    out = orc.attention(q, k, v, sq, sk, block_kv=bkv)
+    ref, _, _ = untiled_attention(q, k, v, sq, sk)
+    assert np.array_equal(out, ref)
+
+
+def test_untiled_matches_bruteforce_real_workload(orc):
+    q, k, v = gen_workload("A7", 1, seed=4)
+    qq, sq = orc.quantize(q)
+    kq, sk = orc.quantize(k)
+    vq, _ = orc.quantize(v)
+    out = orc.attention(qq, kq, vq, sq, sk, block_kv=128)   # N = 49 -> T_c = 1
+    ref, _, _ = untiled_attention(qq, kq, vq, sq, sk)
+    assert np.array_equal(out, ref)
+
+
+def test_first_tile_max_rows_identical_to_untiled(orc):
+    # Rows whose global max lies in KV tile 1 see alpha = s_inv afterwards, so the
+    # release is the identity (R10) and they equal the untiled result bit-for-bit.
+    q, k, v = gen_workload("A1", 1, seed=5)
+    qq, sq = orc.quantize(q)
+    kq, sk = orc.quantize(k)
+    vq, _ = orc.quantize(v)
+    tiled = orc.attention(qq, kq, vq, sq, sk, block_kv=64)
+    untiled, _, _ = untiled_attention(qq, kq, vq, sq, sk)
+    S = np.einsum("pid,pjd->pij", qq.astype(np.int64), kq.astype(np.int64))
+    first = S[:, :, :64].max(-1) >= S.max(-1)
+    assert first.sum() > 50
+    assert np.array_equal(tiled[first], untiled[first])
+    # and tiling is not a no-op elsewhere (block_kv is part of the contract, R15)
+    assert not np.array_equal(tiled, untiled)
+
+
+def test_permutation_and_independence(orc):
+    q, k, v = gen_int8_qkv(4, 197, 64, seed=6)
+    sq, sk = 0.05, 0.05
+    base = orc.attention(q, k, v, sq, sk, block_kv=64)
+    perm = np.random.default_rng(0).permutation(197)
+    # query permutation: exact at any T_c (rows independent)
+    assert np.array_equal(orc.attention(q[:, perm], k, v, sq, sk, block_kv=64), base[:, perm])
+    # problem independence: batched == one by one
+    for p in range(4):
+        one = orc.attention(q[p:p + 1], k[p:p + 1], v[p:p + 1], sq, sk, block_kv=64)
+        assert np.array_equal(one[0], base[p])
+    # key permutation (with V): exact at T_c = 1
+    u = orc.attention(q, k, v, sq, sk, block_kv=256)
+    assert np.array_equal(orc.attention(q, k[:, perm], v[:, perm], sq, sk, block_kv=256), u)
+
+
+def test_max_invariance(orc):
+    # Adding a per-row constant to every score of the row (via channel 0:
+    # Q[i,0] = a_i, K[:,0] = b) leaves all max-subtracted terms unchanged.
+    q, k, v = gen_int8_qkv(2, 150, 64, seed=7)
+    sq, sk = 0.05, 0.05
+    q0, k0 = q.copy(), k.copy()
+    q0[:, :, 0] = 0
+    k0[:, :, 0] = 37
+    q1 = q0.copy()
+    q1[:, :, 0] = np.random.default_rng(1).integers(-128, 128, (2, 150))
+    for bkv in (64, 128, 256):
+        assert np.array_equal(orc.attention(q0, k0, v, sq, sk, block_kv=bkv),
+                              orc.attention(q1, k0, v, sq, sk, block_kv=bkv))
+
+
+def test_single_token_returns_v(orc):
+    q, k, v = gen_int8_qkv(5, 1, 64, seed=8)
+    assert np.array_equal(orc.attention(q, k, v, 0.05, 0.05), v)
+
+
+def test_constant_v(orc):
+    q, k, _ = gen_int8_qkv(2, 197, 64, seed=9)
+    row = np.random.default_rng(2).integers(-128, 128, 64).astype(np.int8)
+    v = np.broadcast_to(row, (2, 197, 64)).copy()
+    exact = orc.attention(q, k, v, 0.05, 0.05, block_kv=256)           # T_c = 1
+    assert np.array_equal(exact, np.broadcast_to(row, exact.shape))
+    tiled = orc.attention(q, k, v, 0.05, 0.05, block_kv=64)            # T_c = 4
+    assert np.abs(tiled.astype(int) - row.astype(int)).max() <= 1
+
+
+def test_block_r_and_threads_do_not_matter(orc):
+    q, k, v = gen_int8_qkv(6, 130, 32, seed=10)
+    base = orc.attention(q, k, v, 0.07, 0.07, block_kv=64)
+    for br in (1, 7, 64, 128, 1000):
+        assert np.array_equal(orc.attention(q, k, v, 0.07, 0.07, block_kv=64, block_r=br), base)
+    assert np.array_equal(orc.attention(q, k, v, 0.07, 0.07, block_kv=64, nthreads=4), base)
+
+
+def test_rows_entry_matches_full(orc):
+    q, k, v = gen_int8_qkv(3, 197, 64, seed=11)
+    full = orc.attention(q, k, v, 0.05, 0.05, block_kv=128)
+    for p, a, b in [(0, 0, 1), (1, 100, 197), (2, 127, 130)]:
+        assert np.array_equal(orc.attention_rows(q, k, v, 0.05, 0.05, p, a, b), full[p, a:b])
+
+
+def test_normaliser_bound(orc):
+    # At T_c = 1, l = sum_c P_c with P_c ~ 127 * s * y_c and s*y_c ~ 2^(s x_c)
+    # within [1, 1.0615] (Eq. 7): check l against the real-valued normaliser
+    # 127 * sum_c 2^(s (S_c - m)), allowing the floors (<= 1 unit per term) and
+    # the 9-bit multiplier (2^-8).
+    q, k, v = gen_workload("A1", 1, seed=12)
+    qq, sq = orc.quantize(q)
+    kq, sk = orc.quantize(k)
+    vq, _ = orc.quantize(v)
+    p = orc.derive_params(sq, sk, 64)
+    s = p["s"]
+    _, l_state, _ = orc.attention_rows_state(qq, kq, vq, sq, sk, 0, 0, 197, block_kv=256)
+    S = qq[0].astype(np.int64) @ kq[0].astype(np.int64).T
+    x = S - S.max(-1, keepdims=True)
+    real = 127.0 * np.exp2(s * x).sum(-1)
+    N = 197
+    ss = s * p["s_inv"]
+    assert np.all(l_state <= 1.0615 * (1 + 2 ** -8) * real * max(ss, 1 / ss) ** 30 + 1)
+    assert np.all(l_state >= (1 - 2 ** -8) * min(ss, 1 / ss) ** 30 * real - 2 * N)
+    assert l_state.min() >= 126   # the row max alone contributes ~127 (no zero denominator)
+
+
+# ----------------------------------------------------------- accuracy regime
+def _sqnr(orc, name, batch, seed, block_kv=128):
+    from oracle.fp_reference import attention_fp64, sqnr_db
+    q, k, v = gen_workload(name, batch, seed)
+    qq, sq = orc.quantize(q)
+    kq, sk = orc.quantize(k)
+    vq, sv = orc.quantize(v)
+    out = orc.attention(qq, kq, vq, sq, sk, block_kv=block_kv, nthreads=4)
+    return sqnr_db(attention_fp64(q, k, v), orc.dequantize(out, sv))
+
+
+@pytest.mark.parametrize("name", ["A1", "A7"])
+def test_sqnr_regime(orc, name):
+    # Table[SQNR]: QFlash 32.50 dB (A2) / 31.02 dB (A7), above I-ViT's
+    # 25.80 / 25.22.  Floor for synthetic inputs: mean >= 30 dB over
+    # seeds 0-9, each seed >= 29 dB.
+    vals = [_sqnr(orc, name, 1, seed) for seed in range(10)]
+    assert np.mean(vals) >= 30.0
+    assert min(vals) >= 29.0
+
+
+def test_sqnr_a2_b8(orc):
+    assert _sqnr(orc, "A2", 8, 0) >= 29.0
+
+
+def test_scale_release_vs_accumulation(orc):
+    # App. B.1: Scale Accumulation (Eq. 13) grows the accumulator's
+    # scale every tile and overflows; Scale Release (Eq. 14) stays bounded.
+    from oracle.fp_reference import attention_fp64, sqnr_db
+    q, k, v = gen_workload("L14", 1, seed=0)
+    q, k, v = q[:2, :513], k[:2, :513], v[:2, :513]
+    qq, sq = orc.quantize(q)
+    kq, sk = orc.quantize(k)
+    vq, sv = orc.quantize(v)
+    rel, ovf_rel = orc.attention(qq, kq, vq, sq, sk, block_kv=64, mode=0, return_overflow=True)
+    acc, ovf_acc = orc.attention(qq, kq, vq, sq, sk, block_kv=64, mode=1, return_overflow=True)
+    assert not ovf_rel and ovf_acc
+    assert sqnr_db(attention_fp64(q, k, v), orc.dequantize(rel, sv)) >= 25.8
+    # single tile: the two coincide (nothing is accumulated across tiles)
+    a1 = orc.attention(qq, kq, vq, sq, sk, block_kv=1024, mode=0)
+    b1 = orc.attention(qq, kq, vq, sq, sk, block_kv=1024, mode=1)
+    assert np.abs(a1.astype(int) - b1.astype(int)).max() <= 1
