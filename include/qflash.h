@@ -1,0 +1,179 @@
+/*
+ * qflash.h -- C ABI of libqflash.so: the B200 (sm_100a) hot path of QFlash,
+ * integer-only fused attention (arxiv 2604.25306).
+ *
+ * Citations: "P:Lnnn" = line of the paper source; Eq./Alg. numbers are the
+ * paper's; R# = a reading of an ambiguous passage.
+ *
+ * Conventions for every entry point
+ *  - Memory: all tensors are DEVICE pointers on the current CUDA device unless a
+ *    parameter says "host".  The caller owns every buffer; the library never
+ *    allocates persistent device memory and keeps no mutable global state except
+ *    a thread-local error string and per-device one-time setup (kernel
+ *    attributes).  Layout: [P, N, d] int8 row-major, contiguous, 16-byte aligned.
+ *  - Streams: work is enqueued on `stream` (cudaStream_t; NULL = legacy default
+ *    stream) and is asynchronous unless a host output pointer is given.
+ *  - Errors: arguments are validated before anything is enqueued; on error
+ *    nothing is written.  CUDA failures return QFLASH_ERR_CUDA with details in
+ *    qflash_last_error().  The functions never throw and never call exit().
+ *  - Determinism: integer outputs are bit-identical across runs and equal to
+ *    the CPU oracle (oracle/qflash_oracle.c) for the same inputs.
+ */
+#ifndef QFLASH_H_
+#define QFLASH_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define QFLASH_API __attribute__((visibility("default")))
+#else
+#define QFLASH_API
+#endif
+
+typedef struct CUstream_st* qflash_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  QFLASH_OK = 0,
+  QFLASH_ERR_INVALID_ARGUMENT = 1,  /* null pointer, negative size, bad dtype, aliasing   */
+  QFLASH_ERR_UNSUPPORTED_SHAPE = 2, /* d not in {32,64,128}; N<1 or N>65536; P<1;
+                                       block_kv not in {0,64,128,256}                       */
+  QFLASH_ERR_SCALE_RANGE = 3,       /* scale <= 0 or non-finite, or
+                                       s = s_q*s_k*log2(e)/sqrt(d) outside [2^-24, 0.5]     */
+  QFLASH_ERR_CUDA = 4,              /* CUDA runtime/driver error (see qflash_last_error)    */
+  QFLASH_ERR_UNSUPPORTED_DEVICE = 5 /* current device is not compute capability 10.0       */
+} qflash_status;
+
+typedef enum { QFLASH_F32 = 0, QFLASH_BF16 = 1, QFLASH_F16 = 2 } qflash_dtype;
+
+/* --------------------------------------------------------------------------
+ * Eq. 2: per-tensor symmetric int8 quantization, dynamic scale
+ * (computed on the fly).
+ *   s   = fl32(max|x| / 127)   (all-zero tensor: s = 1/127, R3)
+ *   x^  = sat8(roundf(fl32(x / s)))   round half away from zero (R1), IEEE fp32
+ *         division (R2); bf16/f16 inputs are widened exactly to fp32.
+ * x: device, numel elements of `dtype`, contiguous.  x_q: device int8[numel].
+ * scale_dev: device float* receiving s (may be NULL).  scale_host: host float*
+ * receiving s (may be NULL; if set the call synchronizes `stream`).  At least
+ * one scale pointer is required.  numel == 0 gives s = 1/127.  A non-finite
+ * input yields a non-finite s (rejected later by qflash_attention_int8).
+ * ------------------------------------------------------------------------ */
+QFLASH_API qflash_status qflash_quantize_per_tensor(const void* x, qflash_dtype dtype, int64_t numel,
+                                         int8_t* x_q, float* scale_dev, float* scale_host,
+                                         qflash_stream_t stream);
+
+/* Fused Q/K/V variant: three tensors of identical dtype and numel quantized in
+ * one amax launch and one quantize launch.  scales_dev: device float[3]
+ * receiving (s_q, s_k, s_v), required.  Same semantics per tensor as above. */
+QFLASH_API qflash_status qflash_quantize_qkv(const void* q, const void* k, const void* v, qflash_dtype dtype,
+                                  int64_t numel, int8_t* q_q, int8_t* k_q, int8_t* v_q,
+                                  float* scales_dev, qflash_stream_t stream);
+
+typedef struct {
+  int32_t num_problems; /* P = batch * windows * heads (windows folded into batch)   */
+  int32_t seq_len;      /* N, 1..65536                                               */
+  int32_t head_dim;     /* d in {32, 64, 128}                                        */
+  int32_t block_kv;     /* B_c in {64, 128, 256}; 0 -> 128.  PART OF THE NUMERICAL
+                           CONTRACT: the tiled result depends on B_c (R15).          */
+} qflash_attn_shape;
+
+/* Kernel selection (tests / ablation).  AUTO picks the Swin-packed kernel when
+ * N <= 64 and the generic tiled kernel otherwise; both give identical bytes. */
+typedef enum {
+  QFLASH_VARIANT_AUTO = 0,
+  QFLASH_VARIANT_GENERIC = 1,
+  QFLASH_VARIANT_PACKED = 2 /* requires N <= 64 */
+} qflash_variant;
+
+/* --------------------------------------------------------------------------
+ * Algorithm 1: QFlash integer-only fused attention forward.
+ * q, k, v: device int8 [P, N, d] (Q^, K^, V^ of Eq. 2, per-tensor scales s_q,
+ * s_k, s_v given on the host).  o: device int8 [P, N, d], must not alias
+ * q/k/v.  s_o: host float* receiving s_O = s_V, may be NULL.
+ * Per problem and query row (all integer):
+ *   S = Q K_j^T (int32, Eq. 3); m' = max(m, rowmax S) (Eq. 4);
+ *   alpha = ShiftExp2(m - m') and P~ = ShiftExp2(S - m') (Alg. 2, Eq. 5-8,
+ *   exact quotient R6); P = min(127, (P~ M_P) >> r_P) (Eq. 9-10, s_P = 1/127);
+ *   l = floor(l alpha / s_inv) + rowsum P; O = floor(O alpha / s_inv) + P V_j
+ *   (ScaleRelease, Eq. 14 / P:L408); out = sat8(floor(O / l)) (step 11).
+ * Asynchronous on `stream`; no allocation, no host synchronization.
+ * ------------------------------------------------------------------------ */
+QFLASH_API qflash_status qflash_attention_int8(const int8_t* q, const int8_t* k, const int8_t* v, float s_q,
+                                    float s_k, float s_v, const qflash_attn_shape* shape,
+                                    int8_t* o, float* s_o, qflash_stream_t stream);
+
+/* Same as qflash_attention_int8 with an explicit kernel variant. */
+QFLASH_API qflash_status qflash_attention_int8_ex(const int8_t* q, const int8_t* k, const int8_t* v,
+                                       float s_q, float s_k, float s_v,
+                                       const qflash_attn_shape* shape, qflash_variant variant,
+                                       int8_t* o, float* s_o, qflash_stream_t stream);
+
+/* Device-scale variant for fully asynchronous pipelines (dynamic quantization,
+ * P:L703): scales_dev = device float[3] holding (s_q, s_k, s_v), e.g. as written
+ * by qflash_quantize_qkv.  A one-thread kernel derives the integer constants on
+ * the device with the same fp64 expression (no FMA contraction) as
+ * qflash_derive_params and stores them in workspace_dev (caller-owned device
+ * memory of QFLASH_DSCALE_WORKSPACE_BYTES bytes, 16-byte aligned); the
+ * attention kernel reads them there.  No host synchronization.  If the scales
+ * are out of range nothing is written to o and the int32 at workspace_dev[0]
+ * holds QFLASH_ERR_SCALE_RANGE (QFLASH_OK otherwise).  s_O = s_V stays in
+ * scales_dev[2]. */
+#define QFLASH_DSCALE_WORKSPACE_BYTES 128
+QFLASH_API qflash_status qflash_attention_int8_dscale(const int8_t* q, const int8_t* k, const int8_t* v,
+                                           const float* scales_dev,
+                                           const qflash_attn_shape* shape, qflash_variant variant,
+                                           int8_t* o, void* workspace_dev,
+                                           qflash_stream_t stream);
+
+/* Inverse of Eq. 2: y = fl32(scale * (float)x^).  x_q device int8[numel],
+ * y device float[numel]. */
+QFLASH_API qflash_status qflash_dequantize(const int8_t* x_q, float scale, int64_t numel, float* y,
+                                qflash_stream_t stream);
+/* Same with the scale read from device memory (scale_dev: device float*). */
+QFLASH_API qflash_status qflash_dequantize_dscale(const int8_t* x_q, const float* scale_dev, int64_t numel,
+                                       float* y, qflash_stream_t stream);
+
+/* --------------------------------------------------------------------------
+ * Pure host helpers (no CUDA calls; usable without a GPU).
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  double s;           /* s = s_q s_k d^(-1/2) log2(e)  */
+  int32_t s_inv;      /* round(1/s)  */
+  int32_t n;          /* floor(log2(127 s))                              (Eq. 9)   */
+  int32_t r_p;        /* 8 - n                                           (Eq. 9)   */
+  int32_t m_p;        /* round(127 s 2^r_p)                              (Eq. 10)  */
+  /* realisation constants of the kernel (division-free, exact):            */
+  uint32_t q_magic;   /* floor(t / s_inv) == umulhi(t, q_magic) >> q_shift          */
+  int32_t q_shift;    /*   for every t the kernel can produce (t < 2^25)            */
+  uint32_t p_mul;     /* floor(y M_P / 2^r_P) == umulhi(y << p_pre, p_mul)          */
+  int32_t p_pre;
+  int32_t p_max;      /* floor(s_inv M_P / 2^r_P): largest P before the 127 clamp  */
+  uint64_t rel_magic; /* floor(n / s_inv) == umul64hi(n, rel_magic) >> rel_shift    */
+  int32_t rel_shift;  /*   for n < 2^56 (ScaleRelease per-row constant)            */
+} qflash_int_params;
+
+/* Derive every constant of one attention call from the host scales.
+ * Returns QFLASH_ERR_SCALE_RANGE / UNSUPPORTED_SHAPE / INVALID_ARGUMENT. */
+QFLASH_API qflash_status qflash_derive_params(float s_q, float s_k, int32_t head_dim,
+                                   qflash_int_params* out);
+
+/* Contiguous split of P independent problems over `world` ranks:
+ * rank r gets [floor(r P / world), floor((r+1) P / world)).  Invalid input
+ * (P < 0, world < 1, rank outside [0, world)) yields begin = count = 0. */
+QFLASH_API void qflash_partition(int32_t num_problems, int32_t world, int32_t rank, int32_t* begin,
+                      int32_t* count);
+
+QFLASH_API const char* qflash_status_string(qflash_status status);
+QFLASH_API const char* qflash_last_error(void); /* thread-local detail of the last failure */
+
+/* Library/ABI version: (major << 16) | minor. */
+QFLASH_API int32_t qflash_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QFLASH_H_ */

@@ -1,0 +1,165 @@
+"""Python API over libqflash.so -- same names as the C ABI, torch tensors in/out.
+
+PyTorch supplies device memory and the current CUDA stream only; every step of
+the QFlash hot path (quantize, fused integer attention, dequantize) runs in the
+library's sm_100a kernels.  There is no CPU or eager-PyTorch fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import AttnShape, IntParams, check, lib
+
+_DTYPES = {torch.float32: _lib.QFLASH_F32, torch.bfloat16: _lib.QFLASH_BF16,
+           torch.float16: _lib.QFLASH_F16}
+
+
+def _stream(stream=None) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev_ptr(t: torch.Tensor) -> ctypes.c_void_p:
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+# ---------------------------------------------------------------- quantizer
+def qflash_quantize_per_tensor(x: torch.Tensor, out: torch.Tensor | None = None,
+                               scale_out: torch.Tensor | None = None, stream=None):
+    """Eq. 2 per-tensor int8 quantization.  Returns (x_q int8, scale float32[1] on device)."""
+    if x.dtype not in _DTYPES:
+        raise TypeError(x.dtype)
+    out = torch.empty(x.shape, dtype=torch.int8, device=x.device) if out is None else out
+    scale_out = torch.empty(1, dtype=torch.float32, device=x.device) if scale_out is None else scale_out
+    check(lib().qflash_quantize_per_tensor(_dev_ptr(x), _DTYPES[x.dtype], x.numel(), _dev_ptr(out),
+                                           _dev_ptr(scale_out), None, _stream(stream)))
+    return out, scale_out
+
+
+def qflash_quantize_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, outs=None,
+                        scales: torch.Tensor | None = None, stream=None):
+    """Fused Q/K/V quantization.  Returns (q_q, k_q, v_q, scales float32[3] on device)."""
+    assert q.shape == k.shape == v.shape and q.dtype == k.dtype == v.dtype
+    if outs is None:
+        outs = [torch.empty(q.shape, dtype=torch.int8, device=q.device) for _ in range(3)]
+    scales = torch.empty(3, dtype=torch.float32, device=q.device) if scales is None else scales
+    check(lib().qflash_quantize_qkv(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v), _DTYPES[q.dtype],
+                                    q.numel(), _dev_ptr(outs[0]), _dev_ptr(outs[1]),
+                                    _dev_ptr(outs[2]), _dev_ptr(scales), _stream(stream)))
+    return outs[0], outs[1], outs[2], scales
+
+
+# ---------------------------------------------------------------- attention
+def _shape(q: torch.Tensor, block_kv: int) -> AttnShape:
+    if q.dim() != 3:
+        raise ValueError("expected [P, N, d] tensors")
+    P, N, d = q.shape
+    return AttnShape(P, N, d, block_kv)
+
+
+def qflash_attention_int8(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, s_q: float,
+                          s_k: float, s_v: float, block_kv: int = 128, variant: str = "auto",
+                          out: torch.Tensor | None = None, stream=None):
+    """Algorithm 1 (integer-only fused attention).  int8 [P, N, d] in, (int8 out, s_O) back."""
+    for t in (q, k, v):
+        if t.dtype != torch.int8:
+            raise TypeError("q, k, v must be int8")
+    out = torch.empty_like(q) if out is None else out
+    shape = _shape(q, block_kv)
+    s_o = ctypes.c_float(0.0)
+    check(lib().qflash_attention_int8_ex(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v), s_q, s_k, s_v,
+                                         ctypes.byref(shape), _lib.VARIANTS[variant],
+                                         _dev_ptr(out), ctypes.byref(s_o), _stream(stream)))
+    return out, float(s_o.value)
+
+
+def qflash_attention_int8_dscale(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                                 scales: torch.Tensor, block_kv: int = 128, variant: str = "auto",
+                                 out: torch.Tensor | None = None,
+                                 workspace: torch.Tensor | None = None, stream=None):
+    """Device-scale attention: scales = device float32[3] (s_q, s_k, s_v); no host sync.
+    Returns (out int8, workspace) -- workspace[0] (int32) holds the status."""
+    out = torch.empty_like(q) if out is None else out
+    if workspace is None:
+        workspace = torch.empty(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=q.device)
+    shape = _shape(q, block_kv)
+    check(lib().qflash_attention_int8_dscale(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v),
+                                             _dev_ptr(scales), ctypes.byref(shape),
+                                             _lib.VARIANTS[variant], _dev_ptr(out),
+                                             _dev_ptr(workspace), _stream(stream)))
+    return out, workspace
+
+
+# ---------------------------------------------------------------- dequantizer
+def qflash_dequantize(x_q: torch.Tensor, scale, out: torch.Tensor | None = None, stream=None):
+    """y = scale * x^ in fp32.  `scale` is a python float or a device float32 tensor."""
+    out = torch.empty(x_q.shape, dtype=torch.float32, device=x_q.device) if out is None else out
+    if isinstance(scale, torch.Tensor):
+        check(lib().qflash_dequantize_dscale(_dev_ptr(x_q), _dev_ptr(scale), x_q.numel(),
+                                             _dev_ptr(out), _stream(stream)))
+    else:
+        check(lib().qflash_dequantize(_dev_ptr(x_q), float(scale), x_q.numel(), _dev_ptr(out),
+                                      _stream(stream)))
+    return out
+
+
+# ---------------------------------------------------------------- pipeline
+class QFlashPipeline:
+    """The whole hot path for one [P, N, d] workload with preallocated buffers:
+    fused Q/K/V quantization -> device-scale integer attention -> dequantization.
+    Four of the library's kernels per call, no host synchronization."""
+
+    def __init__(self, P: int, N: int, d: int, block_kv: int = 128, device="cuda",
+                 variant: str = "auto"):
+        self.shape = (P, N, d)
+        self.block_kv = block_kv
+        self.variant = variant
+        dev = torch.device(device)
+        self.qkv_q = [torch.empty(self.shape, dtype=torch.int8, device=dev) for _ in range(3)]
+        self.scales = torch.empty(3, dtype=torch.float32, device=dev)
+        self.o_q = torch.empty(self.shape, dtype=torch.int8, device=dev)
+        self.workspace = torch.empty(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=dev)
+        self.out = torch.empty(self.shape, dtype=torch.float32, device=dev)
+
+    def __call__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, stream=None):
+        qflash_quantize_qkv(q, k, v, outs=self.qkv_q, scales=self.scales, stream=stream)
+        qflash_attention_int8_dscale(self.qkv_q[0], self.qkv_q[1], self.qkv_q[2], self.scales,
+                                     self.block_kv, self.variant, out=self.o_q,
+                                     workspace=self.workspace, stream=stream)
+        qflash_dequantize(self.o_q, self.scales[2:3], out=self.out, stream=stream)
+        return self.out
+
+
+def qflash_forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, block_kv: int = 128):
+    """End-to-end QFlash attention on real inputs [P, N, d] (fp32/bf16/f16).
+    Host tensors are copied to the current device and the fp32 result copied back."""
+    host = not q.is_cuda
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if host:
+        q, k, v = (t.to(dev, non_blocking=True) for t in (q, k, v))
+    pipe = QFlashPipeline(*q.shape, block_kv=block_kv, device=dev)
+    out = pipe(q.contiguous(), k.contiguous(), v.contiguous())
+    status = int(pipe.workspace[0].item())
+    if status != _lib.QFLASH_OK:
+        raise _lib.QFlashError(status, "device-derived scales out of range")
+    return out.cpu() if host else out
+
+
+# ---------------------------------------------------------------- host helpers
+def qflash_derive_params(s_q: float, s_k: float, head_dim: int) -> dict:
+    p = IntParams()
+    check(lib().qflash_derive_params(s_q, s_k, head_dim, ctypes.byref(p)))
+    return {name: getattr(p, name) for name, _ in IntParams._fields_}
+
+
+def qflash_partition(num_problems: int, world: int, rank: int):
+    b, c = ctypes.c_int32(), ctypes.c_int32()
+    lib().qflash_partition(num_problems, world, rank, ctypes.byref(b), ctypes.byref(c))
+    return b.value, c.value

@@ -1,0 +1,47 @@
+// qflash_common.cuh -- structures shared by the host library and the kernels of
+// libqflash.so (NOT shared with the oracle).
+#pragma once
+#include <cstdint>
+
+namespace qf {
+
+// Per-launch integer constants of Algorithm 1 as the kernel consumes them.
+struct IntParams {
+  int32_t status;     // 0 = OK (device-derived path may report a range error)
+  int32_t s_inv;      // round(1/s)                               (Alg. 2)
+  uint32_t q_magic;   // q1 = umulhi(t, q_magic) >> q_shift == floor(t / s_inv)
+  int32_t q_shift;
+  uint32_t p_mul;     // P = umulhi(y << p_pre, p_mul) == floor(y M_P / 2^r_P)
+  int32_t p_pre;
+  uint32_t rel_magic_lo;  // floor(n / s_inv) == umul64hi(n, rel_magic) >> rel_shift
+  uint32_t rel_magic_hi;
+  int32_t rel_shift;
+  int32_t p_max;
+  int32_t r_p, m_p, n;
+  int32_t pad[3];
+  double s;
+};
+static_assert(sizeof(IntParams) == 72, "IntParams layout");
+
+struct AttnArgs {
+  int32_t N;        // sequence length
+  int32_t P;        // number of problems
+  int32_t Tc;       // ceil(N / B_c) KV tiles (generic kernel)
+  int32_t pad0;
+  IntParams prm;    // used when dev_prm == nullptr
+  const IntParams* dev_prm;  // device-derived constants (dscale path) or nullptr
+  int8_t* out;
+  // bring-up dumps for CTA (problem 0, tile 0) only; nullptr in production:
+  int32_t* dbg_s;  // [128][BC] raw S of KV tile 0
+  int32_t* dbg_p;  // [128][BC/4] packed P words of KV tile 0
+  int32_t* dbg_o;  // [128][D+1] final O and l before normalization
+};
+
+// Up to three tensors quantized by one launch pair (Q/K/V fusion).
+struct QuantTensors {
+  const void* x[3];
+  int8_t* xq[3];
+  float* scale[3];
+};
+
+}  // namespace qf

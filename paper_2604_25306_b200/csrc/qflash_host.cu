@@ -1,0 +1,534 @@
+// qflash_host.cu -- the C ABI of libqflash.so (include/qflash.h): argument
+// validation, derivation of the integer constants (host fp64, or on the device
+// for the dscale path), TMA descriptor encoding and kernel launches.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/qflash.h"
+#include "../../include/qflash_debug.h"
+#include "qflash_common.cuh"
+
+namespace qf {
+cudaError_t launch_attention(int D, int BC, bool packed, const CUtensorMap& tq,
+                             const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& args,
+                             dim3 grid, cudaStream_t stream);
+cudaError_t launch_quantize(const QuantTensors& t, int ntensors, int dtype, int64_t numel,
+                            cudaStream_t stream);
+cudaError_t launch_dequantize(const int8_t* xq, float scale, const float* scale_dev,
+                              int64_t numel, float* y, cudaStream_t stream);
+}  // namespace qf
+
+namespace {
+
+constexpr int32_t kVersion = (1 << 16) | 0;
+thread_local char g_err[512] = "";
+
+void set_err(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+qflash_status fail(qflash_status st, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return st;
+}
+
+qflash_status cuda_fail(cudaError_t e, const char* where) {
+  set_err("%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+  return QFLASH_ERR_CUDA;
+}
+
+// ------------------------------------------------------------------------
+// Constant derivation, shared by the host path and the one-thread device
+// kernel.  fp64 operations are written with explicit round-to-nearest
+// intrinsics on the device (no FMA contraction) and plain operators on the
+// host (compiled with -ffp-contract=off), so both evaluate the identical IEEE
+// expression ((s_q * s_k) * log2e) / sqrt(d) of Alg. 1.
+__host__ __device__ inline double dmul(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dmul_rn(a, b);
+#else
+  return a * b;
+#endif
+}
+__host__ __device__ inline double ddiv(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __ddiv_rn(a, b);
+#else
+  return a / b;
+#endif
+}
+__host__ __device__ inline double dsqrt(double a) {
+#ifdef __CUDA_ARCH__
+  return __dsqrt_rn(a);
+#else
+  return std::sqrt(a);
+#endif
+}
+
+using u128 = unsigned __int128;
+
+// smallest L with 2^L >= x (x >= 1)
+__host__ __device__ inline int ceil_log2(uint64_t x) {
+  int L = 0;
+  while ((uint64_t(1) << L) < x) ++L;
+  return L;
+}
+
+__host__ __device__ inline int derive_core(float s_q, float s_k, int32_t d, qf::IntParams* o,
+                                           qflash_int_params* pub) {
+  if (!(s_q > 0.0f) || !(s_k > 0.0f) || !isfinite(s_q) || !isfinite(s_k))
+    return QFLASH_ERR_SCALE_RANGE;
+  const double log2e = 1.4426950408889634;
+  const double s = ddiv(dmul(dmul(static_cast<double>(s_q), static_cast<double>(s_k)), log2e),
+                        dsqrt(static_cast<double>(d)));
+  if (!(s >= ldexp(1.0, -24)) || !(s <= 0.5)) return QFLASH_ERR_SCALE_RANGE;
+  const int64_t s_inv = llround(ddiv(1.0, s));  // round half away (R1)
+  const double ratio = dmul(s, 127.0);          // s / s_P, s_P = 1/127 (R8)
+  int e = 0;
+  (void)frexp(ratio, &e);
+  const int32_t n = e - 1;                      // floor(log2 ratio)   (Eq. 9)
+  const int32_t r_p = 8 - n;                    // r = b - n           (Eq. 9)
+  const int64_t m_p = llround(ldexp(ratio, r_p));  // round(ratio 2^r) (Eq. 10)
+
+  const uint64_t D = static_cast<uint64_t>(s_inv);
+  // q1 = floor(t / s_inv) for t < 2^25 (t = m - S + s_inv, the kernel's range).
+  uint32_t q_magic;
+  int32_t q_shift;
+  {
+    const uint64_t m = ((uint64_t(1) << 32) + D - 1) / D;
+    const uint64_t err = m * D - (uint64_t(1) << 32);
+    // fast form: exact for t < 27 s_inv (q1 <= 26); beyond, the estimate is
+    // >= the true quotient (>= 26) and the shifted value is < 2^26, so y = 0
+    // exactly as in the oracle.
+    if (D <= (uint64_t(1) << 22) && (27 * D) * err < (uint64_t(1) << 32)) {
+      q_magic = static_cast<uint32_t>(m);
+      q_shift = 0;
+    } else {
+      const int L = ceil_log2(D);
+      const int sh = L > 7 ? L - 7 : 0;
+      const u128 num = (u128(1) << (32 + sh));
+      const u128 mm = (num + D - 1) / D;
+      q_magic = static_cast<uint32_t>(mm);
+      q_shift = sh;
+    }
+  }
+  // P = floor(y M_P / 2^r_P) = umulhi(y << p_pre, p_mul)
+  const int32_t p_pre = r_p < 10 ? 10 - r_p : 0;
+  const uint64_t p_mul = static_cast<uint64_t>(m_p) << (32 - r_p - p_pre);
+  const int64_t p_max = (s_inv * m_p) >> r_p;
+  // release: floor(n / s_inv) for n < 2^56
+  uint64_t rel_magic;
+  int32_t rel_shift;
+  {
+    const int L = ceil_log2(D);
+    const int sh = L > 8 ? L - 8 : 0;
+    const u128 num = (u128(1) << (64 + sh));
+    rel_magic = static_cast<uint64_t>((num + D - 1) / D);
+    rel_shift = sh;
+  }
+  if (o) {
+    o->status = 0;
+    o->s_inv = static_cast<int32_t>(s_inv);
+    o->q_magic = q_magic;
+    o->q_shift = q_shift;
+    o->p_mul = static_cast<uint32_t>(p_mul);
+    o->p_pre = p_pre;
+    o->rel_magic_lo = static_cast<uint32_t>(rel_magic);
+    o->rel_magic_hi = static_cast<uint32_t>(rel_magic >> 32);
+    o->rel_shift = rel_shift;
+    o->p_max = static_cast<int32_t>(p_max);
+    o->r_p = r_p;
+    o->m_p = static_cast<int32_t>(m_p);
+    o->n = n;
+    o->pad[0] = o->pad[1] = o->pad[2] = 0;
+    o->s = s;
+  }
+  if (pub) {
+    pub->s = s;
+    pub->s_inv = static_cast<int32_t>(s_inv);
+    pub->n = n;
+    pub->r_p = r_p;
+    pub->m_p = static_cast<int32_t>(m_p);
+    pub->q_magic = q_magic;
+    pub->q_shift = q_shift;
+    pub->p_mul = static_cast<uint32_t>(p_mul);
+    pub->p_pre = p_pre;
+    pub->p_max = static_cast<int32_t>(p_max);
+    pub->rel_magic = rel_magic;
+    pub->rel_shift = rel_shift;
+  }
+  return QFLASH_OK;
+}
+
+__global__ void derive_params_kernel(const float* __restrict__ scales, int32_t d,
+                                     qf::IntParams* __restrict__ out) {
+  qf::IntParams p;
+  const int st = derive_core(scales[0], scales[1], d, &p, nullptr);
+  if (st != QFLASH_OK) {
+    memset(&p, 0, sizeof(p));
+    p.status = st;
+  }
+  *out = p;
+}
+
+// ------------------------------------------------------------------------
+// Device capability check (sm_100 only), cached per device ordinal.
+qflash_status check_device(int* dev_out) {
+  int dev = -1;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  static int cached[64];  // 0 unknown, 1 ok, 2 bad
+  if (dev >= 0 && dev < 64 && cached[dev] == 1) {
+    *dev_out = dev;
+    return QFLASH_OK;
+  }
+  int major = 0, minor = 0;
+  e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+  e = cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+  if (!(major == 10 && minor == 0))
+    return fail(QFLASH_ERR_UNSUPPORTED_DEVICE, "device %d is sm_%d%d; libqflash is built for sm_100a",
+                dev, major, minor);
+  if (dev >= 0 && dev < 64) cached[dev] = 1;
+  *dev_out = dev;
+  return QFLASH_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D int8 tensor map over [P][N][d] with box {d, rows, probs}.
+qflash_status make_tmap(CUtensorMap* m, const int8_t* base, int P, int N, int d, int rows,
+                        int probs) {
+  auto enc = get_encode_fn();
+  if (!enc) return fail(QFLASH_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(N),
+                        static_cast<cuuint64_t>(P)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(N) * d};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(d), static_cast<cuuint32_t>(rows),
+                       static_cast<cuuint32_t>(probs)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const CUtensorMapSwizzle sw = d == 32   ? CU_TENSOR_MAP_SWIZZLE_32B
+                                : d == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                          : CU_TENSOR_MAP_SWIZZLE_128B;
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(QFLASH_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", static_cast<int>(r));
+  return QFLASH_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bool overlaps(const void* a, int64_t na, const void* b, int64_t nb) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
+  return a0 < b0 + static_cast<uintptr_t>(nb) && b0 < a0 + static_cast<uintptr_t>(na);
+}
+
+qflash_status validate_shape(const qflash_attn_shape* shape, int* bc_out) {
+  if (!shape) return fail(QFLASH_ERR_INVALID_ARGUMENT, "shape is NULL");
+  const int P = shape->num_problems, N = shape->seq_len, d = shape->head_dim;
+  const int bc = shape->block_kv == 0 ? 128 : shape->block_kv;
+  if (P < 1) return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "num_problems %d < 1", P);
+  if (N < 1 || N > 65536) return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "seq_len %d not in [1, 65536]", N);
+  if (d != 32 && d != 64 && d != 128)
+    return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "head_dim %d not in {32, 64, 128}", d);
+  if (bc != 64 && bc != 128 && bc != 256)
+    return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "block_kv %d not in {64, 128, 256}", shape->block_kv);
+  *bc_out = bc;
+  return QFLASH_OK;
+}
+
+qflash_status validate_qkvo(const int8_t* q, const int8_t* k, const int8_t* v, const int8_t* o,
+                            int64_t bytes) {
+  if (!q || !k || !v || !o) return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL tensor pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "tensor pointers must be 16-byte aligned");
+  if (overlaps(o, bytes, q, bytes) || overlaps(o, bytes, k, bytes) || overlaps(o, bytes, v, bytes))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "output o aliases q/k/v");
+  return QFLASH_OK;
+}
+
+qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
+                            const qflash_attn_shape* shape, int bc, qflash_variant variant,
+                            int8_t* o, const qf::IntParams* host_prm,
+                            const qf::IntParams* dev_prm, cudaStream_t stream,
+                            int32_t* dbg_s = nullptr, int32_t* dbg_p = nullptr,
+                            int32_t* dbg_o = nullptr) {
+  const int P = shape->num_problems, N = shape->seq_len, d = shape->head_dim;
+  bool packed;
+  switch (variant) {
+    case QFLASH_VARIANT_AUTO: packed = (N <= 64); break;
+    case QFLASH_VARIANT_GENERIC: packed = false; break;
+    case QFLASH_VARIANT_PACKED:
+      if (N > 64) return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "packed variant needs seq_len <= 64");
+      packed = true;
+      break;
+    default: return fail(QFLASH_ERR_INVALID_ARGUMENT, "unknown variant %d", static_cast<int>(variant));
+  }
+  CUtensorMap tq, tk, tv;
+  const int rows = packed ? 64 : 128;
+  const int probs = packed ? 2 : 1;
+  const int kv_rows = packed ? 64 : bc;
+  qflash_status st;
+  if ((st = make_tmap(&tq, q, P, N, d, rows, probs)) != QFLASH_OK) return st;
+  if ((st = make_tmap(&tk, k, P, N, d, kv_rows, probs)) != QFLASH_OK) return st;
+  if ((st = make_tmap(&tv, v, P, N, d, kv_rows, probs)) != QFLASH_OK) return st;
+  qf::AttnArgs args;
+  memset(&args, 0, sizeof(args));
+  args.N = N;
+  args.P = P;
+  args.Tc = (N + bc - 1) / bc;
+  if (host_prm) args.prm = *host_prm;
+  args.dev_prm = dev_prm;
+  args.out = o;
+  args.dbg_s = dbg_s;
+  args.dbg_p = dbg_p;
+  args.dbg_o = dbg_o;
+  dim3 grid = packed ? dim3((P + 1) / 2, 1, 1) : dim3(P, (N + 127) / 128, 1);
+  cudaError_t e = qf::launch_attention(d, packed ? 128 : bc, packed, tq, tk, tv, args, grid, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "attention launch");
+  return QFLASH_OK;
+}
+
+qflash_status attention_host_scales(const int8_t* q, const int8_t* k, const int8_t* v, float s_q,
+                                    float s_k, float s_v, const qflash_attn_shape* shape,
+                                    qflash_variant variant, int8_t* o, float* s_o,
+                                    cudaStream_t stream) {
+  int bc = 0;
+  qflash_status st = validate_shape(shape, &bc);
+  if (st != QFLASH_OK) return st;
+  const int64_t bytes = static_cast<int64_t>(shape->num_problems) * shape->seq_len * shape->head_dim;
+  if ((st = validate_qkvo(q, k, v, o, bytes)) != QFLASH_OK) return st;
+  if (!(s_v > 0.0f) || !std::isfinite(s_v))
+    return fail(QFLASH_ERR_SCALE_RANGE, "s_v must be positive and finite");
+  qf::IntParams prm;
+  const int rc = derive_core(s_q, s_k, shape->head_dim, &prm, nullptr);
+  if (rc != QFLASH_OK)
+    return fail(static_cast<qflash_status>(rc),
+                "s = s_q s_k log2(e)/sqrt(d) outside [2^-24, 0.5] (s_q=%g, s_k=%g, d=%d)",
+                static_cast<double>(s_q), static_cast<double>(s_k), shape->head_dim);
+  int dev = 0;
+  if ((st = check_device(&dev)) != QFLASH_OK) return st;
+  if ((st = launch_common(q, k, v, shape, bc, variant, o, &prm, nullptr, stream)) != QFLASH_OK)
+    return st;
+  if (s_o) *s_o = s_v;  // s_O = s_V
+  return QFLASH_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+int32_t qflash_version(void) { return kVersion; }
+
+const char* qflash_status_string(qflash_status s) {
+  switch (s) {
+    case QFLASH_OK: return "QFLASH_OK";
+    case QFLASH_ERR_INVALID_ARGUMENT: return "QFLASH_ERR_INVALID_ARGUMENT";
+    case QFLASH_ERR_UNSUPPORTED_SHAPE: return "QFLASH_ERR_UNSUPPORTED_SHAPE";
+    case QFLASH_ERR_SCALE_RANGE: return "QFLASH_ERR_SCALE_RANGE";
+    case QFLASH_ERR_CUDA: return "QFLASH_ERR_CUDA";
+    case QFLASH_ERR_UNSUPPORTED_DEVICE: return "QFLASH_ERR_UNSUPPORTED_DEVICE";
+  }
+  return "QFLASH_ERR_UNKNOWN";
+}
+
+const char* qflash_last_error(void) { return g_err; }
+
+qflash_status qflash_derive_params(float s_q, float s_k, int32_t head_dim, qflash_int_params* out) {
+  if (!out) return fail(QFLASH_ERR_INVALID_ARGUMENT, "out is NULL");
+  if (head_dim != 32 && head_dim != 64 && head_dim != 128)
+    return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "head_dim %d not in {32, 64, 128}", head_dim);
+  const int rc = derive_core(s_q, s_k, head_dim, nullptr, out);
+  if (rc != QFLASH_OK) return fail(static_cast<qflash_status>(rc), "scale out of range");
+  return QFLASH_OK;
+}
+
+void qflash_partition(int32_t num_problems, int32_t world, int32_t rank, int32_t* begin,
+                      int32_t* count) {
+  int32_t b = 0, c = 0;
+  if (num_problems >= 0 && world >= 1 && rank >= 0 && rank < world) {
+    const int64_t lo = static_cast<int64_t>(rank) * num_problems / world;
+    const int64_t hi = static_cast<int64_t>(rank + 1) * num_problems / world;
+    b = static_cast<int32_t>(lo);
+    c = static_cast<int32_t>(hi - lo);
+  }
+  if (begin) *begin = b;
+  if (count) *count = c;
+}
+
+qflash_status qflash_attention_int8(const int8_t* q, const int8_t* k, const int8_t* v, float s_q,
+                                    float s_k, float s_v, const qflash_attn_shape* shape,
+                                    int8_t* o, float* s_o, qflash_stream_t stream) {
+  return attention_host_scales(q, k, v, s_q, s_k, s_v, shape, QFLASH_VARIANT_AUTO, o, s_o,
+                               reinterpret_cast<cudaStream_t>(stream));
+}
+
+qflash_status qflash_attention_int8_ex(const int8_t* q, const int8_t* k, const int8_t* v,
+                                       float s_q, float s_k, float s_v,
+                                       const qflash_attn_shape* shape, qflash_variant variant,
+                                       int8_t* o, float* s_o, qflash_stream_t stream) {
+  return attention_host_scales(q, k, v, s_q, s_k, s_v, shape, variant, o, s_o,
+                               reinterpret_cast<cudaStream_t>(stream));
+}
+
+qflash_status qflash_attention_int8_dscale(const int8_t* q, const int8_t* k, const int8_t* v,
+                                           const float* scales_dev,
+                                           const qflash_attn_shape* shape, qflash_variant variant,
+                                           int8_t* o, void* workspace_dev,
+                                           qflash_stream_t stream) {
+  int bc = 0;
+  qflash_status st = validate_shape(shape, &bc);
+  if (st != QFLASH_OK) return st;
+  const int64_t bytes = static_cast<int64_t>(shape->num_problems) * shape->seq_len * shape->head_dim;
+  if ((st = validate_qkvo(q, k, v, o, bytes)) != QFLASH_OK) return st;
+  if (!scales_dev || !workspace_dev || !aligned16(workspace_dev))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "scales_dev / workspace_dev NULL or misaligned");
+  int dev = 0;
+  if ((st = check_device(&dev)) != QFLASH_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  auto* prm = reinterpret_cast<qf::IntParams*>(workspace_dev);
+  derive_params_kernel<<<1, 1, 0, s>>>(scales_dev, shape->head_dim, prm);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "derive_params_kernel launch");
+  return launch_common(q, k, v, shape, bc, variant, o, nullptr, prm, s);
+}
+
+static qflash_status quantize_impl(const void* const* xs, int8_t* const* xqs, float* const* scales,
+                                   int nt, qflash_dtype dtype, int64_t numel, cudaStream_t stream) {
+  if (numel < 0) return fail(QFLASH_ERR_INVALID_ARGUMENT, "numel < 0");
+  if (dtype != QFLASH_F32 && dtype != QFLASH_BF16 && dtype != QFLASH_F16)
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "unknown dtype %d", static_cast<int>(dtype));
+  for (int i = 0; i < nt; ++i) {
+    if (!xs[i] || !xqs[i] || !scales[i]) return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL pointer");
+    if (!aligned16(xs[i]) || !aligned16(xqs[i]))
+      return fail(QFLASH_ERR_INVALID_ARGUMENT, "x and x_q must be 16-byte aligned");
+  }
+  int dev = 0;
+  qflash_status st = check_device(&dev);
+  if (st != QFLASH_OK) return st;
+  qf::QuantTensors t;
+  memset(&t, 0, sizeof(t));
+  for (int i = 0; i < nt; ++i) {
+    t.x[i] = xs[i];
+    t.xq[i] = xqs[i];
+    t.scale[i] = scales[i];
+  }
+  cudaError_t e = qf::launch_quantize(t, nt, static_cast<int>(dtype), numel, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "quantize launch");
+  return QFLASH_OK;
+}
+
+qflash_status qflash_quantize_per_tensor(const void* x, qflash_dtype dtype, int64_t numel,
+                                         int8_t* x_q, float* scale_dev, float* scale_host,
+                                         qflash_stream_t stream) {
+  if (!scale_dev && !scale_host)
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "need scale_dev or scale_host");
+  if (!x || !x_q) return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  float* sd = scale_dev;
+  bool temp = false;
+  if (!sd) {
+    int dev = 0;
+    qflash_status st = check_device(&dev);
+    if (st != QFLASH_OK) return st;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&sd), sizeof(float), s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(scale)");
+    temp = true;
+  }
+  const void* xs[1] = {x};
+  int8_t* xqs[1] = {x_q};
+  float* scs[1] = {sd};
+  qflash_status st = quantize_impl(xs, xqs, scs, 1, dtype, numel, s);
+  if (st == QFLASH_OK && scale_host) {
+    cudaError_t e = cudaMemcpyAsync(scale_host, sd, sizeof(float), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) st = cuda_fail(e, "scale D2H");
+  }
+  if (temp) cudaFreeAsync(sd, s);
+  return st;
+}
+
+qflash_status qflash_quantize_qkv(const void* q, const void* k, const void* v, qflash_dtype dtype,
+                                  int64_t numel, int8_t* q_q, int8_t* k_q, int8_t* v_q,
+                                  float* scales_dev, qflash_stream_t stream) {
+  if (!scales_dev) return fail(QFLASH_ERR_INVALID_ARGUMENT, "scales_dev is NULL");
+  const void* xs[3] = {q, k, v};
+  int8_t* xqs[3] = {q_q, k_q, v_q};
+  float* scs[3] = {scales_dev, scales_dev + 1, scales_dev + 2};
+  return quantize_impl(xs, xqs, scs, 3, dtype, numel, reinterpret_cast<cudaStream_t>(stream));
+}
+
+static qflash_status dequant_impl(const int8_t* x_q, float scale, const float* scale_dev,
+                                  int64_t numel, float* y, cudaStream_t stream) {
+  if (!x_q || !y) return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (numel < 0) return fail(QFLASH_ERR_INVALID_ARGUMENT, "numel < 0");
+  if (!aligned16(x_q) || !aligned16(y))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "x_q and y must be 16-byte aligned");
+  if (!scale_dev && (!std::isfinite(scale)))
+    return fail(QFLASH_ERR_SCALE_RANGE, "scale must be finite");
+  int dev = 0;
+  qflash_status st = check_device(&dev);
+  if (st != QFLASH_OK) return st;
+  if (numel == 0) return QFLASH_OK;
+  cudaError_t e = qf::launch_dequantize(x_q, scale, scale_dev, numel, y, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "dequantize launch");
+  return QFLASH_OK;
+}
+
+qflash_status qflash_dequantize(const int8_t* x_q, float scale, int64_t numel, float* y,
+                                qflash_stream_t stream) {
+  return dequant_impl(x_q, scale, nullptr, numel, y, reinterpret_cast<cudaStream_t>(stream));
+}
+
+qflash_status qflash_dequantize_dscale(const int8_t* x_q, const float* scale_dev, int64_t numel,
+                                       float* y, qflash_stream_t stream) {
+  if (!scale_dev) return fail(QFLASH_ERR_INVALID_ARGUMENT, "scale_dev is NULL");
+  return dequant_impl(x_q, 0.0f, scale_dev, numel, y, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// Bring-up entry (include/qflash_debug.h): qflash_attention_int8_ex plus raw
+// dumps of S, P and the final (O, l) of CTA (problem 0, query tile 0).
+qflash_status qflash_debug_attention(const int8_t* q, const int8_t* k, const int8_t* v, float s_q,
+                                     float s_k, const qflash_attn_shape* shape,
+                                     qflash_variant variant, int8_t* o, int32_t* dbg_s,
+                                     int32_t* dbg_p, int32_t* dbg_o, qflash_stream_t stream) {
+  int bc = 0;
+  qflash_status st = validate_shape(shape, &bc);
+  if (st != QFLASH_OK) return st;
+  qf::IntParams prm;
+  const int rc = derive_core(s_q, s_k, shape->head_dim, &prm, nullptr);
+  if (rc != QFLASH_OK) return fail(static_cast<qflash_status>(rc), "scale out of range");
+  int dev = 0;
+  if ((st = check_device(&dev)) != QFLASH_OK) return st;
+  return launch_common(q, k, v, shape, bc, variant, o, &prm, nullptr,
+                       reinterpret_cast<cudaStream_t>(stream), dbg_s, dbg_p, dbg_o);
+}
+
+}  // extern "C"
