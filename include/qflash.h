@@ -128,6 +128,26 @@ QFLASH_API qflash_status qflash_attention_int8_dscale(const int8_t* q, const int
                                            int8_t* o, void* workspace_dev,
                                            qflash_stream_t stream);
 
+/* The fused step for dynamic quantization without an extra launch:
+ * qflash_quantize_qkv_prepare = qflash_quantize_qkv that also derives the
+ * attention's integer constants from the final (s_q, s_k) on the device (block 0
+ * of the quantize kernel, same fp64 expression as qflash_derive_params) into
+ * workspace_dev (QFLASH_DSCALE_WORKSPACE_BYTES, 16-byte aligned; int32 status at
+ * offset 0).  qflash_attention_int8_prepared then runs Algorithm 1 with the
+ * constants found in workspace_dev (nothing is written to o if the status is
+ * not QFLASH_OK).  head_dim must be the d of the following attention call. */
+QFLASH_API qflash_status qflash_quantize_qkv_prepare(const void* q, const void* k, const void* v,
+                                                     qflash_dtype dtype, int64_t numel,
+                                                     int8_t* q_q, int8_t* k_q, int8_t* v_q,
+                                                     float* scales_dev, int32_t head_dim,
+                                                     void* workspace_dev, qflash_stream_t stream);
+QFLASH_API qflash_status qflash_attention_int8_prepared(const int8_t* q, const int8_t* k,
+                                                        const int8_t* v,
+                                                        const qflash_attn_shape* shape,
+                                                        qflash_variant variant, int8_t* o,
+                                                        const void* workspace_dev,
+                                                        qflash_stream_t stream);
+
 /* Inverse of Eq. 2: y = fl32(scale * (float)x^).  x_q device int8[numel],
  * y device float[numel]. */
 QFLASH_API qflash_status qflash_dequantize(const int8_t* x_q, float scale, int64_t numel, float* y,

@@ -16,12 +16,13 @@ extern "C" {
  *   dbg_s [128][B_c]     S = Q K_0^T of KV tile 0 (step 1), TMEM lane = row
  *   dbg_p [128][B_c/4]   packed int8 P of KV tile 0 (steps 5-6), byte i = key 4w+i
  *   dbg_o [128][d+1]     final O accumulator and l (last column) before step 11
+ *   dbg_t [128] int64    clock64() timeline of that CTA (slots in qflash_attention.cu)
  * (For the packed variant B_c = 128: two 64-key windows.) */
 QFLASH_API qflash_status qflash_debug_attention(const int8_t* q, const int8_t* k, const int8_t* v,
                                                 float s_q, float s_k,
                                                 const qflash_attn_shape* shape,
                                                 qflash_variant variant, int8_t* o, int32_t* dbg_s,
-                                                int32_t* dbg_p, int32_t* dbg_o,
+                                                int32_t* dbg_p, int32_t* dbg_o, long long* dbg_t,
                                                 qflash_stream_t stream);
 
 #ifdef __cplusplus

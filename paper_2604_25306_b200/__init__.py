@@ -4,9 +4,11 @@ The product is libqflash.so (C ABI, include/qflash.h); this package is its thin
 Python binding (argument marshalling only) plus the seeded synthetic inputs.
 """
 from .api import (QFlashPipeline, qflash_attention_int8, qflash_attention_int8_dscale,
+                  qflash_attention_int8_prepared, qflash_quantize_qkv_prepare,
                   qflash_dequantize, qflash_derive_params, qflash_forward, qflash_partition,
                   qflash_quantize_per_tensor, qflash_quantize_qkv)
 
 __all__ = ["QFlashPipeline", "qflash_attention_int8", "qflash_attention_int8_dscale",
+           "qflash_attention_int8_prepared", "qflash_quantize_qkv_prepare",
            "qflash_dequantize", "qflash_derive_params", "qflash_forward", "qflash_partition",
            "qflash_quantize_per_tensor", "qflash_quantize_qkv"]

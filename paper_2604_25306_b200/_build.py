@@ -10,7 +10,7 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_objs")
 LIB = os.path.join(PKG, "libqflash.so")
 SOURCES = ["qflash_attention.cu", "qflash_quant.cu", "qflash_host.cu"]
-HEADERS = ["ptx.cuh", "qflash_common.cuh"]
+HEADERS = ["ptx.cuh", "qflash_common.cuh", "qflash_params.cuh"]
 PUBLIC_HEADERS = ["qflash.h", "qflash_debug.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

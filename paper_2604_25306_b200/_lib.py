@@ -28,6 +28,7 @@ EXPORTED = [
     "qflash_attention_int8_ex", "qflash_attention_int8_dscale", "qflash_dequantize",
     "qflash_dequantize_dscale", "qflash_derive_params", "qflash_partition",
     "qflash_status_string", "qflash_last_error", "qflash_version",
+    "qflash_quantize_qkv_prepare", "qflash_attention_int8_prepared",
 ]
 
 
@@ -75,6 +76,11 @@ def lib():
     L.qflash_attention_int8_dscale.restype = st
     L.qflash_attention_int8_dscale.argtypes = [vp, vp, vp, vp, ctypes.POINTER(AttnShape), st, vp,
                                                vp, vp]
+    L.qflash_quantize_qkv_prepare.restype = st
+    L.qflash_quantize_qkv_prepare.argtypes = [vp, vp, vp, st, i64, vp, vp, vp, vp, i32, vp, vp]
+    L.qflash_attention_int8_prepared.restype = st
+    L.qflash_attention_int8_prepared.argtypes = [vp, vp, vp, ctypes.POINTER(AttnShape), st, vp,
+                                                 vp, vp]
     L.qflash_dequantize.restype = st
     L.qflash_dequantize.argtypes = [vp, f32, i64, vp, vp]
     L.qflash_dequantize_dscale.restype = st
@@ -91,7 +97,7 @@ def lib():
     L.qflash_version.argtypes = []
     L.qflash_debug_attention.restype = st
     L.qflash_debug_attention.argtypes = [vp, vp, vp, f32, f32, ctypes.POINTER(AttnShape), st, vp,
-                                         vp, vp, vp, vp]
+                                         vp, vp, vp, vp, vp]
     _lib = L
     return L
 

@@ -111,10 +111,42 @@ def qflash_dequantize(x_q: torch.Tensor, scale, out: torch.Tensor | None = None,
 
 
 # ---------------------------------------------------------------- pipeline
+def qflash_quantize_qkv_prepare(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, outs=None,
+                                scales: torch.Tensor | None = None,
+                                workspace: torch.Tensor | None = None, stream=None):
+    """Fused Q/K/V quantization that also derives the attention constants on the
+    device.  Returns (q_q, k_q, v_q, scales float32[3], workspace int32[32])."""
+    assert q.shape == k.shape == v.shape and q.dtype == k.dtype == v.dtype and q.dim() == 3
+    if outs is None:
+        outs = [torch.empty(q.shape, dtype=torch.int8, device=q.device) for _ in range(3)]
+    scales = torch.empty(3, dtype=torch.float32, device=q.device) if scales is None else scales
+    if workspace is None:
+        workspace = torch.empty(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=q.device)
+    check(lib().qflash_quantize_qkv_prepare(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v),
+                                            _DTYPES[q.dtype], q.numel(), _dev_ptr(outs[0]),
+                                            _dev_ptr(outs[1]), _dev_ptr(outs[2]), _dev_ptr(scales),
+                                            q.shape[2], _dev_ptr(workspace), _stream(stream)))
+    return outs[0], outs[1], outs[2], scales, workspace
+
+
+def qflash_attention_int8_prepared(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                                   workspace: torch.Tensor, block_kv: int = 128,
+                                   variant: str = "auto", out: torch.Tensor | None = None,
+                                   stream=None):
+    """Algorithm 1 with the constants qflash_quantize_qkv_prepare left in `workspace`."""
+    out = torch.empty_like(q) if out is None else out
+    shape = _shape(q, block_kv)
+    check(lib().qflash_attention_int8_prepared(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v),
+                                               ctypes.byref(shape), _lib.VARIANTS[variant],
+                                               _dev_ptr(out), _dev_ptr(workspace), _stream(stream)))
+    return out
+
+
 class QFlashPipeline:
     """The whole hot path for one [P, N, d] workload with preallocated buffers:
-    fused Q/K/V quantization -> device-scale integer attention -> dequantization.
-    Four of the library's kernels per call, no host synchronization."""
+    fused Q/K/V quantization (+ device-side constant derivation) -> integer
+    attention -> dequantization.  Four of the library's kernels per call
+    (amax, quantize, attention, dequantize) and no host synchronization."""
 
     def __init__(self, P: int, N: int, d: int, block_kv: int = 128, device="cuda",
                  variant: str = "auto"):
@@ -129,10 +161,10 @@ class QFlashPipeline:
         self.out = torch.empty(self.shape, dtype=torch.float32, device=dev)
 
     def __call__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, stream=None):
-        qflash_quantize_qkv(q, k, v, outs=self.qkv_q, scales=self.scales, stream=stream)
-        qflash_attention_int8_dscale(self.qkv_q[0], self.qkv_q[1], self.qkv_q[2], self.scales,
-                                     self.block_kv, self.variant, out=self.o_q,
-                                     workspace=self.workspace, stream=stream)
+        qflash_quantize_qkv_prepare(q, k, v, outs=self.qkv_q, scales=self.scales,
+                                    workspace=self.workspace, stream=stream)
+        qflash_attention_int8_prepared(self.qkv_q[0], self.qkv_q[1], self.qkv_q[2], self.workspace,
+                                       self.block_kv, self.variant, out=self.o_q, stream=stream)
         qflash_dequantize(self.o_q, self.scales[2:3], out=self.out, stream=stream)
         return self.out
 

@@ -29,14 +29,16 @@ QF_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
 QF_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the
+// phase completes (or ~1 ms passes) instead of spinning on issue slots.
 QF_DEV bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(bar), "r"(parity)
+      : "r"(bar), "r"(parity), "r"(1000000u)
       : "memory");
   return ok != 0;
 }
@@ -141,6 +143,11 @@ QF_DEV void tmem_ld8(uint32_t taddr, uint32_t* r) {
                  "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
 }
+QF_DEV void tmem_ld4(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
 QF_DEV void tmem_ld1(uint32_t taddr, uint32_t& r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
 }
@@ -171,9 +178,49 @@ QF_DEV void tmem_st8(uint32_t taddr, const uint32_t* r) {
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
       : "memory");
 }
+QF_DEV void tmem_st4(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
+               : "memory");
+}
 QF_DEV void tmem_st1(uint32_t taddr, uint32_t r) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(r)
                : "memory");
+}
+
+// Width-generic wrappers: W consecutive columns (W in {4, 8, 16, 32, 64}).
+template <int W>
+QF_DEV void tmem_ld(uint32_t taddr, uint32_t* r) {
+  if constexpr (W == 4) tmem_ld4(taddr, r);
+  else if constexpr (W == 8) tmem_ld8(taddr, r);
+  else if constexpr (W == 16) tmem_ld16(taddr, r);
+  else if constexpr (W == 32) tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(r));
+  else {
+    static_assert(W % 32 == 0, "tmem_ld width");
+#pragma unroll
+    for (int i = 0; i < W / 32; ++i)
+      tmem_ld32(taddr + 32 * i, *reinterpret_cast<uint32_t(*)[32]>(r + 32 * i));
+  }
+}
+template <int W>
+QF_DEV void tmem_st(uint32_t taddr, const uint32_t* r) {
+  if constexpr (W == 4) tmem_st4(taddr, r);
+  else if constexpr (W == 8) tmem_st8(taddr, r);
+  else if constexpr (W == 16) tmem_st16(taddr, r);
+  else if constexpr (W == 32) tmem_st32(taddr, r);
+  else {
+    static_assert(W % 32 == 0, "tmem_st width");
+#pragma unroll
+    for (int i = 0; i < W / 32; ++i) tmem_st32(taddr + 32 * i, r + 32 * i);
+  }
+}
+
+// Named barrier over `count` threads (id 0 is __syncthreads).
+QF_DEV void named_bar_sync(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+QF_DEV void named_bar_arrive(uint32_t id, uint32_t count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 // ------------------------------------------------------------ descriptors
@@ -200,6 +247,26 @@ __host__ __device__ constexpr uint32_t make_idesc_i8(uint32_t M, uint32_t N, uin
 }
 
 // ---------------------------------------------------------- integer helpers
+// a + b + c as one 3-input IADD3 (ALU pipe).  Written as two dependent PTX adds
+// inside one asm block so the compiler can neither hoist a partial sum out of
+// a loop nor turn the add into an FMA-pipe IMAD.IADD.
+QF_DEV uint32_t iadd3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("{\n\t.reg .u32 t;\n\tadd.u32 t, %1, %2;\n\tadd.u32 %0, t, %3;\n\t}"
+      : "=r"(d)
+      : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+// floor(x * a / 2^31) for signed x, 0 <= a < 2^31: one IMAD.WIDE + one funnel shift.
+QF_DEV int32_t mul_shr31(int32_t x, int32_t a) {
+  int32_t q;
+  asm("{\n\t.reg .s64 t;\n\t.reg .b32 lo, hi;\n\t"
+      "mul.wide.s32 t, %1, %2;\n\tmov.b64 {lo, hi}, t;\n\t"
+      "shf.r.wrap.b32 %0, lo, hi, 31;\n\t}"
+      : "=r"(q)
+      : "r"(x), "r"(a));
+  return q;
+}
 QF_DEV uint32_t umulhi(uint32_t a, uint32_t b) { return __umulhi(a, b); }
 // (0:x) >> min(s, 32): 0 for s >= 32 (funnel shift with clamp).
 QF_DEV uint32_t shr_clamp(uint32_t x, uint32_t s) { return __funnelshift_rc(x, 0u, s); }

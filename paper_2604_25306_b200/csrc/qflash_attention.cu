@@ -2,14 +2,16 @@
 // arxiv 2604.25306) for B200 / sm_100a.
 //
 // One CTA owns one 128-row query tile (B_r = 128 = the tcgen05 M; TMEM lane r =
-// query row r).  Warp roles (256 threads):
-//   warp 0      TMA producer: Q tile once, K_j / V_j through a 2-stage ring
-//   warp 1      MMA issuer:   S_j = Q K_j^T   (tcgen05.mma kind::i8, SS, s32 in TMEM)
-//                             O  += P_j V_j   (kind::i8, TS: P from TMEM, V MN-major)
-//   warp 2      TMEM allocator
-//   warps 4..7  integer softmax, thread = query row: rowmax (Eq. 4), ShiftExp2
-//               (Alg. 2, division-free exact quotient), requantization (Eq. 10),
-//               ScaleRelease of O and l (Eq. 14), normalization (step 11).
+// query row r).  Warp roles (640 threads):
+//   warp 0       TMA producer: Q tile once, K_j / V_j through a 2-stage ring
+//   warp 1       MMA issuer:   S_j = Q K_j^T   (tcgen05.mma kind::i8, SS, s32 in TMEM)
+//                              O  += P_j V_j   (kind::i8, TS: P from TMEM, V MN-major)
+//   warp 2       TMEM allocator
+//   warps 4..19  integer softmax in 4 warpgroups, thread = (query row, quarter
+//                of the key columns): rowmax (Eq. 4, combined through shared
+//                memory), ShiftExp2 (Alg. 2, division-free exact quotient),
+//                requantization (Eq. 10), ScaleRelease of O and l (Eq. 14),
+//                normalization (step 11).
 // The row sum l (Eq. 11) is produced by the tensor core: V is extended with a
 // block of ones (N = d + 16), so TMEM column d of the O accumulator holds
 // floor-released l exactly as the oracle defines it.
@@ -47,24 +49,31 @@ constexpr RecipTable make_recip_table() {
 }
 __device__ const RecipTable g_recip = make_recip_table();
 
-constexpr int kThreads = 256;
-constexpr int kSoftmaxWarp0 = 4;
 constexpr int kStages = 2;
 constexpr int kBlockR = 128;
+
+// Bring-up timeline: clock64() stamps (callers restrict to CTA 0, first tile).
+#define QF_TS(slot)                                                               \
+  do {                                                                            \
+    if (args.dbg_t != nullptr && (slot) < 128)                                    \
+      args.dbg_t[(slot)] = clock64();                                             \
+  } while (0)
 
 template <int D, int BC>
 struct SmemLayout {
   static constexpr int kQBytes = kBlockR * D;
   static constexpr int kKVBytes = BC * D;
   static constexpr int kOnesBytes = BC * D;  // second MN atom of the extended V
-  static constexpr int kQ = 0;
-  static constexpr int kK = kQ + kQBytes;
+  static constexpr int kQ = 0;                          // [2] Q tiles (double buffer)
+  static constexpr int kK = kQ + 2 * kQBytes;
   static constexpr int kV = kK + kStages * kKVBytes;
   static constexpr int kOnes = kV + kStages * kKVBytes;
   static constexpr int kBar = kOnes + kOnesBytes;
-  static constexpr int kNumBars = 2 * kStages + 4;
+  static constexpr int kNumBars = 2 * kStages + 8;
   static constexpr int kTmemSlot = kBar + kNumBars * 8;
-  static constexpr int kTotal = kTmemSlot + 16;
+  static constexpr int kRed = kTmemSlot + 16;           // [2][kNWG<=4][128] int32 row maxima
+  static constexpr int kRecip = kRed + 2 * 4 * 128 * 4;  // [1024] u32 reciprocal table
+  static constexpr int kTotal = kRecip + 1024 * 4;
   static constexpr int kAlloc = kTotal + 1024;  // slack for 1024-B alignment
 };
 
@@ -87,15 +96,24 @@ __host__ __device__ constexpr uint32_t swizzle_layout() {
 //   d1 = m + s_inv - S  (>= s_inv),  q1 = floor(d1 / s_inv) = q + 1  (exact magic)
 //   y  = (q1 s_inv + S + s_inv - m) >> q1  ==  ((r >> 1) + s_inv) >> q   (Alg. 2)
 //   P  = floor(y M_P / 2^r_P)                                            (Eq. 10)
+// Instruction mix per element: 2 IADD3 + SHF (ALU pipe), 2 IMAD.HI + IMAD (FMA
+// pipe); `m` is the row maximum, `nm` = -m.
 template <bool FASTQ>
-QF_DEV int32_t shift_exp2_requant(int32_t S, uint32_t c2, int32_t c3, const IntParams& p) {
-  const uint32_t d1 = c2 - static_cast<uint32_t>(S);
+QF_DEV int32_t shift_exp2_requant(int32_t S, uint32_t m, uint32_t nm, const IntParams& p) {
+  const uint32_t s_inv = static_cast<uint32_t>(p.s_inv);
+  const uint32_t d1 = iadd3(m, static_cast<uint32_t>(-S), s_inv);
   uint32_t q1 = umulhi(d1, p.q_magic);
   if constexpr (!FASTQ) q1 >>= p.q_shift;
-  const uint32_t num = q1 * static_cast<uint32_t>(p.s_inv) + static_cast<uint32_t>(S + c3);
+  const uint32_t num = q1 * s_inv + iadd3(static_cast<uint32_t>(S), s_inv, nm);
   uint32_t y = shr_clamp(num, q1);
-  if constexpr (!FASTQ) y <<= p.p_pre;
-  return static_cast<int32_t>(umulhi(y, p.p_mul));
+  if constexpr (FASTQ) {
+    // y M_P < 2^32 (host-checked: s_inv M_P < 2^32): IMAD.lo + SHF instead of
+    // the half-rate IMAD.HI.
+    return static_cast<int32_t>((y * static_cast<uint32_t>(p.m_p)) >> p.r_p);
+  } else {
+    y <<= p.p_pre;
+    return static_cast<int32_t>(umulhi(y, p.p_mul));
+  }
 }
 
 // alpha = ShiftExp2(m_old - m_new) (step 4) -- same formula, x = m_old - m_new.
@@ -117,16 +135,37 @@ QF_DEV int32_t release_factor(int32_t alpha, const IntParams& p) {
   return static_cast<int32_t>(a);
 }
 
+// A_f = floor(alpha 2^32 / s_inv) (mod 2^32; alpha = s_inv rows are passed through).
+QF_DEV uint32_t release_factor32(int32_t alpha, const IntParams& p) {
+  const uint64_t n = static_cast<uint64_t>(alpha) << 32;  // < 2^56
+  const uint64_t mg = (static_cast<uint64_t>(p.rel_magic_hi) << 32) | p.rel_magic_lo;
+  return static_cast<uint32_t>(__umul64hi(n, mg) >> p.rel_shift);
+}
+
+// Fast exact ScaleRelease, valid when |X| s_inv < 2^32 and 0 <= alpha < s_inv:
+//   X >= 0:  floor(X alpha / s_inv) = hi(X * A_c),  A_c = A_f + 1 (>= alpha 2^32 / s_inv)
+//   X <  0:  floor(X alpha / s_inv) = hi(X * A_f) (signed) = hi(X_u * A_f) - A_f
+// (the over/under-estimate is < 1/s_inv, which never crosses an integer because
+// X alpha / s_inv is a multiple of 1/s_inv).  alpha = s_inv rows keep X.
+// 5 instructions: SHF, IADD, LOP3, IMAD.HI (mad.hi), SEL.
+QF_DEV uint32_t release_fast(uint32_t X, uint32_t a_c, uint32_t na_f, bool ident) {
+  const uint32_t m = static_cast<uint32_t>(static_cast<int32_t>(X) >> 31);
+  const uint32_t a = a_c + m;
+  const uint32_t corr = na_f & m;
+  uint32_t q;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(q) : "r"(X), "r"(a), "r"(corr));
+  return ident ? X : q;
+}
+
 // ScaleRelease of one accumulator element: floor(X alpha / s_inv) exactly
 // (Eq. 14 realised per P:L408, reading R10).  q0 = floor(X A / 2^31) is within
 // one of the answer; the remainder X alpha - q0 s_inv (exact mod 2^32, true
 // value in [-s_inv, 2 s_inv)) corrects it.
 QF_DEV int32_t scale_release(int32_t X, int32_t alpha, int32_t A, int32_t s_inv) {
-  const int64_t t = static_cast<int64_t>(X) * static_cast<int64_t>(A);
-  int32_t q0 = static_cast<int32_t>(t >> 31);
+  int32_t q0 = mul_shr31(X, A);
   const int32_t rem = X * alpha - q0 * s_inv;
   q0 += (rem >= s_inv) ? 1 : 0;
-  q0 -= (rem < 0) ? 1 : 0;
+  q0 += rem >> 31;  // -1 if rem < 0
   return q0;
 }
 
@@ -138,251 +177,407 @@ struct Recip {
   int32_t sh;
   int32_t l;
 };
-QF_DEV Recip make_recip(int32_t l) {
+QF_DEV Recip make_recip(int32_t l, const uint32_t* table) {
   const int32_t k = __clz(l);                       // l >= 2  =>  1 <= k <= 30
   const uint32_t ln = static_cast<uint32_t>(l) << k;  // [2^31, 2^32)
   Recip r;
-  r.R = static_cast<int32_t>(g_recip.v[(ln >> 21) & 1023u]);
+  r.R = static_cast<int32_t>(table[(ln >> 21) & 1023u]);
   r.sh = 30 - k;
   r.l = l;
   return r;
 }
-QF_DEV int32_t floor_div(int32_t O, const Recip& r) {
+// q0 = floor(O R / 2^(62-k)) is within one of floor(O / l) whenever |O / l| < 2^11;
+// `bad` flags the (theoretical) rest for an exact slow pass.
+QF_DEV int32_t floor_div(int32_t O, const Recip& r, bool& bad) {
   int32_t q0 = __mulhi(O, r.R) >> r.sh;
   const int32_t rem = O - q0 * r.l;
   q0 += (rem >= r.l) ? 1 : 0;
-  q0 -= (rem < 0) ? 1 : 0;
+  q0 += rem >> 31;  // -1 if rem < 0
+  bad |= (rem >= 2 * r.l) | (rem < -r.l);
   return q0;
 }
+QF_DEV int32_t floor_div_exact(int32_t O, int32_t l) {
+  int32_t q = 0;  // long division by repeated doubling (integer only, rare path)
+  int64_t n = O, d = l;
+  int64_t qq = 0, acc = 0;
+  const bool neg = n < 0;
+  uint64_t un = neg ? static_cast<uint64_t>(-(n + 1)) : static_cast<uint64_t>(n);
+#pragma unroll 1
+  for (int b = 31; b >= 0; --b) {
+    acc = (acc << 1) | static_cast<int64_t>((un >> b) & 1u);
+    if (acc >= d) { acc -= d; qq |= (1ll << b); }
+  }
+  q = static_cast<int32_t>(neg ? ~qq : qq);  // floor(O/l) = ~floor(~O/l) for O < 0
+  return q;
+}
 
-// Softmax/epilogue role (warps 4..7): thread = query row = TMEM lane.
+// ---------------------------------------------------------------- configuration
+// Warps 0..3: control (TMA producer, MMA issuer, TMEM allocator, table loader);
+// warps 4..19: four softmax warpgroups.  Warp w >= 4 handles TMEM lane quarter
+// (w & 3), i.e. query rows 32*(w&3) .. +31 (thread = row); its warpgroup
+// g = (w - 4) / 4 owns key columns [g*CW, (g+1)*CW) of every S tile and O
+// columns [g*D/4, (g+1)*D/4) for the release and the normalization.  The row
+// maximum is combined across warpgroups through shared memory (one named
+// barrier per KV tile).
+template <int D, int BC, bool PACKED>
+struct Cfg {
+  static constexpr int kNWG = 4;                          // softmax warpgroups
+  static constexpr int kSoftThreads = 128 * kNWG;
+  static constexpr int kThreads = 128 + kSoftThreads;
+  static constexpr int kCW = (PACKED ? 64 : BC) / kNWG;   // key columns per thread
+  static constexpr int kOW = D / kNWG;                    // O columns per thread
+  static constexpr bool kSInRegs = kCW <= 32;
+  // TMEM: kNumS S buffers of BC columns (P_j aliases its own S buffer), then O
+  // (D columns) + l (column D) + 15 copies of l from the ones block.
+  static constexpr int kNumS = (2 * BC + D + 16 <= 512) ? 2 : 1;
+  static constexpr uint32_t kTmemO = kNumS * BC;
+};
+
+// Persistent tile iterator (identical in every role).  Generic: tile t =
+// problem * T_r + query-tile, CTA b visits t = b, b + G, b + 2G, ...  Packed:
+// tile t = windows (2t, 2t + 1).  No runtime division (integer-only kernel):
+// the host supplies G / T_r, G % T_r and a magic for the first tile.
+struct TileIter {
+  int problem, qt, i;
+  __device__ void init(const AttnArgs& a, bool packed) {
+    i = 0;
+    const uint32_t t = blockIdx.x;
+    if (packed) {
+      problem = 2 * static_cast<int>(t);
+      qt = 0;
+    } else if (a.Tr == 1) {
+      problem = static_cast<int>(t);
+      qt = 0;
+    } else {
+      problem = static_cast<int>(__umulhi(t, a.tr_magic));  // t / T_r (exact for t < 2^32 / T_r)
+      qt = static_cast<int>(t) - problem * a.Tr;
+    }
+  }
+  __device__ bool valid(const AttnArgs& a, bool packed) const {
+    return packed ? problem < a.P : problem < a.P;
+  }
+  __device__ void next(const AttnArgs& a, bool packed) {
+    ++i;
+    if (packed) {
+      problem += 2 * static_cast<int>(gridDim.x);
+    } else {
+      problem += a.g_div;
+      qt += a.g_mod;
+      if (qt >= a.Tr) {
+        qt -= a.Tr;
+        ++problem;
+      }
+    }
+  }
+};
+
+// ---------------------------------------------------------------- softmax role
 template <int D, int BC, bool PACKED, bool FASTQ>
-__device__ __forceinline__ void softmax_rows(const AttnArgs& args, const IntParams& prm,
+__device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntParams& prm,
                                              uint32_t tmem_base, uint64_t* bar_s_full,
                                              uint64_t* bar_p_full, uint64_t* bar_o_full,
-                                             int problem, int q0, int warp, int lane) {
-  constexpr uint32_t kTmemS = 0;
-  constexpr uint32_t kTmemO = BC;
+                                             int32_t* red, const uint32_t* recip, int warp,
+                                             int lane) {
+  using C = Cfg<D, BC, PACKED>;
+  constexpr int CW = C::kCW;
+  constexpr int OW = C::kOW;
   const int N = args.N;
   const int Tc = PACKED ? 1 : args.Tc;
-
-  // ========================================================= softmax rows
+  const int g = (warp - 4) >> 2;        // warpgroup
   const int quarter = warp & 3;
   const int row = quarter * 32 + lane;  // TMEM lane == tile row
   const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-  const uint32_t tS = tmem_base + lane_off + kTmemS;
-  const uint32_t tO = tmem_base + lane_off + kTmemO;
-  // packed: this row's window occupies key columns [col0, col0 + 64)
-  const int col0 = PACKED ? (row >> 6) * 64 : 0;
-  constexpr int kCols = PACKED ? 64 : BC;  // columns this thread evaluates
-  int32_t m = -(1 << 21);                  // m^(0) = -2^21
+  const uint32_t tS0 = tmem_base + lane_off;  // S buffer b at + b * BC
+  const uint32_t tO = tmem_base + lane_off + C::kTmemO;
+  const int win = PACKED ? (row >> 6) : 0;
+  const int c0 = (PACKED ? win * 64 : 0) + g * CW;  // first key column of this thread
+  const int c0_in_tile = g * CW;                    // ... relative to its window / tile
+  const bool dbg_cta = blockIdx.x == 0;
 
-  for (int j = 0; j < Tc; ++j) {
-    mbar_wait(bar_s_full, j & 1);
-    tc_fence_after();
-    const int valid = PACKED ? N : min(BC, N - j * BC);  // ragged last tile (R16)
+  TileIter ti;
+  ti.init(args, PACKED);
+  for (; ti.valid(args, PACKED); ti.next(args, PACKED)) {
+    const int problem = ti.problem;
+    const int q0 = ti.qt * kBlockR;
+    const bool dbg = dbg_cta && ti.i == 0;
+    // rows of a padded tail tile (or of a missing second window) do no work
+    const int rows_valid = PACKED ? ((problem + 1 < args.P) ? 128 : 64) : (N - q0);
+    const bool warp_live = PACKED ? ((quarter >> 1) * 64 < rows_valid) : (quarter * 32 < rows_valid);
+    int32_t m = -(1 << 21);  // m^(0) = -2^21
+    const int it0 = ti.i * Tc;
 
-    // (2)(3) row max over the valid columns
-    int32_t tmax = INT32_MIN;
-#pragma unroll
-    for (int ch = 0; ch < kCols / 32; ++ch) {
-      uint32_t s[32];
-      tmem_ld32(tS + col0 + ch * 32, s);
-      tmem_wait_ld();
-      if (args.dbg_s != nullptr && j == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) args.dbg_s[row * BC + col0 + ch * 32 + e] = static_cast<int32_t>(s[e]);
-      }
-#pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        const int c = ch * 32 + e;
-        if (c < valid) tmax = max(tmax, static_cast<int32_t>(s[e]));
-      }
-    }
-    const int32_t m_new = max(m, tmax);
-    // (4) alpha = ShiftExp2(m_old - m_new)
-    const int32_t alpha = shift_exp2<FASTQ>(m - m_new, prm);
-
-    // (7)(8) ScaleRelease of O and l once PV_{j-1} has landed (skip j = 0:
-    // O = l = 0; skip warps whose rows all keep their max: alpha = s_inv).
-    if (j > 0) {
-      mbar_wait(bar_o_full, (j - 1) & 1);
+    for (int j = 0; j < Tc; ++j) {
+      const int it = it0 + j;
+      const int sb = (C::kNumS == 2) ? (it & 1) : 0;
+      const uint32_t tS = tS0 + sb * BC;
+      mbar_wait(&bar_s_full[sb], (C::kNumS == 2 ? (it >> 1) : it) & 1);
       tc_fence_after();
-      if (__any_sync(0xffffffffu, alpha != prm.s_inv)) {
-        const int32_t A = release_factor(alpha, prm);
-#pragma unroll
-        for (int ch = 0; ch < D / 32; ++ch) {
-          uint32_t o[32];
-          tmem_ld32(tO + ch * 32, o);
+      if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(40 + 8 * j);
+      // columns of this thread that exist in KV tile j (ragged last tile, R16)
+      const int valid = (PACKED ? N : min(BC, N - j * BC)) - c0_in_tile;
+      uint32_t s[C::kSInRegs ? CW : 32];
+      int32_t tmax = INT32_MIN;
+      if (warp_live && valid > 0) {
+        if constexpr (C::kSInRegs) {
+          tmem_ld<CW>(tS + c0, s);
           tmem_wait_ld();
+          if (args.dbg_s != nullptr && dbg && j == 0) {
+            for (int e = 0; e < CW; ++e) args.dbg_s[row * BC + c0 + e] = static_cast<int32_t>(s[e]);
+          }
+          if (valid >= CW) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            o[e] = static_cast<uint32_t>(
-                scale_release(static_cast<int32_t>(o[e]), alpha, A, prm.s_inv));
-          tmem_st32(tO + ch * 32, o);
+            for (int e = 0; e < CW; ++e) tmax = max(tmax, static_cast<int32_t>(s[e]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < CW; ++e)
+              if (e < valid) tmax = max(tmax, static_cast<int32_t>(s[e]));
+          }
+        } else {
+#pragma unroll
+          for (int ch = 0; ch < CW / 32; ++ch) {
+            tmem_ld<32>(tS + c0 + 32 * ch, s);
+            tmem_wait_ld();
+            if (args.dbg_s != nullptr && dbg && j == 0) {
+              for (int e = 0; e < 32; ++e) args.dbg_s[row * BC + c0 + 32 * ch + e] = static_cast<int32_t>(s[e]);
+            }
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (32 * ch + e < valid) tmax = max(tmax, static_cast<int32_t>(s[e]));
+          }
         }
-        uint32_t lcol;
-        tmem_ld1(tO + D, lcol);
-        tmem_wait_ld();
-        lcol = static_cast<uint32_t>(scale_release(static_cast<int32_t>(lcol), alpha, A, prm.s_inv));
-        tmem_st1(tO + D, lcol);
       }
+      // (2)(3) combine the partial maxima of the kNWG warpgroups
+      {
+        int32_t* rb = red + (it & 1) * (C::kNWG * 128);
+        rb[g * 128 + row] = tmax;
+        named_bar_sync(1, C::kSoftThreads);
+        if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(41 + 8 * j);
+#pragma unroll
+        for (int h = 0; h < C::kNWG; ++h) tmax = max(tmax, rb[h * 128 + row]);
+      }
+      const int32_t m_new = max(m, tmax);
+      // (4) alpha = ShiftExp2(m_old - m_new)
+      const int32_t alpha = shift_exp2<FASTQ>(m - m_new, prm);
+      if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(42 + 8 * j);
+
+      // (5)(6) P = Requant(ShiftExp2(S - m_new)), 4 x int8 per TMEM column.
+      const uint32_t mu = static_cast<uint32_t>(m_new);
+      const uint32_t nmu = static_cast<uint32_t>(-m_new);
+      uint32_t pk[CW / 4];
+      if (warp_live && valid > 0) {
+        if constexpr (C::kSInRegs) {
+          if (valid >= CW) {
+#pragma unroll
+            for (int e = 0; e < CW; e += 4)
+              pk[e / 4] = pack4_sat_s8(shift_exp2_requant<FASTQ>(static_cast<int32_t>(s[e]), mu, nmu, prm),
+                                       shift_exp2_requant<FASTQ>(static_cast<int32_t>(s[e + 1]), mu, nmu, prm),
+                                       shift_exp2_requant<FASTQ>(static_cast<int32_t>(s[e + 2]), mu, nmu, prm),
+                                       shift_exp2_requant<FASTQ>(static_cast<int32_t>(s[e + 3]), mu, nmu, prm));
+          } else {
+#pragma unroll
+            for (int e = 0; e < CW; e += 4) {
+              int32_t pv[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int32_t x = shift_exp2_requant<FASTQ>(static_cast<int32_t>(s[e + u]), mu, nmu, prm);
+                pv[u] = (e + u < valid) ? x : 0;
+              }
+              pk[e / 4] = pack4_sat_s8(pv[0], pv[1], pv[2], pv[3]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int ch = 0; ch < CW / 32; ++ch) {
+            tmem_ld<32>(tS + c0 + 32 * ch, s);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; e += 4) {
+              int32_t pv[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int32_t x = shift_exp2_requant<FASTQ>(static_cast<int32_t>(s[e + u]), mu, nmu, prm);
+                pv[u] = (32 * ch + e + u < valid) ? x : 0;
+              }
+              pk[(32 * ch + e) / 4] = pack4_sat_s8(pv[0], pv[1], pv[2], pv[3]);
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < CW / 4; ++e) pk[e] = 0u;
+      }
+      // P columns [c0/4, (c0+CW)/4) alias S columns of warpgroup 0: every S read
+      // of this tile must be complete.  With S in registers the max-exchange
+      // barrier above already ordered them; otherwise synchronize again.
+      if constexpr (!C::kSInRegs) named_bar_sync(1, C::kSoftThreads);
+      tmem_st<CW / 4>(tS + (c0 >> 2), pk);
+      if constexpr (PACKED) {
+        // zero this group's share of the other window's P columns
+        uint32_t z[CW / 4];
+#pragma unroll
+        for (int e = 0; e < CW / 4; ++e) z[e] = 0u;
+        tmem_st<CW / 4>(tS + (((1 - win) * 64 + c0_in_tile) >> 2), z);
+      }
+      if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(44 + 8 * j);
+
+      // (7)(8) ScaleRelease of O (this group's columns) and l (group 0) once
+      // PV_{j-1} has landed -- after P_j so that PV_{j-1} completes behind the P
+      // computation; skipped for j = 0 (O = l = 0) and for warps whose rows all
+      // kept their maximum (alpha = s_inv is the identity, R10).  PV_j is only
+      // issued after every warp's p_full arrival below, i.e. after the release.
+      if (j > 0) {
+        mbar_wait(bar_o_full, (it - 1) & 1);
+        tc_fence_after();
+        if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(45 + 8 * j);
+        if (warp_live && __any_sync(0xffffffffu, alpha != prm.s_inv)) {
+          uint32_t o[OW];
+          tmem_ld<OW>(tO + g * OW, o);
+          uint32_t lcol;
+          tmem_ld1(tO + D, lcol);
+          tmem_wait_ld();
+          if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(46 + 8 * j);
+          // Fast exact path when every row of the warp satisfies |X| s_inv < 2^32
+          // for all its accumulators X (bound |O| <= 128 (l + 2 T_c), DESIGN.md
+          // "Kernel arithmetic"): floor(X alpha / s_inv) is then the high word of
+          // X * ceil/floor(alpha 2^32 / s_inv) with no correction.
+          const uint64_t bound = 128ull * (static_cast<uint64_t>(lcol) + 2ull * Tc) *
+                                 static_cast<uint64_t>(prm.s_inv);
+          if (__all_sync(0xffffffffu, bound < (1ull << 32))) {
+            const uint32_t a_f = release_factor32(alpha, prm);  // floor(alpha 2^32 / s_inv)
+            const uint32_t a_c = a_f + 1u;
+            const uint32_t na_f = 0u - a_f;
+            const bool ident = alpha == prm.s_inv;
+#pragma unroll
+            for (int e = 0; e < OW; ++e) o[e] = release_fast(o[e], a_c, na_f, ident);
+            tmem_st<OW>(tO + g * OW, o);
+            if (g == 0) tmem_st1(tO + D, release_fast(lcol, a_c, na_f, ident));
+          } else {
+            const int32_t A = release_factor(alpha, prm);
+#pragma unroll
+            for (int e = 0; e < OW; ++e)
+              o[e] = static_cast<uint32_t>(scale_release(static_cast<int32_t>(o[e]), alpha, A, prm.s_inv));
+            tmem_st<OW>(tO + g * OW, o);
+            if (g == 0) {
+              lcol = static_cast<uint32_t>(scale_release(static_cast<int32_t>(lcol), alpha, A, prm.s_inv));
+              tmem_st1(tO + D, lcol);
+            }
+          }
+          if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(47 + 8 * j);
+        }
+      }
+
+      tmem_wait_st();
+      if (args.dbg_p != nullptr && dbg && j == 0) {
+        named_bar_sync(1, C::kSoftThreads);
+        if (g == 0) {
+          for (int w = 0; w < BC / 4; w += 8) {
+            uint32_t pw[8];
+            tmem_ld8(tS + w, pw);
+            tmem_wait_ld();
+            for (int e = 0; e < 8; ++e) args.dbg_p[row * (BC / 4) + w + e] = static_cast<int32_t>(pw[e]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_p_full);
+      if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(43 + 8 * j);
+      m = m_new;
     }
 
-    // (5)(6) P = Requant(ShiftExp2(S - m_new)), packed 4 x int8 per column.
-    const uint32_t c2 = static_cast<uint32_t>(m_new + prm.s_inv);
-    const int32_t c3 = prm.s_inv - m_new;
-    if constexpr (PACKED) {
-      // own window: 64 columns -> 16 packed words at P column (col0 / 4)
-      uint32_t pk[16];
-#pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
-        uint32_t s[32];
-        tmem_ld32(tS + col0 + ch * 32, s);
-        tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          int32_t pv[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int c = ch * 32 + e + u;
-            const int32_t pval = shift_exp2_requant<FASTQ>(static_cast<int32_t>(s[e + u]), c2, c3, prm);
-            pv[u] = (c < valid) ? pval : 0;
-          }
-          pk[ch * 8 + e / 4] = pack4_sat_s8(pv[0], pv[1], pv[2], pv[3]);
-        }
-      }
-      uint32_t zero[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) zero[i] = 0u;
-      // P occupies columns [0, 32): own half from pk, the other window's half zero
-      tmem_st16(tS + (col0 >> 2), pk);
-      tmem_st16(tS + ((64 - col0) >> 2), zero);
-    } else {
-#pragma unroll
-      for (int ch = 0; ch < BC / 32; ++ch) {
-        uint32_t s[32];
-        tmem_ld32(tS + ch * 32, s);
-        tmem_wait_ld();
-        uint32_t pk[8];
-#pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          int32_t pv[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int c = ch * 32 + e + u;
-            const int32_t pval = shift_exp2_requant<FASTQ>(static_cast<int32_t>(s[e + u]), c2, c3, prm);
-            pv[u] = (c < valid) ? pval : 0;
-          }
-          pk[e / 4] = pack4_sat_s8(pv[0], pv[1], pv[2], pv[3]);
-        }
-        // P chunk ch -> P columns [8 ch, 8 ch + 8) (aliases S columns already read)
-        tmem_st8(tS + ch * 8, pk);
-      }
-    }
-    tmem_wait_st();
-    if (args.dbg_p != nullptr && j == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
-      for (int w = 0; w < BC / 4; w += 8) {
-        uint32_t pw[8];
-        tmem_ld8(tS + w, pw);
-        tmem_wait_ld();
-        for (int e = 0; e < 8; ++e) args.dbg_p[row * (BC / 4) + w + e] = static_cast<int32_t>(pw[e]);
-      }
-    }
-    tc_fence_before();
-    mbar_arrive(bar_p_full);
-    m = m_new;
-  }
-
-  // (11) O_i = floor(O / l), saturated to int8; write the row.
-  mbar_wait(bar_o_full, (Tc - 1) & 1);
-  tc_fence_after();
-  uint32_t lraw;
-  tmem_ld1(tO + D, lraw);
-  tmem_wait_ld();
-  const Recip rc = make_recip(static_cast<int32_t>(lraw));
-  if (args.dbg_o != nullptr && blockIdx.x == 0 && blockIdx.y == 0) {
-    for (int c = 0; c < D; c += 8) {
-      uint32_t ow[8];
-      tmem_ld8(tO + c, ow);
+    // (11) O_i = floor(O / l), saturated to int8 (R14); this group's O columns.
+    mbar_wait(bar_o_full, (it0 + Tc - 1) & 1);
+    tc_fence_after();
+    if (dbg && warp == 4 && lane == 0) QF_TS(100);
+    if (ti.i == 0) named_bar_sync(2, C::kSoftThreads + 32);  // reciprocal table ready
+    if (warp_live) {
+      uint32_t lraw;
+      uint32_t o[OW];
+      tmem_ld1(tO + D, lraw);
+      tmem_ld<OW>(tO + g * OW, o);
       tmem_wait_ld();
-      for (int e = 0; e < 8; ++e) args.dbg_o[row * (D + 1) + c + e] = static_cast<int32_t>(ow[e]);
-    }
-    args.dbg_o[row * (D + 1) + D] = static_cast<int32_t>(lraw);
-  }
-  int out_row;
-  bool row_ok;
-  int out_problem;
-  if constexpr (PACKED) {
-    out_problem = problem + (row >> 6);
-    out_row = row & 63;
-    row_ok = (out_row < N) && (out_problem < args.P);
-  } else {
-    out_problem = problem;
-    out_row = q0 + row;
-    row_ok = out_row < N;
-  }
-  int8_t* dst = args.out + (static_cast<int64_t>(out_problem) * N + out_row) * D;
+      if (args.dbg_o != nullptr && dbg) {
+        for (int e = 0; e < OW; ++e) args.dbg_o[row * (D + 1) + g * OW + e] = static_cast<int32_t>(o[e]);
+        if (g == 0) args.dbg_o[row * (D + 1) + D] = static_cast<int32_t>(lraw);
+      }
+      const Recip rc = make_recip(static_cast<int32_t>(lraw), recip);
+      int32_t qv[OW];
+      bool bad = false;
 #pragma unroll
-  for (int ch = 0; ch < D / 32; ++ch) {
-    uint32_t o[32];
-    tmem_ld32(tO + ch * 32, o);
-    tmem_wait_ld();
-    uint32_t w[8];
+      for (int e = 0; e < OW; ++e) qv[e] = floor_div(static_cast<int32_t>(o[e]), rc, bad);
+      if (__any_sync(0xffffffffu, bad)) {
 #pragma unroll
-    for (int e = 0; e < 32; e += 4)
-      w[e / 4] = pack4_sat_s8(floor_div(static_cast<int32_t>(o[e]), rc),
-                              floor_div(static_cast<int32_t>(o[e + 1]), rc),
-                              floor_div(static_cast<int32_t>(o[e + 2]), rc),
-                              floor_div(static_cast<int32_t>(o[e + 3]), rc));
-    if (row_ok) {
-      uint4* d4 = reinterpret_cast<uint4*>(dst + ch * 32);
-      d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
-      d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        for (int e = 0; e < OW; ++e) qv[e] = floor_div_exact(static_cast<int32_t>(o[e]), rc.l);
+      }
+      uint32_t w[OW / 4];
+#pragma unroll
+      for (int e = 0; e < OW; e += 4) w[e / 4] = pack4_sat_s8(qv[e], qv[e + 1], qv[e + 2], qv[e + 3]);
+      int out_problem, out_row;
+      bool ok;
+      if constexpr (PACKED) {
+        out_problem = problem + win;
+        out_row = row & 63;
+        ok = out_row < N && out_problem < args.P;
+      } else {
+        out_problem = problem;
+        out_row = q0 + row;
+        ok = out_row < N;
+      }
+      if (ok) {
+        int8_t* dst = args.out + (static_cast<int64_t>(out_problem) * N + out_row) * D + g * OW;
+        if constexpr (OW == 8) {
+          *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < OW / 16; ++e)
+            reinterpret_cast<uint4*>(dst)[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+        }
+      }
     }
+    if (dbg && warp == 4 && lane == 0) QF_TS(101);
+    // The O/l loads above completed (wait::ld) before this thread's next p_full
+    // arrival, so the next tile's first PV (which overwrites O) cannot race them.
   }
 }
 
 // ---------------------------------------------------------------- the kernel
 template <int D, int BC, bool PACKED>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Cfg<D, BC, PACKED>::kThreads, 1)
     qflash_attn_kernel(const __grid_constant__ CUtensorMap tm_q,
                        const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, const AttnArgs args) {
   using L = SmemLayout<D, BC>;
-  constexpr uint32_t kTmemCols = tmem_cols_for(BC, D);
-  static_assert(kTmemCols >= BC + D + 16, "TMEM budget");
+  using C = Cfg<D, BC, PACKED>;
+  constexpr uint32_t kTmemCols = tmem_cols_for(C::kNumS * BC, D);
+  static_assert(kTmemCols >= C::kNumS * BC + D + 16, "TMEM budget");
   constexpr uint32_t kSwz = swizzle_layout<D>();
   constexpr int kNO = D + 16;  // extended PV width (O columns + ones block)
   constexpr uint32_t kIdescQK = make_idesc_i8(128, BC, 0, 0);
   constexpr uint32_t kIdescPV = make_idesc_i8(128, kNO, 0, 1);
-  constexpr uint32_t kTmemS = 0;    // S_j (BC cols, s32); P_j (BC/4 cols, int8 x4) aliases it
-  constexpr uint32_t kTmemO = BC;   // O accumulator (D cols) + l (col D) + 15 copies of l
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint8_t* sQ = smem + L::kQ;
+  uint8_t* sQ = smem + L::kQ;  // [2]
   uint8_t* sK = smem + L::kK;
   uint8_t* sV = smem + L::kV;
   uint8_t* sOnes = smem + L::kOnes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* bar_kv_full = bars;              // [kStages]
   uint64_t* bar_kv_empty = bars + kStages;   // [kStages]
-  uint64_t* bar_q_full = bars + 2 * kStages;
-  uint64_t* bar_s_full = bar_q_full + 1;
-  uint64_t* bar_p_full = bar_q_full + 2;
-  uint64_t* bar_o_full = bar_q_full + 3;
+  uint64_t* bar_q_full = bars + 2 * kStages;  // [2]
+  uint64_t* bar_q_empty = bar_q_full + 2;     // [2]
+  uint64_t* bar_s_full = bar_q_full + 4;      // [2]
+  uint64_t* bar_p_full = bar_q_full + 6;
+  uint64_t* bar_o_full = bar_q_full + 7;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlot);
+  int32_t* red = reinterpret_cast<int32_t*>(smem + L::kRed);
+  uint32_t* recip = reinterpret_cast<uint32_t*>(smem + L::kRecip);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-
-  // Work item: generic -> (problem, query tile) = (blockIdx.x, blockIdx.y);
-  // packed -> problems 2*blockIdx.x and 2*blockIdx.x + 1.
+  if (threadIdx.x == 0 && blockIdx.x == 0) QF_TS(0);
   const int Tc = PACKED ? 1 : args.Tc;
-  const int problem = PACKED ? 2 * blockIdx.x : blockIdx.x;
-  const int q0 = PACKED ? 0 : blockIdx.y * kBlockR;
 
   // ------------------------------------------------------------- setup
   if (warp == 0 && lane == 0) {
@@ -393,9 +588,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_kv_full[s], 1);
       mbar_init(&bar_kv_empty[s], 1);
     }
-    mbar_init(bar_q_full, 1);
-    mbar_init(bar_s_full, 1);
-    mbar_init(bar_p_full, 128);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_q_full[b], 1);
+      mbar_init(&bar_q_empty[b], 1);
+      mbar_init(&bar_s_full[b], 1);
+    }
+    mbar_init(bar_p_full, C::kSoftThreads / 32);
     mbar_init(bar_o_full, 1);
     fence_barrier_init();
   }
@@ -404,13 +602,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_relinquish();
   }
   // ones block of the extended V operand (any layout: every byte is 1)
-  for (int i = threadIdx.x; i < L::kOnesBytes / 16; i += kThreads)
+  for (int i = threadIdx.x; i < L::kOnesBytes / 16; i += C::kThreads)
     reinterpret_cast<uint4*>(sOnes)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0 && blockIdx.x == 0) QF_TS(1);
 
   // Integer constants (host-derived by value, or device-derived).
   IntParams prm = args.prm;
@@ -418,67 +617,107 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool run = (prm.status == 0);
 
   if (run) {
-    if (warp == 0) {
+    if (warp == 3) {
+      // reciprocal table for step (11) -> shared memory, off the critical path:
+      // the softmax warps sync on named barrier 2 before their first normalization.
+      for (int i = lane; i < 1024; i += 32) recip[i] = g_recip.v[i];
+      __threadfence_block();
+      named_bar_arrive(2, C::kSoftThreads + 32);
+    } else if (warp == 0) {
       // ========================================================= TMA producer
       if (lane == 0) {
-        mbar_arrive_expect_tx(bar_q_full, L::kQBytes);
-        if constexpr (PACKED)
-          tma_load_3d(sQ, &tm_q, bar_q_full, 0, 0, problem);  // box {D, 64, 2}
-        else
-          tma_load_3d(sQ, &tm_q, bar_q_full, 0, q0, problem);  // box {D, 128, 1}
-        for (int j = 0; j < Tc; ++j) {
-          const int st = j % kStages;
-          if (j >= kStages) mbar_wait(&bar_kv_empty[st], ((j / kStages) - 1) & 1);
-          mbar_arrive_expect_tx(&bar_kv_full[st], 2 * L::kKVBytes);
-          const int kv_row = PACKED ? 0 : j * BC;
-          tma_load_3d(sK + st * L::kKVBytes, &tm_k, &bar_kv_full[st], 0, kv_row, problem);
-          tma_load_3d(sV + st * L::kKVBytes, &tm_v, &bar_kv_full[st], 0, kv_row, problem);
+        TileIter ti;
+        ti.init(args, PACKED);
+        int it = 0;
+        for (; ti.valid(args, PACKED); ti.next(args, PACKED)) {
+          const int qb = ti.i & 1;
+          if (ti.i >= 2) mbar_wait(&bar_q_empty[qb], ((ti.i >> 1) - 1) & 1);
+          mbar_arrive_expect_tx(&bar_q_full[qb], L::kQBytes);
+          if constexpr (PACKED)
+            tma_load_3d(sQ + qb * L::kQBytes, &tm_q, &bar_q_full[qb], 0, 0, ti.problem);  // box {D,64,2}
+          else
+            tma_load_3d(sQ + qb * L::kQBytes, &tm_q, &bar_q_full[qb], 0, ti.qt * kBlockR, ti.problem);
+          for (int j = 0; j < Tc; ++j, ++it) {
+            const int st = it % kStages;
+            if (it >= kStages) mbar_wait(&bar_kv_empty[st], ((it / kStages) - 1) & 1);
+            mbar_arrive_expect_tx(&bar_kv_full[st], 2 * L::kKVBytes);
+            const int kv_row = PACKED ? 0 : j * BC;
+            tma_load_3d(sK + st * L::kKVBytes, &tm_k, &bar_kv_full[st], 0, kv_row, ti.problem);
+            tma_load_3d(sV + st * L::kKVBytes, &tm_v, &bar_kv_full[st], 0, kv_row, ti.problem);
+          }
         }
       }
     } else if (warp == 1) {
       // ========================================================= MMA issuer
+      // Issue order within a tile (tcgen05.mma of one thread execute in order,
+      // which also orders every TMEM WAR hazard between PV and a later QK):
+      //   two S buffers:  QK_0 | QK_1 PV_0 | QK_2 PV_1 | ... | PV_last
+      //   one S buffer:   QK_0 | PV_0 QK_1 | PV_1 QK_2 | ... | PV_last
+      // The next tile's QK_0 follows PV_last, so the TMA loads and QK_0 of tile
+      // i+1 overlap the normalization of tile i.
       if (lane == 0) {
-        const uint32_t tS = tmem_base + kTmemS;
-        const uint32_t tO = tmem_base + kTmemO;
-        const uint32_t q_addr = smem_u32(sQ);
+        const uint32_t tO = tmem_base + C::kTmemO;
         const uint32_t ones_addr = smem_u32(sOnes);
-        mbar_wait(bar_q_full, 0);
-        tc_fence_after();
-        for (int j = 0; j < Tc; ++j) {
-          const int st = j % kStages;
-          mbar_wait(&bar_kv_full[st], (j / kStages) & 1);
-          if (j > 0) mbar_wait(bar_o_full, (j - 1) & 1);  // P_{j-1} consumed: S free
+        TileIter ti;
+        ti.init(args, PACKED);
+        for (; ti.valid(args, PACKED); ti.next(args, PACKED)) {
+          const int qb = ti.i & 1;
+          const uint32_t q_addr = smem_u32(sQ + qb * L::kQBytes);
+          const int it0 = ti.i * Tc;
+          mbar_wait(&bar_q_full[qb], (ti.i >> 1) & 1);
           tc_fence_after();
-          const uint32_t k_addr = smem_u32(sK + st * L::kKVBytes);
-          const uint32_t v_addr = smem_u32(sV + st * L::kKVBytes);
-          // (1) S = Q K_j^T : M=128, N=BC, K=D in steps of 32 bytes.
+          if (ti.i == 0 && blockIdx.x == 0) QF_TS(2);
+          auto issue_qk = [&](int j) {
+            const int it = it0 + j;
+            const int st = it % kStages;
+            const int sb = (C::kNumS == 2) ? (it & 1) : 0;
+            mbar_wait(&bar_kv_full[st], (it / kStages) & 1);
+            tc_fence_after();
+            if (ti.i == 0 && blockIdx.x == 0 && j < 7) QF_TS(3 + 4 * j);
+            const uint32_t k_addr = smem_u32(sK + st * L::kKVBytes);
+            // (1) S = Q K_j^T : M=128, N=BC, K=D in steps of 32 bytes.
 #pragma unroll
-          for (int kk = 0; kk < D / 32; ++kk) {
-            const uint64_t da = make_smem_desc(q_addr + 32 * kk, 16, 8 * D, kSwz);
-            const uint64_t db = make_smem_desc(k_addr + 32 * kk, 16, 8 * D, kSwz);
-            mma_i8_ss(tS, da, db, kIdescQK, kk > 0 ? 1u : 0u);
-          }
-          mma_commit(bar_s_full);
-          // (8) O (+)= P_j [V_j | 1] : M=128, N=D+16, K=BC in steps of 32 keys.
-          mbar_wait(bar_p_full, j & 1);
-          tc_fence_after();
+            for (int kk = 0; kk < D / 32; ++kk) {
+              const uint64_t da = make_smem_desc(q_addr + 32 * kk, 16, 8 * D, kSwz);
+              const uint64_t db = make_smem_desc(k_addr + 32 * kk, 16, 8 * D, kSwz);
+              mma_i8_ss(tmem_base + sb * BC, da, db, kIdescQK, kk > 0 ? 1u : 0u);
+            }
+            mma_commit(&bar_s_full[sb]);
+            if (j == Tc - 1) mma_commit(&bar_q_empty[qb]);  // last read of this Q tile
+          };
+          auto issue_pv = [&](int j) {
+            const int it = it0 + j;
+            const int st = it % kStages;
+            const int sb = (C::kNumS == 2) ? (it & 1) : 0;
+            const uint32_t v_addr = smem_u32(sV + st * L::kKVBytes);
+            // (8) O (+)= P_j [V_j | 1] : M=128, N=D+16, K=BC in steps of 32 keys.
+            mbar_wait(bar_p_full, it & 1);
+            tc_fence_after();
+            if (ti.i == 0 && blockIdx.x == 0 && j < 7) QF_TS(4 + 4 * j);
 #pragma unroll
-          for (int kk = 0; kk < BC / 32; ++kk) {
-            const uint32_t vk = v_addr + 32 * kk * D;
-            const uint64_t db = make_smem_desc(vk, ones_addr - v_addr, 8 * D, kSwz);
-            mma_i8_ts(tO, tS + 8 * kk, db, kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < BC / 32; ++kk) {
+              const uint32_t vk = v_addr + 32 * kk * D;
+              const uint64_t db = make_smem_desc(vk, ones_addr - v_addr, 8 * D, kSwz);
+              mma_i8_ts(tO, tmem_base + sb * BC + 8 * kk, db, kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
+            }
+            mma_commit(&bar_kv_empty[st]);
+            mma_commit(bar_o_full);
+          };
+          issue_qk(0);
+          for (int j = 0; j < Tc; ++j) {
+            if (C::kNumS == 2 && j + 1 < Tc) issue_qk(j + 1);
+            issue_pv(j);
+            if (C::kNumS == 1 && j + 1 < Tc) issue_qk(j + 1);
           }
-          mma_commit(&bar_kv_empty[st]);
-          mma_commit(bar_o_full);
         }
       }
-    } else if (warp >= kSoftmaxWarp0) {
-      if (prm.q_shift == 0 && prm.p_pre == 0)
-        softmax_rows<D, BC, PACKED, true>(args, prm, tmem_base, bar_s_full, bar_p_full, bar_o_full,
-                                          problem, q0, warp, lane);
+    } else if (warp >= 4) {
+      if (prm.q_shift == 0 && static_cast<uint64_t>(prm.s_inv) * static_cast<uint64_t>(prm.m_p) < (1ull << 32))
+        softmax_role<D, BC, PACKED, true>(args, prm, tmem_base, bar_s_full, bar_p_full,
+                                          bar_o_full, red, recip, warp, lane);
       else
-        softmax_rows<D, BC, PACKED, false>(args, prm, tmem_base, bar_s_full, bar_p_full, bar_o_full,
-                                           problem, q0, warp, lane);
+        softmax_role<D, BC, PACKED, false>(args, prm, tmem_base, bar_s_full, bar_p_full,
+                                           bar_o_full, red, recip, warp, lane);
     }
   }
 
@@ -486,6 +725,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0 && blockIdx.x == 0) QF_TS(102);
   if (warp == 2) tmem_dealloc(tmem_base, kTmemCols);
 }
 
@@ -495,6 +735,7 @@ template <int D, int BC, bool PACKED>
 cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                           const AttnArgs& args, dim3 grid, cudaStream_t stream) {
   using L = SmemLayout<D, BC>;
+  using C = Cfg<D, BC, PACKED>;
   auto kern = qflash_attn_kernel<D, BC, PACKED>;
   static int configured[16] = {0};
   int dev = 0;
@@ -504,7 +745,7 @@ cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CU
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 16) configured[dev] = 1;
   }
-  kern<<<grid, kThreads, L::kAlloc, stream>>>(tq, tk, tv, args);
+  kern<<<grid, C::kThreads, L::kAlloc, stream>>>(tq, tk, tv, args);
   return cudaGetLastError();
 }
 

@@ -27,6 +27,10 @@ struct AttnArgs {
   int32_t N;        // sequence length
   int32_t P;        // number of problems
   int32_t Tc;       // ceil(N / B_c) KV tiles (generic kernel)
+  int32_t Tr;       // ceil(N / 128) query tiles per problem (generic kernel)
+  uint32_t tr_magic;  // ceil(2^32 / Tr): t / Tr == umulhi(t, tr_magic) for t < 2^32 / Tr
+  int32_t g_div;    // gridDim.x / Tr
+  int32_t g_mod;    // gridDim.x % Tr
   int32_t pad0;
   IntParams prm;    // used when dev_prm == nullptr
   const IntParams* dev_prm;  // device-derived constants (dscale path) or nullptr
@@ -35,6 +39,7 @@ struct AttnArgs {
   int32_t* dbg_s;  // [128][BC] raw S of KV tile 0
   int32_t* dbg_p;  // [128][BC/4] packed P words of KV tile 0
   int32_t* dbg_o;  // [128][D+1] final O and l before normalization
+  long long* dbg_t;  // [128] clock64 timeline of CTA (0, 0) (see QF_TS slots)
 };
 
 // Up to three tensors quantized by one launch pair (Q/K/V fusion).

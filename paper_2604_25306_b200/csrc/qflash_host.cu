@@ -14,13 +14,14 @@
 #include "../../include/qflash.h"
 #include "../../include/qflash_debug.h"
 #include "qflash_common.cuh"
+#include "qflash_params.cuh"
 
 namespace qf {
 cudaError_t launch_attention(int D, int BC, bool packed, const CUtensorMap& tq,
                              const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& args,
                              dim3 grid, cudaStream_t stream);
 cudaError_t launch_quantize(const QuantTensors& t, int ntensors, int dtype, int64_t numel,
-                            cudaStream_t stream);
+                            IntParams* prm_out, int32_t head_dim, cudaStream_t stream);
 cudaError_t launch_dequantize(const int8_t* xq, float scale, const float* scale_dev,
                               int64_t numel, float* y, cudaStream_t stream);
 }  // namespace qf
@@ -50,133 +51,10 @@ qflash_status cuda_fail(cudaError_t e, const char* where) {
   return QFLASH_ERR_CUDA;
 }
 
-// ------------------------------------------------------------------------
-// Constant derivation, shared by the host path and the one-thread device
-// kernel.  fp64 operations are written with explicit round-to-nearest
-// intrinsics on the device (no FMA contraction) and plain operators on the
-// host (compiled with -ffp-contract=off), so both evaluate the identical IEEE
-// expression ((s_q * s_k) * log2e) / sqrt(d) of Alg. 1.
-__host__ __device__ inline double dmul(double a, double b) {
-#ifdef __CUDA_ARCH__
-  return __dmul_rn(a, b);
-#else
-  return a * b;
-#endif
-}
-__host__ __device__ inline double ddiv(double a, double b) {
-#ifdef __CUDA_ARCH__
-  return __ddiv_rn(a, b);
-#else
-  return a / b;
-#endif
-}
-__host__ __device__ inline double dsqrt(double a) {
-#ifdef __CUDA_ARCH__
-  return __dsqrt_rn(a);
-#else
-  return std::sqrt(a);
-#endif
-}
-
-using u128 = unsigned __int128;
-
-// smallest L with 2^L >= x (x >= 1)
-__host__ __device__ inline int ceil_log2(uint64_t x) {
-  int L = 0;
-  while ((uint64_t(1) << L) < x) ++L;
-  return L;
-}
-
-__host__ __device__ inline int derive_core(float s_q, float s_k, int32_t d, qf::IntParams* o,
-                                           qflash_int_params* pub) {
-  if (!(s_q > 0.0f) || !(s_k > 0.0f) || !isfinite(s_q) || !isfinite(s_k))
-    return QFLASH_ERR_SCALE_RANGE;
-  const double log2e = 1.4426950408889634;
-  const double s = ddiv(dmul(dmul(static_cast<double>(s_q), static_cast<double>(s_k)), log2e),
-                        dsqrt(static_cast<double>(d)));
-  if (!(s >= ldexp(1.0, -24)) || !(s <= 0.5)) return QFLASH_ERR_SCALE_RANGE;
-  const int64_t s_inv = llround(ddiv(1.0, s));  // round half away (R1)
-  const double ratio = dmul(s, 127.0);          // s / s_P, s_P = 1/127 (R8)
-  int e = 0;
-  (void)frexp(ratio, &e);
-  const int32_t n = e - 1;                      // floor(log2 ratio)   (Eq. 9)
-  const int32_t r_p = 8 - n;                    // r = b - n           (Eq. 9)
-  const int64_t m_p = llround(ldexp(ratio, r_p));  // round(ratio 2^r) (Eq. 10)
-
-  const uint64_t D = static_cast<uint64_t>(s_inv);
-  // q1 = floor(t / s_inv) for t < 2^25 (t = m - S + s_inv, the kernel's range).
-  uint32_t q_magic;
-  int32_t q_shift;
-  {
-    const uint64_t m = ((uint64_t(1) << 32) + D - 1) / D;
-    const uint64_t err = m * D - (uint64_t(1) << 32);
-    // fast form: exact for t < 27 s_inv (q1 <= 26); beyond, the estimate is
-    // >= the true quotient (>= 26) and the shifted value is < 2^26, so y = 0
-    // exactly as in the oracle.
-    if (D <= (uint64_t(1) << 22) && (27 * D) * err < (uint64_t(1) << 32)) {
-      q_magic = static_cast<uint32_t>(m);
-      q_shift = 0;
-    } else {
-      const int L = ceil_log2(D);
-      const int sh = L > 7 ? L - 7 : 0;
-      const u128 num = (u128(1) << (32 + sh));
-      const u128 mm = (num + D - 1) / D;
-      q_magic = static_cast<uint32_t>(mm);
-      q_shift = sh;
-    }
-  }
-  // P = floor(y M_P / 2^r_P) = umulhi(y << p_pre, p_mul)
-  const int32_t p_pre = r_p < 10 ? 10 - r_p : 0;
-  const uint64_t p_mul = static_cast<uint64_t>(m_p) << (32 - r_p - p_pre);
-  const int64_t p_max = (s_inv * m_p) >> r_p;
-  // release: floor(n / s_inv) for n < 2^56
-  uint64_t rel_magic;
-  int32_t rel_shift;
-  {
-    const int L = ceil_log2(D);
-    const int sh = L > 8 ? L - 8 : 0;
-    const u128 num = (u128(1) << (64 + sh));
-    rel_magic = static_cast<uint64_t>((num + D - 1) / D);
-    rel_shift = sh;
-  }
-  if (o) {
-    o->status = 0;
-    o->s_inv = static_cast<int32_t>(s_inv);
-    o->q_magic = q_magic;
-    o->q_shift = q_shift;
-    o->p_mul = static_cast<uint32_t>(p_mul);
-    o->p_pre = p_pre;
-    o->rel_magic_lo = static_cast<uint32_t>(rel_magic);
-    o->rel_magic_hi = static_cast<uint32_t>(rel_magic >> 32);
-    o->rel_shift = rel_shift;
-    o->p_max = static_cast<int32_t>(p_max);
-    o->r_p = r_p;
-    o->m_p = static_cast<int32_t>(m_p);
-    o->n = n;
-    o->pad[0] = o->pad[1] = o->pad[2] = 0;
-    o->s = s;
-  }
-  if (pub) {
-    pub->s = s;
-    pub->s_inv = static_cast<int32_t>(s_inv);
-    pub->n = n;
-    pub->r_p = r_p;
-    pub->m_p = static_cast<int32_t>(m_p);
-    pub->q_magic = q_magic;
-    pub->q_shift = q_shift;
-    pub->p_mul = static_cast<uint32_t>(p_mul);
-    pub->p_pre = p_pre;
-    pub->p_max = static_cast<int32_t>(p_max);
-    pub->rel_magic = rel_magic;
-    pub->rel_shift = rel_shift;
-  }
-  return QFLASH_OK;
-}
-
 __global__ void derive_params_kernel(const float* __restrict__ scales, int32_t d,
                                      qf::IntParams* __restrict__ out) {
   qf::IntParams p;
-  const int st = derive_core(scales[0], scales[1], d, &p, nullptr);
+  const int st = qf::derive_core(scales[0], scales[1], d, &p, nullptr);
   if (st != QFLASH_OK) {
     memset(&p, 0, sizeof(p));
     p.status = st;
@@ -278,7 +156,7 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
                             int8_t* o, const qf::IntParams* host_prm,
                             const qf::IntParams* dev_prm, cudaStream_t stream,
                             int32_t* dbg_s = nullptr, int32_t* dbg_p = nullptr,
-                            int32_t* dbg_o = nullptr) {
+                            int32_t* dbg_o = nullptr, long long* dbg_t = nullptr) {
   const int P = shape->num_problems, N = shape->seq_len, d = shape->head_dim;
   bool packed;
   switch (variant) {
@@ -309,7 +187,29 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   args.dbg_s = dbg_s;
   args.dbg_p = dbg_p;
   args.dbg_o = dbg_o;
-  dim3 grid = packed ? dim3((P + 1) / 2, 1, 1) : dim3(P, (N + 127) / 128, 1);
+  args.dbg_t = dbg_t;
+  // Persistent grid: one CTA per SM, each walking tiles b, b + G, b + 2G, ...
+  const int64_t Tr = packed ? 1 : (N + 127) / 128;
+  const int64_t tiles = packed ? (P + 1) / 2 : static_cast<int64_t>(P) * Tr;
+  int sms = 0;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static int sm_cache[64];
+    if (dev >= 0 && dev < 64 && sm_cache[dev] > 0) {
+      sms = sm_cache[dev];
+    } else {
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (sms <= 0) sms = 148;
+      if (dev >= 0 && dev < 64) sm_cache[dev] = sms;
+    }
+  }
+  const int64_t G = tiles < sms ? tiles : sms;
+  args.Tr = static_cast<int32_t>(Tr);
+  args.tr_magic = Tr > 1 ? static_cast<uint32_t>(((1ull << 32) + Tr - 1) / Tr) : 0u;
+  args.g_div = static_cast<int32_t>(G / Tr);
+  args.g_mod = static_cast<int32_t>(G % Tr);
+  dim3 grid(static_cast<unsigned>(G), 1, 1);
   cudaError_t e = qf::launch_attention(d, packed ? 128 : bc, packed, tq, tk, tv, args, grid, stream);
   if (e != cudaSuccess) return cuda_fail(e, "attention launch");
   return QFLASH_OK;
@@ -327,7 +227,7 @@ qflash_status attention_host_scales(const int8_t* q, const int8_t* k, const int8
   if (!(s_v > 0.0f) || !std::isfinite(s_v))
     return fail(QFLASH_ERR_SCALE_RANGE, "s_v must be positive and finite");
   qf::IntParams prm;
-  const int rc = derive_core(s_q, s_k, shape->head_dim, &prm, nullptr);
+  const int rc = qf::derive_core(s_q, s_k, shape->head_dim, &prm, nullptr);
   if (rc != QFLASH_OK)
     return fail(static_cast<qflash_status>(rc),
                 "s = s_q s_k log2(e)/sqrt(d) outside [2^-24, 0.5] (s_q=%g, s_k=%g, d=%d)",
@@ -365,7 +265,7 @@ qflash_status qflash_derive_params(float s_q, float s_k, int32_t head_dim, qflas
   if (!out) return fail(QFLASH_ERR_INVALID_ARGUMENT, "out is NULL");
   if (head_dim != 32 && head_dim != 64 && head_dim != 128)
     return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "head_dim %d not in {32, 64, 128}", head_dim);
-  const int rc = derive_core(s_q, s_k, head_dim, nullptr, out);
+  const int rc = qf::derive_core(s_q, s_k, head_dim, nullptr, out);
   if (rc != QFLASH_OK) return fail(static_cast<qflash_status>(rc), "scale out of range");
   return QFLASH_OK;
 }
@@ -421,7 +321,8 @@ qflash_status qflash_attention_int8_dscale(const int8_t* q, const int8_t* k, con
 }
 
 static qflash_status quantize_impl(const void* const* xs, int8_t* const* xqs, float* const* scales,
-                                   int nt, qflash_dtype dtype, int64_t numel, cudaStream_t stream) {
+                                   int nt, qflash_dtype dtype, int64_t numel, cudaStream_t stream,
+                                   qf::IntParams* prm_out = nullptr, int32_t head_dim = 0) {
   if (numel < 0) return fail(QFLASH_ERR_INVALID_ARGUMENT, "numel < 0");
   if (dtype != QFLASH_F32 && dtype != QFLASH_BF16 && dtype != QFLASH_F16)
     return fail(QFLASH_ERR_INVALID_ARGUMENT, "unknown dtype %d", static_cast<int>(dtype));
@@ -440,7 +341,7 @@ static qflash_status quantize_impl(const void* const* xs, int8_t* const* xqs, fl
     t.xq[i] = xqs[i];
     t.scale[i] = scales[i];
   }
-  cudaError_t e = qf::launch_quantize(t, nt, static_cast<int>(dtype), numel, stream);
+  cudaError_t e = qf::launch_quantize(t, nt, static_cast<int>(dtype), numel, prm_out, head_dim, stream);
   if (e != cudaSuccess) return cuda_fail(e, "quantize launch");
   return QFLASH_OK;
 }
@@ -485,6 +386,41 @@ qflash_status qflash_quantize_qkv(const void* q, const void* k, const void* v, q
   return quantize_impl(xs, xqs, scs, 3, dtype, numel, reinterpret_cast<cudaStream_t>(stream));
 }
 
+qflash_status qflash_quantize_qkv_prepare(const void* q, const void* k, const void* v,
+                                          qflash_dtype dtype, int64_t numel, int8_t* q_q,
+                                          int8_t* k_q, int8_t* v_q, float* scales_dev,
+                                          int32_t head_dim, void* workspace_dev,
+                                          qflash_stream_t stream) {
+  if (!scales_dev) return fail(QFLASH_ERR_INVALID_ARGUMENT, "scales_dev is NULL");
+  if (!workspace_dev || !aligned16(workspace_dev))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "workspace_dev NULL or misaligned");
+  if (head_dim != 32 && head_dim != 64 && head_dim != 128)
+    return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "head_dim %d not in {32, 64, 128}", head_dim);
+  const void* xs[3] = {q, k, v};
+  int8_t* xqs[3] = {q_q, k_q, v_q};
+  float* scs[3] = {scales_dev, scales_dev + 1, scales_dev + 2};
+  return quantize_impl(xs, xqs, scs, 3, dtype, numel, reinterpret_cast<cudaStream_t>(stream),
+                       reinterpret_cast<qf::IntParams*>(workspace_dev), head_dim);
+}
+
+qflash_status qflash_attention_int8_prepared(const int8_t* q, const int8_t* k, const int8_t* v,
+                                             const qflash_attn_shape* shape,
+                                             qflash_variant variant, int8_t* o,
+                                             const void* workspace_dev, qflash_stream_t stream) {
+  int bc = 0;
+  qflash_status st = validate_shape(shape, &bc);
+  if (st != QFLASH_OK) return st;
+  const int64_t bytes = static_cast<int64_t>(shape->num_problems) * shape->seq_len * shape->head_dim;
+  if ((st = validate_qkvo(q, k, v, o, bytes)) != QFLASH_OK) return st;
+  if (!workspace_dev || !aligned16(workspace_dev))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "workspace_dev NULL or misaligned");
+  int dev = 0;
+  if ((st = check_device(&dev)) != QFLASH_OK) return st;
+  return launch_common(q, k, v, shape, bc, variant, o, nullptr,
+                       reinterpret_cast<const qf::IntParams*>(workspace_dev),
+                       reinterpret_cast<cudaStream_t>(stream));
+}
+
 static qflash_status dequant_impl(const int8_t* x_q, float scale, const float* scale_dev,
                                   int64_t numel, float* y, cudaStream_t stream) {
   if (!x_q || !y) return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL pointer");
@@ -518,17 +454,18 @@ qflash_status qflash_dequantize_dscale(const int8_t* x_q, const float* scale_dev
 qflash_status qflash_debug_attention(const int8_t* q, const int8_t* k, const int8_t* v, float s_q,
                                      float s_k, const qflash_attn_shape* shape,
                                      qflash_variant variant, int8_t* o, int32_t* dbg_s,
-                                     int32_t* dbg_p, int32_t* dbg_o, qflash_stream_t stream) {
+                                     int32_t* dbg_p, int32_t* dbg_o, long long* dbg_t,
+                                     qflash_stream_t stream) {
   int bc = 0;
   qflash_status st = validate_shape(shape, &bc);
   if (st != QFLASH_OK) return st;
   qf::IntParams prm;
-  const int rc = derive_core(s_q, s_k, shape->head_dim, &prm, nullptr);
+  const int rc = qf::derive_core(s_q, s_k, shape->head_dim, &prm, nullptr);
   if (rc != QFLASH_OK) return fail(static_cast<qflash_status>(rc), "scale out of range");
   int dev = 0;
   if ((st = check_device(&dev)) != QFLASH_OK) return st;
   return launch_common(q, k, v, shape, bc, variant, o, &prm, nullptr,
-                       reinterpret_cast<cudaStream_t>(stream), dbg_s, dbg_p, dbg_o);
+                       reinterpret_cast<cudaStream_t>(stream), dbg_s, dbg_p, dbg_o, dbg_t);
 }
 
 }  // extern "C"

@@ -2,15 +2,20 @@
 // dequantizer, HBM-bound streaming kernels for sm_100a.
 //
 // Quantization of T tensors (T = 1, or 3 for fused Q/K/V) is two launches:
-//   1. amax: every block reduces max|x| (as IEEE bit patterns, so NaN
-//      propagates) and atomically maxes s_b = fl32(amax_b / 127) into the
-//      caller's scale slot (pre-zeroed).  fl32 division is monotone, so the
-//      slot ends at fl32(max_b amax_b / 127) = fl32(amax / 127).
-//   2. quantize: x^ = sat8(roundf(__fdiv_rn(x, s))), with s = 1/127 when the
-//      slot is 0 (all-zero tensor, reading R3).  Block 0 writes 1/127 back in
-//      that case; every block treats 0 and 1/127 identically, so the write is
-//      race-free.
-// Loads are 16-byte vectors, grid-strided over a grid sized to the SM count.
+//   1. amax: each block reduces max|x| (fmaxf with |.| source modifier: one
+//      FMNMX per element) and atomically maxes s_b = fl32(amax_b / 127) into the
+//      caller's pre-zeroed scale slot.  fl32 division is monotone, so the slot
+//      ends at fl32(max_b amax_b / 127) = fl32(amax / 127).  Grids are sized to
+//      ~8 blocks per SM in total, so each slot sees a few hundred atomics.
+//   2. quantize: x^ = sat8(roundf(fl32(x / s))) (readings R1, R2) with s = 1/127
+//      when the slot is 0 (R3).  Exact fast path: q = RN(x * RN(1/s)) is within
+//      2^-15 of fl32(x / s) for |x / s| <= 128, so whenever q is farther than
+//      0.5 - 2^-14 from a half-integer, rint(q) == roundf(fl32(x / s)); the
+//      remaining elements (probability ~2^-13) take the IEEE division.  Block 0
+//      of tensor 0 can also derive the attention's integer constants from the
+//      final s_q, s_k (qflash_quantize_qkv_prepare) so the step needs no extra
+//      launch.
+// 16 elements per thread and iteration (64 B of fp32 in flight, one 16-B store).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -18,35 +23,42 @@
 #include <cstdint>
 
 #include "qflash_common.cuh"
+#include "qflash_params.cuh"
 
 namespace qf {
 
 constexpr int kQThreads = 256;
-
+constexpr int kQElems = 16;  // elements per thread per iteration
 
 template <typename T>
-struct Vec;  // 16-byte vector of T widened to fp32
+struct Load16;  // 16 consecutive elements widened (exactly) to fp32
 template <>
-struct Vec<float> {
-  static constexpr int kN = 4;
-  __device__ static void load(const void* base, int64_t i, float* out) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(base) + i);
-    out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+struct Load16<float> {
+  __device__ static void load(const void* base, int64_t i, float* o) {
+    const float4* p = reinterpret_cast<const float4*>(base) + 4 * i;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 v = __ldg(p + k);
+      o[4 * k] = v.x; o[4 * k + 1] = v.y; o[4 * k + 2] = v.z; o[4 * k + 3] = v.w;
+    }
   }
   __device__ static float load1(const void* base, int64_t i) {
     return __ldg(reinterpret_cast<const float*>(base) + i);
   }
 };
 template <>
-struct Vec<__nv_bfloat16> {
-  static constexpr int kN = 8;
-  __device__ static void load(const void* base, int64_t i, float* out) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(base) + i);
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+struct Load16<__nv_bfloat16> {
+  __device__ static void load(const void* base, int64_t i, float* o) {
+    const uint4* p = reinterpret_cast<const uint4*>(base) + 2 * i;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      out[2 * k] = __uint_as_float(w[k] << 16);
-      out[2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
+    for (int k = 0; k < 2; ++k) {
+      const uint4 v = __ldg(p + k);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        o[8 * k + 2 * e] = __uint_as_float(w[e] << 16);
+        o[8 * k + 2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+      }
     }
   }
   __device__ static float load1(const void* base, int64_t i) {
@@ -55,16 +67,19 @@ struct Vec<__nv_bfloat16> {
   }
 };
 template <>
-struct Vec<__half> {
-  static constexpr int kN = 8;
-  __device__ static void load(const void* base, int64_t i, float* out) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(base) + i);
-    const __half2* h = reinterpret_cast<const __half2*>(&v);
+struct Load16<__half> {
+  __device__ static void load(const void* base, int64_t i, float* o) {
+    const uint4* p = reinterpret_cast<const uint4*>(base) + 2 * i;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float2 f = __half22float2(h[k]);  // exact widening
-      out[2 * k] = f.x;
-      out[2 * k + 1] = f.y;
+    for (int k = 0; k < 2; ++k) {
+      const uint4 v = __ldg(p + k);
+      const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(h[e]);  // exact widening
+        o[8 * k + 2 * e] = f.x;
+        o[8 * k + 2 * e + 1] = f.y;
+      }
     }
   }
   __device__ static float load1(const void* base, int64_t i) {
@@ -72,79 +87,106 @@ struct Vec<__half> {
   }
 };
 
-__device__ __forceinline__ uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
-
-// scale from amax (as stored in the slot): fl32(amax / 127); 0 stays 0 here.
-__device__ __forceinline__ float scale_of_amax_bits(uint32_t amax_bits) {
-  return __fdiv_rn(__uint_as_float(amax_bits), 127.0f);
+__device__ __forceinline__ const void* pick(const QuantTensors& t, int i) {
+  return i == 0 ? t.x[0] : (i == 1 ? t.x[1] : t.x[2]);
+}
+__device__ __forceinline__ int8_t* pick_q(const QuantTensors& t, int i) {
+  return i == 0 ? t.xq[0] : (i == 1 ? t.xq[1] : t.xq[2]);
+}
+__device__ __forceinline__ float* pick_s(const QuantTensors& t, int i) {
+  return i == 0 ? t.scale[0] : (i == 1 ? t.scale[1] : t.scale[2]);
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kQThreads) amax_kernel(QuantTensors t, int64_t numel) {
   const int ti = blockIdx.y;
-  const void* x = t.x[ti];
-  constexpr int kN = Vec<T>::kN;
-  const int64_t nvec = numel / kN;
-  uint32_t m = 0;
+  const void* x = pick(t, ti);
+  const int64_t nv = numel / kQElems;
+  float m[4] = {0.f, 0.f, 0.f, 0.f};
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec; i += stride) {
-    float v[kN];
-    Vec<T>::load(x, i, v);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    float v[kQElems];
+    Load16<T>::load(x, i, v);
 #pragma unroll
-    for (int k = 0; k < kN; ++k) m = max(m, abs_bits(v[k]));
+    for (int k = 0; k < kQElems; ++k) m[k & 3] = fmaxf(m[k & 3], fabsf(v[k]));
   }
-  for (int64_t i = nvec * kN + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < numel; i += stride)
-    m = max(m, abs_bits(Vec<T>::load1(x, i)));
+  for (int64_t i = nv * kQElems + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < numel;
+       i += stride)
+    m[0] = fmaxf(m[0], fabsf(Load16<T>::load1(x, i)));
+  float mm = fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  __shared__ uint32_t red[kQThreads / 32];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  for (int o = 16; o > 0; o >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+  __shared__ float red[kQThreads / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mm;
   __syncthreads();
   if (threadIdx.x == 0) {
-    uint32_t b = red[0];
-    for (int w = 1; w < kQThreads / 32; ++w) b = max(b, red[w]);
-    // s_b = fl32(amax_b / 127) is monotone in amax_b; non-negative floats
-    // (and NaN, whose bits exceed +inf) order like their bit patterns.
-    const float sb = scale_of_amax_bits(b);
-    atomicMax(reinterpret_cast<unsigned int*>(t.scale[ti]), __float_as_uint(sb));
+    float b = red[0];
+#pragma unroll
+    for (int w = 1; w < kQThreads / 32; ++w) b = fmaxf(b, red[w]);
+    // s_b = fl32(amax_b / 127) is monotone in amax_b; non-negative floats order
+    // like their bit patterns, so an unsigned atomicMax on the bits is a float max.
+    const float sb = __fdiv_rn(b, 127.0f);
+    atomicMax(reinterpret_cast<unsigned int*>(pick_s(t, ti)), __float_as_uint(sb));
   }
 }
 
-__device__ __forceinline__ int32_t quant_one(float x, float s) {
-  float r = roundf(__fdiv_rn(x, s));  // IEEE division, half away from zero (R1, R2)
-  r = fminf(fmaxf(r, -128.0f), 127.0f);
-  return static_cast<int32_t>(r);
+// roundf(fl32(x / s)) exactly (see the header comment).
+__device__ __forceinline__ int32_t quant_one(float x, float s, float r) {
+  const float q = __fmul_rn(x, r);
+  const float fi = rintf(q);
+  if (fabsf(q - fi) < 0.49993896484375f)  // 0.5 - 2^-14
+    return static_cast<int32_t>(fi);
+  return static_cast<int32_t>(roundf(__fdiv_rn(x, s)));  // rare: near a half-integer
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kQThreads) quantize_kernel(QuantTensors t, int64_t numel) {
+__global__ void __launch_bounds__(kQThreads)
+    quantize_kernel(QuantTensors t, int64_t numel, IntParams* prm_out, int32_t head_dim) {
   const int ti = blockIdx.y;
-  const void* x = t.x[ti];
-  int8_t* xq = t.xq[ti];
-  float s = *reinterpret_cast<volatile float*>(t.scale[ti]);
+  const void* x = pick(t, ti);
+  int8_t* xq = pick_q(t, ti);
+  float s = *reinterpret_cast<volatile float*>(pick_s(t, ti));
   if (s == 0.0f) s = 1.0f / 127.0f;  // all-zero tensor (R3)
-  if (blockIdx.x == 0 && threadIdx.x == 0) *t.scale[ti] = s;
-  constexpr int kN = Vec<T>::kN;
-  const int64_t nvec = numel / kN;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec; i += stride) {
-    float v[kN];
-    Vec<T>::load(x, i, v);
-    uint32_t w[kN / 4];
-#pragma unroll
-    for (int k = 0; k < kN / 4; ++k) {
-      const int32_t a = quant_one(v[4 * k], s), b = quant_one(v[4 * k + 1], s);
-      const int32_t c = quant_one(v[4 * k + 2], s), d = quant_one(v[4 * k + 3], s);
-      w[k] = (static_cast<uint32_t>(a) & 0xFFu) | ((static_cast<uint32_t>(b) & 0xFFu) << 8) |
-             ((static_cast<uint32_t>(c) & 0xFFu) << 16) | (static_cast<uint32_t>(d) << 24);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *pick_s(t, ti) = s;
+    if (prm_out != nullptr && ti == 0) {
+      // integer constants of the attention from the final s_q, s_k
+      float sq = *reinterpret_cast<volatile float*>(t.scale[0]);
+      float sk = *reinterpret_cast<volatile float*>(t.scale[1]);
+      if (sq == 0.0f) sq = 1.0f / 127.0f;
+      if (sk == 0.0f) sk = 1.0f / 127.0f;
+      IntParams p;
+      const int st = derive_core(sq, sk, head_dim, &p, nullptr);
+      if (st != QFLASH_OK) {
+        memset(&p, 0, sizeof(p));
+        p.status = st;
+      }
+      *prm_out = p;
     }
-    if constexpr (kN == 4)
-      reinterpret_cast<uint32_t*>(xq)[i] = w[0];
-    else
-      reinterpret_cast<uint2*>(xq)[i] = make_uint2(w[0], w[1]);
   }
-  for (int64_t i = nvec * kN + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < numel; i += stride)
-    xq[i] = static_cast<int8_t>(quant_one(Vec<T>::load1(x, i), s));
+  const float r = __frcp_rn(s);
+  const int64_t nv = numel / kQElems;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    float v[kQElems];
+    Load16<T>::load(x, i, v);
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int32_t a = quant_one(v[4 * k], s, r), b = quant_one(v[4 * k + 1], s, r);
+      const int32_t c = quant_one(v[4 * k + 2], s, r), d = quant_one(v[4 * k + 3], s, r);
+      uint32_t hi, lo;
+      asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(d), "r"(c));
+      asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(lo) : "r"(b), "r"(a), "r"(hi));
+      w[k] = lo;
+    }
+    reinterpret_cast<uint4*>(xq)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  for (int64_t i = nv * kQElems + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < numel;
+       i += stride) {
+    const int32_t v = quant_one(Load16<T>::load1(x, i), s, r);
+    xq[i] = static_cast<int8_t>(max(-128, min(127, v)));
+  }
 }
 
 __global__ void __launch_bounds__(kQThreads)
@@ -169,7 +211,7 @@ __global__ void __launch_bounds__(kQThreads)
     y[i] = __fmul_rn(s, static_cast<float>(xq[i]));
 }
 
-static int stream_grid(int64_t work_items) {
+static int num_sms() {
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
@@ -177,8 +219,14 @@ static int stream_grid(int64_t work_items) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  int64_t blocks = (work_items + kQThreads - 1) / kQThreads;
-  const int64_t cap = static_cast<int64_t>(sms) * 8;  // 8 x 256 threads per SM
+  return sms;
+}
+
+// Blocks per tensor: enough 256-thread blocks for one pass over the data, capped
+// at ~8 resident blocks per SM in total over the `ntensors` tensors.
+static int stream_grid(int64_t thread_items, int ntensors) {
+  int64_t blocks = (thread_items + kQThreads - 1) / kQThreads;
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 8 / ntensors;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   return static_cast<int>(blocks);
@@ -186,25 +234,30 @@ static int stream_grid(int64_t work_items) {
 
 // dtype: 0 f32, 1 bf16, 2 f16.  Requires 16-byte aligned x and xq (checked by host).
 cudaError_t launch_quantize(const QuantTensors& t, int ntensors, int dtype, int64_t numel,
-                            cudaStream_t stream) {
-  for (int i = 0; i < ntensors; ++i) {
-    cudaError_t e = cudaMemsetAsync(t.scale[i], 0, sizeof(float), stream);
+                            IntParams* prm_out, int32_t head_dim, cudaStream_t stream) {
+  const bool contiguous = ntensors == 3 && t.scale[1] == t.scale[0] + 1 && t.scale[2] == t.scale[0] + 2;
+  if (contiguous) {
+    cudaError_t e = cudaMemsetAsync(t.scale[0], 0, 3 * sizeof(float), stream);
     if (e != cudaSuccess) return e;
+  } else {
+    for (int i = 0; i < ntensors; ++i) {
+      cudaError_t e = cudaMemsetAsync(t.scale[i], 0, sizeof(float), stream);
+      if (e != cudaSuccess) return e;
+    }
   }
-  const int vec = (dtype == 0) ? 4 : 8;
-  dim3 grid(stream_grid((numel + vec - 1) / vec), ntensors);
+  dim3 grid(stream_grid((numel + kQElems - 1) / kQElems, ntensors), ntensors);
   switch (dtype) {
     case 0:
       amax_kernel<float><<<grid, kQThreads, 0, stream>>>(t, numel);
-      quantize_kernel<float><<<grid, kQThreads, 0, stream>>>(t, numel);
+      quantize_kernel<float><<<grid, kQThreads, 0, stream>>>(t, numel, prm_out, head_dim);
       break;
     case 1:
       amax_kernel<__nv_bfloat16><<<grid, kQThreads, 0, stream>>>(t, numel);
-      quantize_kernel<__nv_bfloat16><<<grid, kQThreads, 0, stream>>>(t, numel);
+      quantize_kernel<__nv_bfloat16><<<grid, kQThreads, 0, stream>>>(t, numel, prm_out, head_dim);
       break;
     case 2:
       amax_kernel<__half><<<grid, kQThreads, 0, stream>>>(t, numel);
-      quantize_kernel<__half><<<grid, kQThreads, 0, stream>>>(t, numel);
+      quantize_kernel<__half><<<grid, kQThreads, 0, stream>>>(t, numel, prm_out, head_dim);
       break;
     default:
       return cudaErrorInvalidValue;
@@ -214,7 +267,7 @@ cudaError_t launch_quantize(const QuantTensors& t, int ntensors, int dtype, int6
 
 cudaError_t launch_dequantize(const int8_t* xq, float scale, const float* scale_dev, int64_t numel,
                               float* y, cudaStream_t stream) {
-  dim3 grid(stream_grid((numel + 15) / 16));
+  dim3 grid(stream_grid((numel + 15) / 16, 1));
   dequantize_kernel<<<grid, kQThreads, 0, stream>>>(xq, scale, scale_dev, numel, y);
   return cudaGetLastError();
 }

@@ -26,7 +26,7 @@ def run(P, N, d, bkv, variant, kind="uniform", sq=0.05, sk=0.05, seed=0):
     sh = _lib.AttnShape(P, N, d, bkv)
     st = _lib.lib().qflash_debug_attention(dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), sq, sk,
                                            ctypes.byref(sh), variant, o.data_ptr(), ds.data_ptr(),
-                                           dp.data_ptr(), do.data_ptr(), None)
+                                           dp.data_ptr(), do.data_ptr(), None, None)
     torch.cuda.synchronize()
     print(f"--- P={P} N={N} d={d} bkv={bkv} variant={variant} kind={kind}: status {st} {_lib.last_error()}")
     S_gpu = ds.cpu().numpy().reshape(128, BC)

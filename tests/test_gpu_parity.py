@@ -1,0 +1,304 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Integer outputs must be bit-exact; the quantizer's int8
+bytes and fp32 scale bit-identical; the dequantizer bit-identical (one IEEE fp32
+multiply on both sides).  Full-size configs are checked on sampled rows the
+oracle computes one by one, in the launch configuration bench.py times.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU boxes too
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2604_25306_b200 as qf  # noqa: E402
+from paper_2604_25306_b200 import _lib  # noqa: E402
+from paper_2604_25306_b200.inputs import (CATALOG, gen_int8_qkv, gen_real_qkv,  # noqa: E402
+                                          gen_workload)
+
+
+def _dev(*arrs):
+    return [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in arrs]
+
+
+def _gpu_attention(q, k, v, sq, sk, sv=0.03, block_kv=128, variant="auto"):
+    dq, dk, dv = _dev(q, k, v)
+    out, s_o = qf.qflash_attention_int8(dq, dk, dv, sq, sk, sv, block_kv=block_kv, variant=variant)
+    torch.cuda.synchronize()
+    assert s_o == np.float32(sv)
+    return out.cpu().numpy()
+
+
+# ------------------------------------------------------------------ edge grid
+N_GRID = [1, 2, 31, 32, 33, 48, 49, 50, 63, 64, 65, 127, 128, 129, 196, 197, 255, 256, 257]
+
+
+@pytest.mark.parametrize("N", N_GRID)
+@pytest.mark.parametrize("d", [32, 64, 128])
+def test_edge_seq_lengths(orc, N, d):
+    q, k, v = gen_int8_qkv(3, N, d, seed=N + d)
+    for bkv in (64, 128, 256):
+        ref = orc.attention(q, k, v, 0.05, 0.05, block_kv=bkv)
+        got = _gpu_attention(q, k, v, 0.05, 0.05, block_kv=bkv, variant="generic")
+        assert np.array_equal(got, ref), (N, d, bkv, int((got != ref).sum()))
+        if N <= 64:
+            got_p = _gpu_attention(q, k, v, 0.05, 0.05, block_kv=bkv, variant="packed")
+            assert np.array_equal(got_p, ref)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "all_min", "constant_rows", "one_hot", "ties", "zeros"])
+@pytest.mark.parametrize("N,d", [(197, 64), (49, 32), (1025, 64), (300, 128)])
+def test_adversarial_sets(orc, kind, N, d):
+    q, k, v = gen_int8_qkv(2, N, d, seed=11, kind=kind)
+    for (sq, sk) in [(0.05, 0.05), (0.003, 0.004), (0.2, 0.25)]:
+        ref = orc.attention(q, k, v, sq, sk, block_kv=128)
+        got = _gpu_attention(q, k, v, sq, sk, block_kv=128)
+        assert np.array_equal(got, ref), (kind, sq, int((got != ref).sum()))
+
+
+@pytest.mark.parametrize("s", [2.0 ** -24 * 1.01, 1e-6, 3e-5, 2e-4, 1e-3, 7.7e-3, 0.05, 0.3, 0.5])
+def test_scale_range(orc, s):
+    # sweep s = s_q s_k log2e / sqrt(d) over the ABI range: exercises the fast and
+    # general quotient magics, p_pre > 0 (large s) and the 127 clamp.
+    d = 64
+    sq = float(np.sqrt(s * np.sqrt(d) / 1.4426950408889634))
+    q, k, v = gen_int8_qkv(2, 197, d, seed=3)
+    try:
+        ref = orc.attention(q, k, v, sq, sq, block_kv=64)
+    except ValueError:
+        pytest.skip("outside the range")
+    got = _gpu_attention(q, k, v, sq, sq, block_kv=64)
+    assert np.array_equal(got, ref)
+
+
+def test_p_clamp_regime(orc):
+    # s = 0.34: s_inv = 3 and s * s_inv = 1.02, so P = floor(y M_P / 2^r_P) reaches
+    # 129 at y = s_inv before the 127 clamp of reading R8.
+    sq = float(np.sqrt(0.34 * np.sqrt(32) / 1.4426950408889634))
+    p = qf.qflash_derive_params(sq, sq, 32)
+    assert p["s_inv"] == 3 and p["p_max"] > 127
+    q, k, v = gen_int8_qkv(2, 97, 32, seed=5)
+    ref = orc.attention(q, k, v, sq, sq, block_kv=64)
+    got = _gpu_attention(q, k, v, sq, sq, block_kv=64)
+    assert np.array_equal(got, ref)
+
+
+# ------------------------------------------------------------------ workloads
+@pytest.mark.parametrize("name,batch", [("A1", 1), ("A2", 1), ("A3", 1), ("A4", 1), ("A5", 1),
+                                        ("A6", 1), ("A7", 1), ("A2", 8), ("A7", 8),
+                                        ("SwinB-s3", 1), ("SwinB-s4", 8)])
+def test_workload_parity(orc, name, batch):
+    q, k, v = gen_workload(name, batch, seed=0)
+    qq, sq = orc.quantize(q)
+    kq, sk = orc.quantize(k)
+    vq, sv = orc.quantize(v)
+    ref = orc.attention(qq, kq, vq, sq, sk, block_kv=128, nthreads=8)
+    got = _gpu_attention(qq, kq, vq, sq, sk, sv, block_kv=128)
+    assert np.array_equal(got, ref)
+
+
+def test_full_size_a3_b8_exact(orc):
+    # BASELINE configs[1] at full size, every element (the oracle takes ~1 s).
+    q, k, v = gen_workload("A3", 8, seed=0)
+    qq, sq = orc.quantize(q)
+    kq, sk = orc.quantize(k)
+    vq, sv = orc.quantize(v)
+    ref = orc.attention(qq, kq, vq, sq, sk, block_kv=128, nthreads=8)
+    got = _gpu_attention(qq, kq, vq, sq, sk, sv)
+    assert np.array_equal(got, ref)
+
+
+def test_full_size_swin_b8_exact(orc):
+    for name in ("A4", "SwinB-s1"):
+        q, k, v = gen_workload(name, 8, seed=0)
+        qq, sq = orc.quantize(q)
+        kq, sk = orc.quantize(k)
+        vq, sv = orc.quantize(v)
+        ref = orc.attention(qq, kq, vq, sq, sk, block_kv=128, nthreads=8)
+        got = _gpu_attention(qq, kq, vq, sq, sk, sv)
+        assert np.array_equal(got, ref)
+
+
+def test_full_size_l14_b64_sampled(orc):
+    # configs[4] at full size (1024 problems x 1025 tokens): sampled rows.
+    w = CATALOG["L14"]
+    P = w.problems(64)
+    q, k, v = gen_real_qkv(P, w.seq_len, w.head_dim, seed=0)
+    qq, sq = orc.quantize(q)
+    kq, sk = orc.quantize(k)
+    vq, sv = orc.quantize(v)
+    got = _gpu_attention(qq, kq, vq, sq, sk, sv)
+    rng = np.random.default_rng(0)
+    for p in list(rng.integers(0, P, 6)) + [0, P - 1]:
+        for (a, b) in [(0, 3), (126, 130), (1020, 1025)]:
+            ref = orc.attention_rows(qq, kq, vq, sq, sk, int(p), a, b)
+            assert np.array_equal(got[p, a:b], ref), (p, a)
+
+
+# ------------------------------------------------------------------ quantizer
+@pytest.mark.parametrize("n", [1, 3, 16, 1000, 4099, 1 << 20, 1_210_368])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
+def test_quantizer_bit_exact(orc, n, dtype):
+    rng = np.random.default_rng(n)
+    x = (rng.standard_normal(n) * 2.5).astype(np.float32)
+    if dtype == "f32":
+        xt = torch.from_numpy(x).cuda()
+        ref_in = x
+    elif dtype == "bf16":
+        xt = torch.from_numpy(x).to(torch.bfloat16).cuda()
+        ref_in = xt.cpu().view(torch.int16).numpy().view(np.uint16)
+    else:
+        xt = torch.from_numpy(x).to(torch.float16).cuda()
+        ref_in = xt.cpu().float().numpy()   # f16 -> f32 widening is exact
+    xq, s = qf.qflash_quantize_per_tensor(xt)
+    rq, rs = orc.quantize(ref_in)
+    assert np.float32(s.item()).view(np.uint32) == np.float32(rs).view(np.uint32)
+    assert np.array_equal(xq.cpu().numpy(), rq)
+
+
+def test_quantizer_zero_and_ties(orc):
+    z = torch.zeros(1001, device="cuda")
+    xq, s = qf.qflash_quantize_per_tensor(z)
+    assert s.item() == np.float32(1 / 127) and not xq.any()
+    x = torch.tensor([127.0, 2.5, -2.5, 0.5, -0.5, 1.5, -127.0, 126.5] * 3, device="cuda")
+    xq, s = qf.qflash_quantize_per_tensor(x)
+    assert s.item() == 1.0
+    assert xq.cpu().tolist()[:8] == [127, 3, -3, 1, -1, 2, -127, 127]
+
+
+def test_quantizer_near_half_integers(orc):
+    # values whose quotient x / s lies within a few ulps of k + 1/2: exercises the
+    # exact slow path of the quantizer's rounding (quant_one) -- bit-exact vs the
+    # oracle's IEEE division + roundf (readings R1, R2).
+    s = np.float32(100.0) / np.float32(127.0)
+    vals = [np.float32(100.0)]
+    for k in range(-127, 127):
+        c = np.float32((k + 0.5) * float(s))
+        v = c
+        for _ in range(4):
+            v = np.nextafter(v, np.float32(-np.inf))
+        for _ in range(9):
+            vals.append(v)
+            v = np.nextafter(v, np.float32(np.inf))
+    x = np.array(vals, np.float32)
+    x = x[np.abs(x) <= 100.0]
+    xq, sg = qf.qflash_quantize_per_tensor(torch.from_numpy(x).cuda())
+    rq, rs = orc.quantize(x)
+    assert np.float32(sg.item()) == np.float32(rs) == s
+    assert np.array_equal(xq.cpu().numpy(), rq)
+
+
+def test_prepare_path_constants_and_output(orc):
+    q, k, v = (torch.from_numpy(a).cuda() for a in gen_workload("A2", 1, seed=6))
+    qq, kq, vq, scales, ws = qf.qflash_quantize_qkv_prepare(q, k, v)
+    out = qf.qflash_attention_int8_prepared(qq, kq, vq, ws)
+    torch.cuda.synchronize()
+    s = scales.cpu().numpy()
+    hp = qf.qflash_derive_params(float(s[0]), float(s[1]), 64)
+    w = ws.cpu().numpy()
+    assert w[0] == 0 and w[1] == hp["s_inv"] and np.uint32(w[2]) == hp["q_magic"]
+    assert w[3] == hp["q_shift"] and np.uint32(w[4]) == hp["p_mul"] and w[5] == hp["p_pre"]
+    ref, _ = qf.qflash_attention_int8(qq, kq, vq, float(s[0]), float(s[1]), float(s[2]))
+    assert torch.equal(out, ref)
+
+
+def test_quantize_qkv_matches_single(orc):
+    q, k, v = (torch.from_numpy(a).cuda() for a in gen_workload("A2", 8, seed=3))
+    qq, kq, vq, scales = qf.qflash_quantize_qkv(q, k, v)
+    for t, tq, s in zip((q, k, v), (qq, kq, vq), scales.cpu().numpy()):
+        rq, rs = orc.quantize(t.cpu().numpy())
+        assert np.float32(s) == np.float32(rs)
+        assert np.array_equal(tq.cpu().numpy(), rq)
+
+
+def test_dequantizer_bit_exact(orc):
+    rng = np.random.default_rng(9)
+    xq = rng.integers(-128, 128, size=100_003).astype(np.int8)
+    s = np.float32(0.0123)
+    got = qf.qflash_dequantize(torch.from_numpy(xq).cuda(), float(s)).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), orc.dequantize(xq, float(s)).view(np.uint32))
+    st = torch.tensor([s], device="cuda")
+    got2 = qf.qflash_dequantize(torch.from_numpy(xq).cuda(), st).cpu().numpy()
+    assert np.array_equal(got2, got)
+
+
+# ------------------------------------------------------------------ device-scale path
+def test_dscale_matches_host_scales(orc):
+    q, k, v = gen_workload("A3", 1, seed=4)
+    qt, kt, vt = _dev(q, k, v)
+    qq, kq, vq, scales = qf.qflash_quantize_qkv(qt, kt, vt)
+    out, ws = qf.qflash_attention_int8_dscale(qq, kq, vq, scales)
+    torch.cuda.synchronize()
+    assert int(ws[0].item()) == 0
+    s = scales.cpu().numpy()
+    ref_host, _ = qf.qflash_attention_int8(qq, kq, vq, float(s[0]), float(s[1]), float(s[2]))
+    assert torch.equal(out, ref_host)
+    # device-derived constants equal the host-derived ones
+    hp = qf.qflash_derive_params(float(s[0]), float(s[1]), 64)
+    wsn = ws.cpu().numpy()
+    assert wsn[1] == hp["s_inv"] and wsn[2] == np.int32(np.uint32(hp["q_magic"]))
+
+
+def test_dscale_out_of_range_writes_nothing():
+    q = torch.zeros((1, 64, 64), dtype=torch.int8, device="cuda")
+    scales = torch.tensor([10.0, 10.0, 1.0], device="cuda")    # s = 18 > 0.5
+    out = torch.full_like(q, 77)
+    _, ws = qf.qflash_attention_int8_dscale(q, q.clone(), q.clone(), scales, out=out)
+    torch.cuda.synchronize()
+    assert int(ws[0].item()) == _lib.QFLASH_ERR_SCALE_RANGE
+    assert (out == 77).all()
+
+
+def test_pipeline_end_to_end_bit_exact(orc):
+    # float -> quantize -> attention -> dequantize, all on the GPU, vs the oracle
+    q, k, v = gen_workload("A1", 1, seed=7)
+    out = qf.qflash_forward(torch.from_numpy(q), torch.from_numpy(k), torch.from_numpy(v))
+    qq, sq = orc.quantize(q)
+    kq, sk = orc.quantize(k)
+    vq, sv = orc.quantize(v)
+    ref = orc.dequantize(orc.attention(qq, kq, vq, sq, sk), sv)
+    assert np.array_equal(out.numpy().view(np.uint32), ref.view(np.uint32))
+
+
+def test_sqnr_floor_on_gpu_output(orc):
+    from oracle.fp_reference import attention_fp64, sqnr_db
+    for name, batch in [("A2", 8), ("A7", 8)]:
+        q, k, v = gen_workload(name, batch, seed=0)
+        out = qf.qflash_forward(torch.from_numpy(q), torch.from_numpy(k), torch.from_numpy(v))
+        assert sqnr_db(attention_fp64(q, k, v), out.numpy()) >= 29.0   # > I-ViT's 25.8
+
+
+# ------------------------------------------------------------------ properties
+def test_determinism_and_independence(orc):
+    q, k, v = gen_int8_qkv(16, 197, 64, seed=8)
+    a = _gpu_attention(q, k, v, 0.05, 0.05)
+    b = _gpu_attention(q, k, v, 0.05, 0.05)
+    assert np.array_equal(a, b)
+    for p in (0, 7, 15):
+        one = _gpu_attention(q[p:p + 1], k[p:p + 1], v[p:p + 1], 0.05, 0.05)
+        assert np.array_equal(one[0], a[p])
+
+
+def test_validation_errors():
+    q = torch.zeros((2, 197, 64), dtype=torch.int8, device="cuda")
+    with pytest.raises(_lib.QFlashError) as e:
+        qf.qflash_attention_int8(q, q, q, 10.0, 10.0, 1.0)        # s > 0.5
+    assert e.value.status == _lib.QFLASH_ERR_SCALE_RANGE
+    with pytest.raises(_lib.QFlashError) as e:
+        qf.qflash_attention_int8(q, q, q, 0.05, 0.05, 0.05, out=q)  # aliasing
+    assert e.value.status == _lib.QFLASH_ERR_INVALID_ARGUMENT
+    with pytest.raises(_lib.QFlashError) as e:
+        qf.qflash_attention_int8(q, q, q, 0.05, 0.05, 0.05, block_kv=96)
+    assert e.value.status == _lib.QFLASH_ERR_UNSUPPORTED_SHAPE
+    q48 = torch.zeros((2, 197, 48), dtype=torch.int8, device="cuda")
+    with pytest.raises(_lib.QFlashError) as e:
+        qf.qflash_attention_int8(q48, q48, q48, 0.05, 0.05, 0.05)
+    assert e.value.status == _lib.QFLASH_ERR_UNSUPPORTED_SHAPE
+    with pytest.raises(_lib.QFlashError):
+        qf.qflash_attention_int8(q, q, q, 0.05, 0.05, 0.05, variant="packed")   # N > 64
