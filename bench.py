@@ -343,6 +343,33 @@ def main():
     torch.cuda.synchronize()
     durs = sorted(x.elapsed_time(y) for x, y in zip(ka, kb))
     attn_ms = statistics.mean(durs[: max(1, int(0.9 * len(durs)))])  # drop the slowest 10 %
+
+    # ---- per-stage breakdown of one step (eager, events between the launches)
+    from paper_2604_25306_b200 import _lib as _l
+    k_bd = min(args.steps, 500)
+    evs = []
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(int(k_bd * 120e-6 * 2.0e9))
+        for i in range(k_bd):
+            p = pipes[i % n_sets]
+            s_in = sets[i % n_sets]
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e[0].record(stream)
+            qfl.qflash_quantize_qkv_prepare(*s_in, outs=p.qkv_q, scales=p.scales,
+                                            workspace=p.workspace, stream=stream)
+            e[1].record(stream)
+            qfl.qflash_attention_int8_prepared(p.qkv_q[0], p.qkv_q[1], p.qkv_q[2], p.workspace,
+                                               args.block_kv, out=p.o_q, stream=stream)
+            e[2].record(stream)
+            qfl.qflash_dequantize(p.o_q, p.scales[2:3], out=p.out, stream=stream)
+            e[3].record(stream)
+            evs.append(e)
+    torch.cuda.synchronize()
+    def _med(a, b):
+        return statistics.median(x[a].elapsed_time(x[b]) for x in evs) * 1e3
+    breakdown = {"quantize_qkv_us": _med(0, 1), "attention_us": _med(1, 2),
+                 "dequantize_us": _med(2, 3),
+                 "note": "eager launches, GPU kept busy; medians over %d steps" % k_bd}
     # share of the step (the ncu launch list must agree on this share)
     attn_share = attn_ms / ms_per_step
 
@@ -358,6 +385,7 @@ def main():
         "per_unit": "10 int32 ops per score element (SURVEY 8(d)); units = N^2 P per launch",
         "peak_source": "148 SM x 128 int32 lanes x %.3f GHz (B200_PROFILING sm max clock)" % sm_clk_ghz,
         "attn_us": attn_ms * 1e3, "attn_share_of_step": attn_share,
+        "step_breakdown": breakdown,
         "tensor": {"achieved_tops": alg["int8_ops"] / (attn_ms * 1e-3) / 1e12,
                    "peak_tops": int8_peak_tops,
                    "frac": alg["int8_ops"] / (attn_ms * 1e-3) / 1e12 / int8_peak_tops,

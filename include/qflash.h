@@ -121,7 +121,7 @@ QFLASH_API qflash_status qflash_attention_int8_ex(const int8_t* q, const int8_t*
  * are out of range nothing is written to o and the int32 at workspace_dev[0]
  * holds QFLASH_ERR_SCALE_RANGE (QFLASH_OK otherwise).  s_O = s_V stays in
  * scales_dev[2]. */
-#define QFLASH_DSCALE_WORKSPACE_BYTES 128
+#define QFLASH_DSCALE_WORKSPACE_BYTES 4096
 QFLASH_API qflash_status qflash_attention_int8_dscale(const int8_t* q, const int8_t* k, const int8_t* v,
                                            const float* scales_dev,
                                            const qflash_attn_shape* shape, qflash_variant variant,
@@ -133,7 +133,9 @@ QFLASH_API qflash_status qflash_attention_int8_dscale(const int8_t* q, const int
  * attention's integer constants from the final (s_q, s_k) on the device (block 0
  * of the quantize kernel, same fp64 expression as qflash_derive_params) into
  * workspace_dev (QFLASH_DSCALE_WORKSPACE_BYTES, 16-byte aligned; int32 status at
- * offset 0).  qflash_attention_int8_prepared then runs Algorithm 1 with the
+ * offset 0; bytes 256.. hold per-CTA amax partials).  When Q, K and V fit in the
+ * GPU's aggregate shared memory the quantization is a single cooperative pass
+ * (HBM read once); otherwise amax and quantize are two streaming launches.  qflash_attention_int8_prepared then runs Algorithm 1 with the
  * constants found in workspace_dev (nothing is written to o if the status is
  * not QFLASH_OK).  head_dim must be the d of the following attention call. */
 QFLASH_API qflash_status qflash_quantize_qkv_prepare(const void* q, const void* k, const void* v,

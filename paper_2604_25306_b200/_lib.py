@@ -21,7 +21,7 @@ QFLASH_ERR_UNSUPPORTED_DEVICE = 5
 
 QFLASH_F32, QFLASH_BF16, QFLASH_F16 = 0, 1, 2
 VARIANTS = {"auto": 0, "generic": 1, "packed": 2}
-DSCALE_WORKSPACE_BYTES = 128
+DSCALE_WORKSPACE_BYTES = 4096
 
 EXPORTED = [
     "qflash_quantize_per_tensor", "qflash_quantize_qkv", "qflash_attention_int8",

@@ -98,13 +98,23 @@ __host__ __device__ constexpr uint32_t swizzle_layout() {
 //   P  = floor(y M_P / 2^r_P)                                            (Eq. 10)
 // Instruction mix per element: 2 IADD3 + SHF (ALU pipe), 2 IMAD.HI + IMAD (FMA
 // pipe); `m` is the row maximum, `nm` = -m.
-template <bool FASTQ>
-QF_DEV int32_t shift_exp2_requant(int32_t S, uint32_t m, uint32_t nm, const IntParams& p) {
+// ALT = true computes u = S + (s_inv - m) with IMAD (FMA pipe) instead of IADD3
+// (ALU pipe); alternating the two forms balances the pipes (ALU 4.5 / FMA 4.5
+// issue slots per element).
+template <bool FASTQ, bool ALT>
+QF_DEV int32_t shift_exp2_requant(int32_t S, uint32_t m, uint32_t nm, uint32_t c3, uint32_t one,
+                                  const IntParams& p) {
   const uint32_t s_inv = static_cast<uint32_t>(p.s_inv);
   const uint32_t d1 = iadd3(m, static_cast<uint32_t>(-S), s_inv);
   uint32_t q1 = umulhi(d1, p.q_magic);
   if constexpr (!FASTQ) q1 >>= p.q_shift;
-  const uint32_t num = q1 * s_inv + iadd3(static_cast<uint32_t>(S), s_inv, nm);
+  uint32_t u;
+  if constexpr (ALT) {
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(u) : "r"(static_cast<uint32_t>(S)), "r"(one), "r"(c3));
+  } else {
+    u = iadd3(static_cast<uint32_t>(S), s_inv, nm);
+  }
+  const uint32_t num = q1 * s_inv + u;
   uint32_t y = shr_clamp(num, q1);
   if constexpr (FASTQ) {
     // y M_P < 2^32 (host-checked: s_inv M_P < 2^32): IMAD.lo + SHF instead of
@@ -142,19 +152,35 @@ QF_DEV uint32_t release_factor32(int32_t alpha, const IntParams& p) {
   return static_cast<uint32_t>(__umul64hi(n, mg) >> p.rel_shift);
 }
 
-// Fast exact ScaleRelease, valid when |X| s_inv < 2^32 and 0 <= alpha < s_inv:
-//   X >= 0:  floor(X alpha / s_inv) = hi(X * A_c),  A_c = A_f + 1 (>= alpha 2^32 / s_inv)
-//   X <  0:  floor(X alpha / s_inv) = hi(X * A_f) (signed) = hi(X_u * A_f) - A_f
-// (the over/under-estimate is < 1/s_inv, which never crosses an integer because
-// X alpha / s_inv is a multiple of 1/s_inv).  alpha = s_inv rows keep X.
-// 5 instructions: SHF, IADD, LOP3, IMAD.HI (mad.hi), SEL.
-QF_DEV uint32_t release_fast(uint32_t X, uint32_t a_c, uint32_t na_f, bool ident) {
-  const uint32_t m = static_cast<uint32_t>(static_cast<int32_t>(X) >> 31);
-  const uint32_t a = a_c + m;
-  const uint32_t corr = na_f & m;
-  uint32_t q;
-  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(q) : "r"(X), "r"(a), "r"(corr));
-  return ident ? X : q;
+// Fast exact ScaleRelease (2 instructions per element).  With a per-row bound
+// |X| <= bound and (2 bound + s_inv) s_inv < 2^32, pick B = floor(bound/s_inv) + 1
+// so X' = X + B s_inv >= 1; since B s_inv alpha / s_inv = B alpha is an integer,
+//   floor(X alpha / s_inv) = floor(X' alpha / s_inv) - B alpha
+//                          = hi(X' * A_c) - B alpha,   A_c = floor(alpha 2^32 / s_inv) + 1,
+// exact because X' s_inv < 2^32 keeps the ceiling error below 1/s_inv (the
+// fractional part of X' alpha / s_inv is a multiple of 1/s_inv).  alpha = s_inv rows
+// (identity) use A = 2^32 - 1: hi(X' (2^32 - 1)) = X' - 1, corrected by +1.
+// Per element: IADD3 (X + B s_inv), IMAD.HI, IADD3 (+ addend): ALU 2, FMA 1.
+struct BiasedRelease {
+  uint32_t bias;    // B s_inv
+  uint32_t mul;     // A_c (or 2^32 - 1 for identity rows)
+  uint32_t add;     // -B alpha (+1 for identity rows)
+  uint32_t zero;    // runtime 0: keeps the final add a separate ALU IADD3 (ptxas would
+                    // otherwise fold it into IMAD.HI's 64-bit addend pair + 2 IMAD.MOV)
+  QF_DEV uint32_t apply(uint32_t X) const {
+    return iadd3(__umulhi(iadd3(X, bias, zero), mul), add, zero);
+  }
+};
+QF_DEV BiasedRelease make_biased_release(int32_t alpha, uint32_t bound, const IntParams& p) {
+  const uint64_t mg = (static_cast<uint64_t>(p.rel_magic_hi) << 32) | p.rel_magic_lo;
+  const uint32_t B = static_cast<uint32_t>(__umul64hi(bound, mg) >> p.rel_shift) + 1u;  // floor(bound/s_inv)+1
+  const bool ident = alpha == p.s_inv;
+  BiasedRelease r;
+  r.bias = B * static_cast<uint32_t>(p.s_inv);
+  r.mul = ident ? 0xFFFFFFFFu : release_factor32(alpha, p) + 1u;
+  r.add = (0u - B * static_cast<uint32_t>(alpha)) + (ident ? 1u : 0u);
+  r.zero = static_cast<uint32_t>(p.zero);
+  return r;
 }
 
 // ScaleRelease of one accumulator element: floor(X alpha / s_inv) exactly
@@ -219,17 +245,26 @@ QF_DEV int32_t floor_div_exact(int32_t O, int32_t l) {
 // columns [g*D/4, (g+1)*D/4) for the release and the normalization.  The row
 // maximum is combined across warpgroups through shared memory (one named
 // barrier per KV tile).
-template <int D, int BC, bool PACKED>
+// MODE 0: one CTA per SM, 4 softmax warpgroups, 4 control warps, double S buffer.
+// MODE 1: two CTAs per SM (when TMEM allows), 2 softmax warpgroups, 2 control warps.
+// MODE 2: two CTAs per SM (when TMEM allows), 4 softmax warpgroups, 2 control
+//         warps, S processed in 16-column chunks to fit ~56 registers per thread.
+template <int D, int BC, bool PACKED, int MODE>
 struct Cfg {
-  static constexpr int kNWG = 4;                          // softmax warpgroups
+  static constexpr int kNWG = MODE == 1 ? 2 : 4;          // softmax warpgroups
+  static constexpr int kCtl = MODE == 0 ? 4 : 2;          // control warps
   static constexpr int kSoftThreads = 128 * kNWG;
-  static constexpr int kThreads = 128 + kSoftThreads;
+  static constexpr int kThreads = 32 * kCtl + kSoftThreads;
   static constexpr int kCW = (PACKED ? 64 : BC) / kNWG;   // key columns per thread
   static constexpr int kOW = D / kNWG;                    // O columns per thread
-  static constexpr bool kSInRegs = kCW <= 32;
+  static constexpr int kChunk = MODE == 2 ? (kCW < 16 ? kCW : 16) : (kCW < 32 ? kCW : 32);
+  static constexpr bool kSInRegs = kCW == kChunk;
+  static constexpr int kAllocWarp = kCtl == 4 ? 2 : 1;    // TMEM allocator
+  static constexpr int kTableWarp = kCtl == 4 ? 3 : 1;    // reciprocal-table loader
   // TMEM: kNumS S buffers of BC columns (P_j aliases its own S buffer), then O
   // (D columns) + l (column D) + 15 copies of l from the ones block.
-  static constexpr int kNumS = (2 * BC + D + 16 <= 512) ? 2 : 1;
+  static constexpr int kMinBlocks = (MODE != 0 && BC + D + 16 <= 256) ? 2 : 1;
+  static constexpr int kNumS = (kMinBlocks == 1 && 2 * BC + D + 16 <= 512) ? 2 : 1;
   static constexpr uint32_t kTmemO = kNumS * BC;
 };
 
@@ -272,18 +307,18 @@ struct TileIter {
 };
 
 // ---------------------------------------------------------------- softmax role
-template <int D, int BC, bool PACKED, bool FASTQ>
+template <int D, int BC, bool PACKED, int MODE, bool FASTQ>
 __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntParams& prm,
                                              uint32_t tmem_base, uint64_t* bar_s_full,
                                              uint64_t* bar_p_full, uint64_t* bar_o_full,
                                              int32_t* red, const uint32_t* recip, int warp,
                                              int lane) {
-  using C = Cfg<D, BC, PACKED>;
+  using C = Cfg<D, BC, PACKED, MODE>;
   constexpr int CW = C::kCW;
   constexpr int OW = C::kOW;
   const int N = args.N;
   const int Tc = PACKED ? 1 : args.Tc;
-  const int g = (warp - 4) >> 2;        // warpgroup
+  const int g = (warp - C::kCtl) >> 2;  // warpgroup
   const int quarter = warp & 3;
   const int row = quarter * 32 + lane;  // TMEM lane == tile row
   const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
@@ -312,10 +347,11 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
       const uint32_t tS = tS0 + sb * BC;
       mbar_wait(&bar_s_full[sb], (C::kNumS == 2 ? (it >> 1) : it) & 1);
       tc_fence_after();
-      if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(40 + 8 * j);
+      if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(40 + 8 * j);
       // columns of this thread that exist in KV tile j (ragged last tile, R16)
       const int valid = (PACKED ? N : min(BC, N - j * BC)) - c0_in_tile;
-      uint32_t s[C::kSInRegs ? CW : 32];
+      constexpr int CK = C::kChunk;
+      uint32_t s[C::kSInRegs ? CW : CK];
       int32_t tmax = INT32_MIN;
       if (warp_live && valid > 0) {
         if constexpr (C::kSInRegs) {
@@ -334,15 +370,15 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
           }
         } else {
 #pragma unroll
-          for (int ch = 0; ch < CW / 32; ++ch) {
-            tmem_ld<32>(tS + c0 + 32 * ch, s);
+          for (int ch = 0; ch < CW / CK; ++ch) {
+            tmem_ld<CK>(tS + c0 + CK * ch, s);
             tmem_wait_ld();
             if (args.dbg_s != nullptr && dbg && j == 0) {
-              for (int e = 0; e < 32; ++e) args.dbg_s[row * BC + c0 + 32 * ch + e] = static_cast<int32_t>(s[e]);
+              for (int e = 0; e < CK; ++e) args.dbg_s[row * BC + c0 + CK * ch + e] = static_cast<int32_t>(s[e]);
             }
 #pragma unroll
-            for (int e = 0; e < 32; ++e)
-              if (32 * ch + e < valid) tmax = max(tmax, static_cast<int32_t>(s[e]));
+            for (int e = 0; e < CK; ++e)
+              if (CK * ch + e < valid) tmax = max(tmax, static_cast<int32_t>(s[e]));
           }
         }
       }
@@ -351,35 +387,38 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
         int32_t* rb = red + (it & 1) * (C::kNWG * 128);
         rb[g * 128 + row] = tmax;
         named_bar_sync(1, C::kSoftThreads);
-        if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(41 + 8 * j);
+        if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(41 + 8 * j);
 #pragma unroll
         for (int h = 0; h < C::kNWG; ++h) tmax = max(tmax, rb[h * 128 + row]);
       }
       const int32_t m_new = max(m, tmax);
       // (4) alpha = ShiftExp2(m_old - m_new)
       const int32_t alpha = shift_exp2<FASTQ>(m - m_new, prm);
-      if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(42 + 8 * j);
+      if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(42 + 8 * j);
 
       // (5)(6) P = Requant(ShiftExp2(S - m_new)), 4 x int8 per TMEM column.
       const uint32_t mu = static_cast<uint32_t>(m_new);
       const uint32_t nmu = static_cast<uint32_t>(-m_new);
+      const uint32_t c3 = static_cast<uint32_t>(prm.s_inv - m_new);
+      const uint32_t one = static_cast<uint32_t>(prm.one);
       uint32_t pk[CW / 4];
       if (warp_live && valid > 0) {
         if constexpr (C::kSInRegs) {
           if (valid >= CW) {
 #pragma unroll
             for (int e = 0; e < CW; e += 4)
-              pk[e / 4] = pack4_sat_s8(shift_exp2_requant<FASTQ>(static_cast<int32_t>(s[e]), mu, nmu, prm),
-                                       shift_exp2_requant<FASTQ>(static_cast<int32_t>(s[e + 1]), mu, nmu, prm),
-                                       shift_exp2_requant<FASTQ>(static_cast<int32_t>(s[e + 2]), mu, nmu, prm),
-                                       shift_exp2_requant<FASTQ>(static_cast<int32_t>(s[e + 3]), mu, nmu, prm));
+              pk[e / 4] = pack4_sat_s8(
+                  shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(s[e]), mu, nmu, c3, one, prm),
+                  shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(s[e + 1]), mu, nmu, c3, one, prm),
+                  shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(s[e + 2]), mu, nmu, c3, one, prm),
+                  shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(s[e + 3]), mu, nmu, c3, one, prm));
           } else {
 #pragma unroll
             for (int e = 0; e < CW; e += 4) {
               int32_t pv[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                const int32_t x = shift_exp2_requant<FASTQ>(static_cast<int32_t>(s[e + u]), mu, nmu, prm);
+                const int32_t x = shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(s[e + u]), mu, nmu, c3, one, prm);
                 pv[u] = (e + u < valid) ? x : 0;
               }
               pk[e / 4] = pack4_sat_s8(pv[0], pv[1], pv[2], pv[3]);
@@ -387,18 +426,18 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
           }
         } else {
 #pragma unroll
-          for (int ch = 0; ch < CW / 32; ++ch) {
-            tmem_ld<32>(tS + c0 + 32 * ch, s);
+          for (int ch = 0; ch < CW / CK; ++ch) {
+            tmem_ld<CK>(tS + c0 + CK * ch, s);
             tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; e += 4) {
+            for (int e = 0; e < CK; e += 4) {
               int32_t pv[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                const int32_t x = shift_exp2_requant<FASTQ>(static_cast<int32_t>(s[e + u]), mu, nmu, prm);
-                pv[u] = (32 * ch + e + u < valid) ? x : 0;
+                const int32_t x = shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(s[e + u]), mu, nmu, c3, one, prm);
+                pv[u] = (CK * ch + e + u < valid) ? x : 0;
               }
-              pk[(32 * ch + e) / 4] = pack4_sat_s8(pv[0], pv[1], pv[2], pv[3]);
+              pk[(CK * ch + e) / 4] = pack4_sat_s8(pv[0], pv[1], pv[2], pv[3]);
             }
           }
         }
@@ -418,7 +457,7 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
         for (int e = 0; e < CW / 4; ++e) z[e] = 0u;
         tmem_st<CW / 4>(tS + (((1 - win) * 64 + c0_in_tile) >> 2), z);
       }
-      if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(44 + 8 * j);
+      if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(44 + 8 * j);
 
       // (7)(8) ScaleRelease of O (this group's columns) and l (group 0) once
       // PV_{j-1} has landed -- after P_j so that PV_{j-1} completes behind the P
@@ -428,29 +467,26 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
       if (j > 0) {
         mbar_wait(bar_o_full, (it - 1) & 1);
         tc_fence_after();
-        if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(45 + 8 * j);
+        if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(45 + 8 * j);
         if (warp_live && __any_sync(0xffffffffu, alpha != prm.s_inv)) {
           uint32_t o[OW];
           tmem_ld<OW>(tO + g * OW, o);
           uint32_t lcol;
           tmem_ld1(tO + D, lcol);
           tmem_wait_ld();
-          if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(46 + 8 * j);
+          if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(46 + 8 * j);
           // Fast exact path when every row of the warp satisfies |X| s_inv < 2^32
           // for all its accumulators X (bound |O| <= 128 (l + 2 T_c), DESIGN.md
           // "Kernel arithmetic"): floor(X alpha / s_inv) is then the high word of
           // X * ceil/floor(alpha 2^32 / s_inv) with no correction.
-          const uint64_t bound = 128ull * (static_cast<uint64_t>(lcol) + 2ull * Tc) *
-                                 static_cast<uint64_t>(prm.s_inv);
-          if (__all_sync(0xffffffffu, bound < (1ull << 32))) {
-            const uint32_t a_f = release_factor32(alpha, prm);  // floor(alpha 2^32 / s_inv)
-            const uint32_t a_c = a_f + 1u;
-            const uint32_t na_f = 0u - a_f;
-            const bool ident = alpha == prm.s_inv;
+          const uint64_t bound = 128ull * (static_cast<uint64_t>(lcol) + 2ull * Tc);
+          const uint64_t D64 = static_cast<uint64_t>(prm.s_inv);
+          if (__all_sync(0xffffffffu, (2ull * bound + D64) * D64 < (1ull << 32))) {
+            const BiasedRelease br = make_biased_release(alpha, static_cast<uint32_t>(bound), prm);
 #pragma unroll
-            for (int e = 0; e < OW; ++e) o[e] = release_fast(o[e], a_c, na_f, ident);
+            for (int e = 0; e < OW; ++e) o[e] = br.apply(o[e]);
             tmem_st<OW>(tO + g * OW, o);
-            if (g == 0) tmem_st1(tO + D, release_fast(lcol, a_c, na_f, ident));
+            if (g == 0) tmem_st1(tO + D, br.apply(lcol));
           } else {
             const int32_t A = release_factor(alpha, prm);
 #pragma unroll
@@ -462,7 +498,7 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
               tmem_st1(tO + D, lcol);
             }
           }
-          if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(47 + 8 * j);
+          if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(47 + 8 * j);
         }
       }
 
@@ -481,14 +517,14 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_p_full);
-      if (dbg && warp == 4 && lane == 0 && j < 7) QF_TS(43 + 8 * j);
+      if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(43 + 8 * j);
       m = m_new;
     }
 
     // (11) O_i = floor(O / l), saturated to int8 (R14); this group's O columns.
     mbar_wait(bar_o_full, (it0 + Tc - 1) & 1);
     tc_fence_after();
-    if (dbg && warp == 4 && lane == 0) QF_TS(100);
+    if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0) QF_TS(100);
     if (ti.i == 0) named_bar_sync(2, C::kSoftThreads + 32);  // reciprocal table ready
     if (warp_live) {
       uint32_t lraw;
@@ -534,20 +570,20 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
         }
       }
     }
-    if (dbg && warp == 4 && lane == 0) QF_TS(101);
+    if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0) QF_TS(101);
     // The O/l loads above completed (wait::ld) before this thread's next p_full
     // arrival, so the next tile's first PV (which overwrites O) cannot race them.
   }
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int D, int BC, bool PACKED>
-__global__ void __launch_bounds__(Cfg<D, BC, PACKED>::kThreads, 1)
+template <int D, int BC, bool PACKED, int MODE>
+__global__ void __launch_bounds__(Cfg<D, BC, PACKED, MODE>::kThreads, Cfg<D, BC, PACKED, MODE>::kMinBlocks)
     qflash_attn_kernel(const __grid_constant__ CUtensorMap tm_q,
                        const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, const AttnArgs args) {
   using L = SmemLayout<D, BC>;
-  using C = Cfg<D, BC, PACKED>;
+  using C = Cfg<D, BC, PACKED, MODE>;
   constexpr uint32_t kTmemCols = tmem_cols_for(C::kNumS * BC, D);
   static_assert(kTmemCols >= C::kNumS * BC + D + 16, "TMEM budget");
   constexpr uint32_t kSwz = swizzle_layout<D>();
@@ -597,7 +633,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, PACKED>::kThreads, 1)
     mbar_init(bar_o_full, 1);
     fence_barrier_init();
   }
-  if (warp == 2) {
+  if (warp == C::kAllocWarp) {
     tmem_alloc(tmem_slot, kTmemCols);
     tmem_relinquish();
   }
@@ -617,13 +653,14 @@ __global__ void __launch_bounds__(Cfg<D, BC, PACKED>::kThreads, 1)
   const bool run = (prm.status == 0);
 
   if (run) {
-    if (warp == 3) {
+    if (warp == C::kTableWarp) {
       // reciprocal table for step (11) -> shared memory, off the critical path:
       // the softmax warps sync on named barrier 2 before their first normalization.
       for (int i = lane; i < 1024; i += 32) recip[i] = g_recip.v[i];
       __threadfence_block();
       named_bar_arrive(2, C::kSoftThreads + 32);
-    } else if (warp == 0) {
+    }
+    if (warp == 0) {
       // ========================================================= TMA producer
       if (lane == 0) {
         TileIter ti;
@@ -711,13 +748,13 @@ __global__ void __launch_bounds__(Cfg<D, BC, PACKED>::kThreads, 1)
           }
         }
       }
-    } else if (warp >= 4) {
+    } else if (warp >= C::kCtl) {
       if (prm.q_shift == 0 && static_cast<uint64_t>(prm.s_inv) * static_cast<uint64_t>(prm.m_p) < (1ull << 32))
-        softmax_role<D, BC, PACKED, true>(args, prm, tmem_base, bar_s_full, bar_p_full,
-                                          bar_o_full, red, recip, warp, lane);
+        softmax_role<D, BC, PACKED, MODE, true>(args, prm, tmem_base, bar_s_full, bar_p_full,
+                                               bar_o_full, red, recip, warp, lane);
       else
-        softmax_role<D, BC, PACKED, false>(args, prm, tmem_base, bar_s_full, bar_p_full,
-                                           bar_o_full, red, recip, warp, lane);
+        softmax_role<D, BC, PACKED, MODE, false>(args, prm, tmem_base, bar_s_full, bar_p_full,
+                                                bar_o_full, red, recip, warp, lane);
     }
   }
 
@@ -726,17 +763,18 @@ __global__ void __launch_bounds__(Cfg<D, BC, PACKED>::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (threadIdx.x == 0 && blockIdx.x == 0) QF_TS(102);
-  if (warp == 2) tmem_dealloc(tmem_base, kTmemCols);
+  if (warp == C::kAllocWarp) tmem_dealloc(tmem_base, kTmemCols);
 }
 
 // ----------------------------------------------------------------------------
-// Host-side launch helpers (called by qflash_host.cu).
-template <int D, int BC, bool PACKED>
+// Host-side launch helpers (called by qflash_host.cu).  `tiles` = number of work
+// tiles; the persistent grid is min(tiles, CTAs-per-SM x SMs).
+template <int D, int BC, bool PACKED, int MODE>
 cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                          const AttnArgs& args, dim3 grid, cudaStream_t stream) {
+                          AttnArgs args, int64_t tiles, int sms, cudaStream_t stream) {
   using L = SmemLayout<D, BC>;
-  using C = Cfg<D, BC, PACKED>;
-  auto kern = qflash_attn_kernel<D, BC, PACKED>;
+  using C = Cfg<D, BC, PACKED, MODE>;
+  auto kern = qflash_attn_kernel<D, BC, PACKED, MODE>;
   static int configured[16] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -745,29 +783,45 @@ cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CU
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 16) configured[dev] = 1;
   }
-  kern<<<grid, C::kThreads, L::kAlloc, stream>>>(tq, tk, tv, args);
+  const int64_t cap = static_cast<int64_t>(C::kMinBlocks) * sms;
+  const int64_t G = tiles < cap ? tiles : cap;
+  const int64_t Tr = args.Tr;
+  args.tr_magic = Tr > 1 ? static_cast<uint32_t>(((1ull << 32) + Tr - 1) / Tr) : 0u;
+  args.g_div = static_cast<int32_t>(G / Tr);
+  args.g_mod = static_cast<int32_t>(G % Tr);
+  kern<<<dim3(static_cast<unsigned>(G)), C::kThreads, L::kAlloc, stream>>>(tq, tk, tv, args);
   return cudaGetLastError();
 }
 
-cudaError_t launch_attention(int D, int BC, bool packed, const CUtensorMap& tq,
-                             const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& args,
-                             dim3 grid, cudaStream_t stream) {
+template <int MODE>
+static cudaError_t launch_attention_mode(int D, int BC, bool packed, const CUtensorMap& tq,
+                                        const CUtensorMap& tk, const CUtensorMap& tv,
+                                        const AttnArgs& args, int64_t tiles, int sms,
+                                        cudaStream_t stream) {
   if (packed) {
     // T_c = 1 and the KV tile is 2 x 64 keys regardless of block_kv.
     switch (D) {
-      case 32: return launch_attn_t<32, 128, true>(tq, tk, tv, args, grid, stream);
-      case 64: return launch_attn_t<64, 128, true>(tq, tk, tv, args, grid, stream);
-      case 128: return launch_attn_t<128, 128, true>(tq, tk, tv, args, grid, stream);
+      case 32: return launch_attn_t<32, 128, true, MODE>(tq, tk, tv, args, tiles, sms, stream);
+      case 64: return launch_attn_t<64, 128, true, MODE>(tq, tk, tv, args, tiles, sms, stream);
+      case 128: return launch_attn_t<128, 128, true, MODE>(tq, tk, tv, args, tiles, sms, stream);
     }
     return cudaErrorInvalidValue;
   }
 #define QF_CASE(d, bc) \
-  if (D == d && BC == bc) return launch_attn_t<d, bc, false>(tq, tk, tv, args, grid, stream);
+  if (D == d && BC == bc) return launch_attn_t<d, bc, false, MODE>(tq, tk, tv, args, tiles, sms, stream);
   QF_CASE(32, 64) QF_CASE(32, 128) QF_CASE(32, 256)
   QF_CASE(64, 64) QF_CASE(64, 128) QF_CASE(64, 256)
   QF_CASE(128, 64) QF_CASE(128, 128) QF_CASE(128, 256)
 #undef QF_CASE
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_attention(int D, int BC, bool packed, const CUtensorMap& tq,
+                             const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& args,
+                             int64_t tiles, int sms, int mode, cudaStream_t stream) {
+  if (mode == 1) return launch_attention_mode<1>(D, BC, packed, tq, tk, tv, args, tiles, sms, stream);
+  if (mode == 2) return launch_attention_mode<2>(D, BC, packed, tq, tk, tv, args, tiles, sms, stream);
+  return launch_attention_mode<0>(D, BC, packed, tq, tk, tv, args, tiles, sms, stream);
 }
 
 }  // namespace qf

@@ -18,7 +18,9 @@ struct IntParams {
   int32_t rel_shift;
   int32_t p_max;
   int32_t r_p, m_p, n;
-  int32_t pad[3];
+  int32_t one;        // always 1 (a runtime multiplier that keeps an add on the FMA pipe)
+  int32_t zero;       // always 0 (a runtime addend that keeps an add on the ALU pipe)
+  int32_t pad[1];
   double s;
 };
 static_assert(sizeof(IntParams) == 72, "IntParams layout");

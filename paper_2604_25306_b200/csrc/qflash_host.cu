@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 
 #include "../../include/qflash.h"
 #include "../../include/qflash_debug.h"
@@ -19,9 +20,10 @@
 namespace qf {
 cudaError_t launch_attention(int D, int BC, bool packed, const CUtensorMap& tq,
                              const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& args,
-                             dim3 grid, cudaStream_t stream);
+                             int64_t tiles, int sms, int mode, cudaStream_t stream);
 cudaError_t launch_quantize(const QuantTensors& t, int ntensors, int dtype, int64_t numel,
-                            IntParams* prm_out, int32_t head_dim, cudaStream_t stream);
+                            IntParams* prm_out, int32_t head_dim, cudaStream_t stream,
+                            float* partial);
 cudaError_t launch_dequantize(const int8_t* xq, float scale, const float* scale_dev,
                               int64_t numel, float* y, cudaStream_t stream);
 }  // namespace qf
@@ -204,13 +206,18 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
       if (dev >= 0 && dev < 64) sm_cache[dev] = sms;
     }
   }
-  const int64_t G = tiles < sms ? tiles : sms;
   args.Tr = static_cast<int32_t>(Tr);
-  args.tr_magic = Tr > 1 ? static_cast<uint32_t>(((1ull << 32) + Tr - 1) / Tr) : 0u;
-  args.g_div = static_cast<int32_t>(G / Tr);
-  args.g_mod = static_cast<int32_t>(G % Tr);
-  dim3 grid(static_cast<unsigned>(G), 1, 1);
-  cudaError_t e = qf::launch_attention(d, packed ? 128 : bc, packed, tq, tk, tv, args, grid, stream);
+  // Kernel configuration (qflash_attention.cu "MODE"): packed windows run two
+  // CTAs per SM with two softmax warpgroups (fastest there); the generic kernel
+  // one CTA per SM with four.  QFLASH_ATTN_MODE=0/1/2 overrides (experiments).
+  static int mode_env = -2;
+  if (mode_env == -2) {
+    const char* env = getenv("QFLASH_ATTN_MODE");
+    mode_env = (env != nullptr && env[0] >= '0' && env[0] <= '2') ? env[0] - '0' : -1;
+  }
+  const int mode = mode_env >= 0 ? mode_env : (packed ? 1 : 0);
+  cudaError_t e = qf::launch_attention(d, packed ? 128 : bc, packed, tq, tk, tv, args, tiles, sms,
+                                       mode, stream);
   if (e != cudaSuccess) return cuda_fail(e, "attention launch");
   return QFLASH_OK;
 }
@@ -322,7 +329,8 @@ qflash_status qflash_attention_int8_dscale(const int8_t* q, const int8_t* k, con
 
 static qflash_status quantize_impl(const void* const* xs, int8_t* const* xqs, float* const* scales,
                                    int nt, qflash_dtype dtype, int64_t numel, cudaStream_t stream,
-                                   qf::IntParams* prm_out = nullptr, int32_t head_dim = 0) {
+                                   qf::IntParams* prm_out = nullptr, int32_t head_dim = 0,
+                                   float* partial = nullptr) {
   if (numel < 0) return fail(QFLASH_ERR_INVALID_ARGUMENT, "numel < 0");
   if (dtype != QFLASH_F32 && dtype != QFLASH_BF16 && dtype != QFLASH_F16)
     return fail(QFLASH_ERR_INVALID_ARGUMENT, "unknown dtype %d", static_cast<int>(dtype));
@@ -341,7 +349,8 @@ static qflash_status quantize_impl(const void* const* xs, int8_t* const* xqs, fl
     t.xq[i] = xqs[i];
     t.scale[i] = scales[i];
   }
-  cudaError_t e = qf::launch_quantize(t, nt, static_cast<int>(dtype), numel, prm_out, head_dim, stream);
+  cudaError_t e = qf::launch_quantize(t, nt, static_cast<int>(dtype), numel, prm_out, head_dim, stream,
+                                      partial);
   if (e != cudaSuccess) return cuda_fail(e, "quantize launch");
   return QFLASH_OK;
 }
@@ -399,8 +408,10 @@ qflash_status qflash_quantize_qkv_prepare(const void* q, const void* k, const vo
   const void* xs[3] = {q, k, v};
   int8_t* xqs[3] = {q_q, k_q, v_q};
   float* scs[3] = {scales_dev, scales_dev + 1, scales_dev + 2};
+  // workspace layout: [0, 128) integer constants, [256, ...) per-CTA amax partials
   return quantize_impl(xs, xqs, scs, 3, dtype, numel, reinterpret_cast<cudaStream_t>(stream),
-                       reinterpret_cast<qf::IntParams*>(workspace_dev), head_dim);
+                       reinterpret_cast<qf::IntParams*>(workspace_dev), head_dim,
+                       reinterpret_cast<float*>(static_cast<char*>(workspace_dev) + 256));
 }
 
 qflash_status qflash_attention_int8_prepared(const int8_t* q, const int8_t* k, const int8_t* v,

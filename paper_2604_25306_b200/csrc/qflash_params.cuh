@@ -115,7 +115,9 @@ __host__ __device__ inline int derive_core(float s_q, float s_k, int32_t d, qf::
     o->r_p = r_p;
     o->m_p = static_cast<int32_t>(m_p);
     o->n = n;
-    o->pad[0] = o->pad[1] = o->pad[2] = 0;
+    o->one = 1;
+    o->zero = 0;
+    o->pad[0] = 0;
     o->s = s;
   }
   if (pub) {

@@ -16,11 +16,20 @@
 //      final s_q, s_k (qflash_quantize_qkv_prepare) so the step needs no extra
 //      launch.
 // 16 elements per thread and iteration (64 B of fp32 in flight, one 16-B store).
+//
+// Single-pass variant (quantize_fused_kernel): when the three tensors fit in the
+// GPU's aggregate shared memory, a cooperative grid (one CTA per SM) bulk-loads
+// its chunk of Q, K and V into shared memory with TMA (cp.async.bulk), reduces
+// the chunk amax, exchanges per-CTA partials through the caller's workspace
+// around one grid barrier, and quantizes from shared memory: HBM is read once,
+// one launch, no memset, no atomics.
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "qflash_common.cuh"
 #include "qflash_params.cuh"
@@ -130,13 +139,44 @@ __global__ void __launch_bounds__(kQThreads) amax_kernel(QuantTensors t, int64_t
   }
 }
 
-// roundf(fl32(x / s)) exactly (see the header comment).
-__device__ __forceinline__ int32_t quant_one(float x, float s, float r) {
+// roundf(fl32(x / s)) exactly (see the header comment).  Fast path: q = RN(x r),
+// rint(q) by the 1.5*2^23 magic-number add (exact for |q| < 2^22, no FRND/F2I),
+// flag `bad` when q is within 2^-14 of a half-integer.
+__device__ __forceinline__ int32_t quant_fast(float x, float r, bool& bad) {
   const float q = __fmul_rn(x, r);
-  const float fi = rintf(q);
-  if (fabsf(q - fi) < 0.49993896484375f)  // 0.5 - 2^-14
-    return static_cast<int32_t>(fi);
-  return static_cast<int32_t>(roundf(__fdiv_rn(x, s)));  // rare: near a half-integer
+  const float t = __fadd_rn(q, 12582912.0f);                    // 1.5 * 2^23
+  const float fi = __fadd_rn(t, -12582912.0f);                  // rint(q), exact
+  bad |= fabsf(__fadd_rn(q, -fi)) >= 0.49993896484375f;         // 0.5 - 2^-14
+  return static_cast<int32_t>(__float_as_uint(t) - 0x4B400000u);  // int(rint(q))
+}
+// the exact definition: IEEE division then round half away from zero (R1, R2)
+__device__ __forceinline__ int32_t quant_exact(float x, float s) {
+  return static_cast<int32_t>(roundf(__fdiv_rn(x, s)));
+}
+__device__ __forceinline__ int32_t quant_one(float x, float s, float r) {
+  bool bad = false;
+  const int32_t v = quant_fast(x, r, bad);
+  return bad ? quant_exact(x, s) : v;
+}
+// 16 elements -> 16 int8 (uint4), one warp-voted exact pass if any lane needs it.
+__device__ __forceinline__ uint4 quant16(const float* f, float s, float r) {
+  int32_t v[16];
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = quant_fast(f[k], r, bad);
+  if (__any_sync(__activemask(), bad)) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = quant_exact(f[k], s);
+  }
+  uint32_t w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t hi, lo;
+    asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(v[4 * k + 3]), "r"(v[4 * k + 2]));
+    asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(lo) : "r"(v[4 * k + 1]), "r"(v[4 * k]), "r"(hi));
+    w[k] = lo;
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 template <typename T>
@@ -170,17 +210,7 @@ __global__ void __launch_bounds__(kQThreads)
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nv; i += stride) {
     float v[kQElems];
     Load16<T>::load(x, i, v);
-    uint32_t w[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int32_t a = quant_one(v[4 * k], s, r), b = quant_one(v[4 * k + 1], s, r);
-      const int32_t c = quant_one(v[4 * k + 2], s, r), d = quant_one(v[4 * k + 3], s, r);
-      uint32_t hi, lo;
-      asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(d), "r"(c));
-      asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(lo) : "r"(b), "r"(a), "r"(hi));
-      w[k] = lo;
-    }
-    reinterpret_cast<uint4*>(xq)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    reinterpret_cast<uint4*>(xq)[i] = quant16(v, s, r);
   }
   for (int64_t i = nv * kQElems + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < numel;
        i += stride) {
@@ -189,25 +219,194 @@ __global__ void __launch_bounds__(kQThreads)
   }
 }
 
+// ----------------------------------------------------------- fused single pass
+// Cooperative grid (2 CTAs x 256 threads per SM, 128 registers per thread).  Thread g of
+// the grid owns the 16-byte vectors g, g + T, ..., g + (VPT-1) T of every tensor
+// (coalesced), keeps them in registers across one grid barrier, and quantizes
+// them with the global scale: one launch, HBM read once, no memset, no atomics.
+constexpr int kFThreads = 256;
+constexpr int kFBlocksPerSM = 2;
+
+template <typename T>
+__device__ __forceinline__ void widen16(const uint4& v, float* f);  // 16 B -> 16/sizeof(T) floats
+template <>
+__device__ __forceinline__ void widen16<float>(const uint4& v, float* f) {
+  f[0] = __uint_as_float(v.x); f[1] = __uint_as_float(v.y);
+  f[2] = __uint_as_float(v.z); f[3] = __uint_as_float(v.w);
+}
+template <>
+__device__ __forceinline__ void widen16<__nv_bfloat16>(const uint4& v, float* f) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    f[2 * e] = __uint_as_float(w[e] << 16);
+    f[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+  }
+}
+template <>
+__device__ __forceinline__ void widen16<__half>(const uint4& v, float* f) {
+  const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 x = __half22float2(h[e]);
+    f[2 * e] = x.x;
+    f[2 * e + 1] = x.y;
+  }
+}
+
+template <typename T, int VPT>
+__global__ void __launch_bounds__(kFThreads, kFBlocksPerSM)
+    quantize_fused_kernel(QuantTensors t, int64_t numel, float* partial, IntParams* prm_out,
+                          int32_t head_dim) {
+  namespace cg = cooperative_groups;
+  constexpr int kE = 16 / sizeof(T);  // elements per 16-byte vector
+  __shared__ float red[3][kFThreads / 32];
+  __shared__ float sc[3];
+  const int64_t T_all = static_cast<int64_t>(gridDim.x) * kFThreads;
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * kFThreads + threadIdx.x;
+  const int64_t nvec = numel / kE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  uint4 v[3][VPT];
+  float m[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const uint4* src = reinterpret_cast<const uint4*>(pick(t, i));
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int64_t idx = g + u * T_all;
+      v[i][u] = idx < nvec ? __ldg(src + idx) : make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+  // tail elements (numel % kE): thread 0 of block 0 folds them into its amax
+  // here and re-reads them for quantization after the barrier (<= 7 scalars)
+  const int ntail = static_cast<int>(numel - nvec * kE);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      float f[kE];
+      widen16<T>(v[i][u], f);
+#pragma unroll
+      for (int e = 0; e < kE; ++e) m[i] = fmaxf(m[i], fabsf(f[e]));
+    }
+    if (g == 0) {
+      for (int e = 0; e < ntail; ++e) m[i] = fmaxf(m[i], fabsf(Load16<T>::load1(pick(t, i), nvec * kE + e)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m[i] = fmaxf(m[i], __shfl_xor_sync(0xffffffffu, m[i], o));
+    if (lane == 0) red[i][warp] = m[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    float b = 0.f;
+#pragma unroll
+    for (int w = 0; w < kFThreads / 32; ++w) b = fmaxf(b, red[threadIdx.x][w]);
+    partial[threadIdx.x * gridDim.x + blockIdx.x] = b;
+  }
+  __threadfence();
+  cg::this_grid().sync();
+  // per-tensor scale s = fl32(amax / 127) (R3: 1/127 for an all-zero tensor)
+  if (warp < 3) {
+    float b = 0.f;
+    for (int j = lane; j < static_cast<int>(gridDim.x); j += 32) b = fmaxf(b, __ldcg(&partial[warp * gridDim.x + j]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+    if (lane == 0) {
+      float s = __fdiv_rn(b, 127.0f);
+      if (s == 0.0f) s = 1.0f / 127.0f;
+      sc[warp] = s;
+    }
+  }
+  __syncthreads();
+  if (g == 0) {
+    for (int i = 0; i < 3; ++i) *pick_s(t, i) = sc[i];
+    if (prm_out != nullptr) {
+      IntParams p;
+      const int st = derive_core(sc[0], sc[1], head_dim, &p, nullptr);
+      if (st != QFLASH_OK) {
+        memset(&p, 0, sizeof(p));
+        p.status = st;
+      }
+      *prm_out = p;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float s = sc[i];
+    const float r = __frcp_rn(s);
+    int8_t* xq = pick_q(t, i);
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int64_t idx = g + u * T_all;
+      float f[16];
+      widen16<T>(v[i][u], f);
+      if constexpr (kE == 4) {
+        // 4 elements -> one 32-bit store
+        int32_t q[4];
+        bool bad = false;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) q[e] = quant_fast(f[e], r, bad);
+        if (bad) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) q[e] = quant_exact(f[e], s);
+        }
+        uint32_t hi, lo;
+        asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(q[3]), "r"(q[2]));
+        asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(lo) : "r"(q[1]), "r"(q[0]), "r"(hi));
+        if (idx < nvec) reinterpret_cast<uint32_t*>(xq)[idx] = lo;
+      } else {
+        int32_t q[8];
+        bool bad = false;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) q[e] = quant_fast(f[e], r, bad);
+        if (bad) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) q[e] = quant_exact(f[e], s);
+        }
+        uint32_t w[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          uint32_t hi, lo;
+          asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(q[4 * k + 3]), "r"(q[4 * k + 2]));
+          asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(lo) : "r"(q[4 * k + 1]), "r"(q[4 * k]), "r"(hi));
+          w[k] = lo;
+        }
+        if (idx < nvec) reinterpret_cast<uint2*>(xq)[idx] = make_uint2(w[0], w[1]);
+      }
+    }
+    if (g == 0) {
+      for (int e = 0; e < ntail; ++e)
+        xq[nvec * kE + e] = static_cast<int8_t>(
+            max(-128, min(127, quant_one(Load16<T>::load1(pick(t, i), nvec * kE + e), s, r))));
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kQThreads)
     dequantize_kernel(const int8_t* __restrict__ xq, float scale, const float* __restrict__ scale_dev,
                       int64_t numel, float* __restrict__ y) {
   const float s = scale_dev ? *scale_dev : scale;
-  const int64_t nvec = numel / 16;
+  // 4 int8 per thread per step: one 4-B load and one 16-B store, both coalesced
+  const int64_t n4 = numel / 4;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec; i += stride) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(xq) + i);
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    float4* dst = reinterpret_cast<float4*>(y) + 4 * i;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int32_t b0 = static_cast<int8_t>(w[k] & 0xFF), b1 = static_cast<int8_t>((w[k] >> 8) & 0xFF);
-      const int32_t b2 = static_cast<int8_t>((w[k] >> 16) & 0xFF), b3 = static_cast<int8_t>(w[k] >> 24);
-      dst[k] = make_float4(__fmul_rn(s, static_cast<float>(b0)), __fmul_rn(s, static_cast<float>(b1)),
-                           __fmul_rn(s, static_cast<float>(b2)), __fmul_rn(s, static_cast<float>(b3)));
-    }
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += 2 * stride) {
+    const uint32_t w0 = __ldg(reinterpret_cast<const uint32_t*>(xq) + i);
+    const int64_t i2 = i + stride;
+    const uint32_t w1 = i2 < n4 ? __ldg(reinterpret_cast<const uint32_t*>(xq) + i2) : 0u;
+    reinterpret_cast<float4*>(y)[i] =
+        make_float4(__fmul_rn(s, static_cast<float>(static_cast<int8_t>(w0 & 0xFF))),
+                    __fmul_rn(s, static_cast<float>(static_cast<int8_t>((w0 >> 8) & 0xFF))),
+                    __fmul_rn(s, static_cast<float>(static_cast<int8_t>((w0 >> 16) & 0xFF))),
+                    __fmul_rn(s, static_cast<float>(static_cast<int8_t>(w0 >> 24))));
+    if (i2 < n4)
+      reinterpret_cast<float4*>(y)[i2] =
+          make_float4(__fmul_rn(s, static_cast<float>(static_cast<int8_t>(w1 & 0xFF))),
+                      __fmul_rn(s, static_cast<float>(static_cast<int8_t>((w1 >> 8) & 0xFF))),
+                      __fmul_rn(s, static_cast<float>(static_cast<int8_t>((w1 >> 16) & 0xFF))),
+                      __fmul_rn(s, static_cast<float>(static_cast<int8_t>(w1 >> 24))));
   }
-  for (int64_t i = nvec * 16 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < numel; i += stride)
+  for (int64_t i = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < numel; i += stride)
     y[i] = __fmul_rn(s, static_cast<float>(xq[i]));
 }
 
@@ -232,9 +431,71 @@ static int stream_grid(int64_t thread_items, int ntensors) {
   return static_cast<int>(blocks);
 }
 
+// Single-pass fused launch (three tensors) when every thread's share fits in
+// registers (<= 4 vectors per tensor).  Returns cudaErrorNotSupported (nothing
+// enqueued) otherwise.
+template <typename T, int VPT>
+static cudaError_t launch_fused_vpt(const QuantTensors& t, int64_t numel, float* partial,
+                                    IntParams* prm_out, int32_t head_dim, int blocks,
+                                    cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+  cfg.blockDim = dim3(kFThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, quantize_fused_kernel<T, VPT>, t, numel, partial, prm_out, head_dim);
+}
+
+template <typename T>
+static cudaError_t launch_fused_t(const QuantTensors& t, int ntensors, int64_t numel,
+                                  float* partial, IntParams* prm_out, int32_t head_dim,
+                                  cudaStream_t stream) {
+  if (ntensors != 3) return cudaErrorNotSupported;
+  constexpr int kE = 16 / sizeof(T);
+  const int64_t nvec = numel / kE;
+  // blocks: as few as needed at <= 4 vectors per thread, capped at full occupancy
+  const int64_t cap = static_cast<int64_t>(num_sms()) * kFBlocksPerSM;
+  int64_t blocks = (nvec + kFThreads - 1) / kFThreads;  // VPT = 1
+  int vpt = 1;
+  while (blocks > cap && vpt < 4) {
+    ++vpt;
+    blocks = (nvec + static_cast<int64_t>(kFThreads) * vpt - 1) / (static_cast<int64_t>(kFThreads) * vpt);
+  }
+  if (blocks > cap) return cudaErrorNotSupported;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 960) return cudaErrorNotSupported;  // partials must fit the workspace
+  switch (vpt) {
+    case 1: return launch_fused_vpt<T, 1>(t, numel, partial, prm_out, head_dim, static_cast<int>(blocks), stream);
+    case 2: return launch_fused_vpt<T, 2>(t, numel, partial, prm_out, head_dim, static_cast<int>(blocks), stream);
+    case 3: return launch_fused_vpt<T, 3>(t, numel, partial, prm_out, head_dim, static_cast<int>(blocks), stream);
+    default: return launch_fused_vpt<T, 4>(t, numel, partial, prm_out, head_dim, static_cast<int>(blocks), stream);
+  }
+}
+
 // dtype: 0 f32, 1 bf16, 2 f16.  Requires 16-byte aligned x and xq (checked by host).
+// `partial` (device, >= 3 * #SMs floats) enables the single-pass fused kernel.
 cudaError_t launch_quantize(const QuantTensors& t, int ntensors, int dtype, int64_t numel,
-                            IntParams* prm_out, int32_t head_dim, cudaStream_t stream) {
+                            IntParams* prm_out, int32_t head_dim, cudaStream_t stream,
+                            float* partial) {
+  static int fused_mode = -1;  // QFLASH_QUANT_FUSED=0 disables the single-pass kernel
+  if (fused_mode < 0) {
+    const char* env = getenv("QFLASH_QUANT_FUSED");
+    fused_mode = (env != nullptr && env[0] == '0') ? 0 : 1;
+  }
+  if (fused_mode == 1 && partial != nullptr && numel > 0) {
+    cudaError_t e = cudaErrorNotSupported;
+    switch (dtype) {
+      case 0: e = launch_fused_t<float>(t, ntensors, numel, partial, prm_out, head_dim, stream); break;
+      case 1: e = launch_fused_t<__nv_bfloat16>(t, ntensors, numel, partial, prm_out, head_dim, stream); break;
+      case 2: e = launch_fused_t<__half>(t, ntensors, numel, partial, prm_out, head_dim, stream); break;
+    }
+    if (e != cudaErrorNotSupported) return e;
+  }
   const bool contiguous = ntensors == 3 && t.scale[1] == t.scale[0] + 1 && t.scale[2] == t.scale[0] + 2;
   if (contiguous) {
     cudaError_t e = cudaMemsetAsync(t.scale[0], 0, 3 * sizeof(float), stream);

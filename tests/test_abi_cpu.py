@@ -164,15 +164,16 @@ def _hi32(a, b):
     return ((a & 0xFFFFFFFF) * (b & 0xFFFFFFFF)) >> 32
 
 
-def _release_fast(X, alpha, D):
-    a_f = ((alpha << 32) // D) & 0xFFFFFFFF
-    a_c = (a_f + 1) & 0xFFFFFFFF
-    m = 0xFFFFFFFF if X < 0 else 0
-    a = (a_c + m) & 0xFFFFFFFF
-    corr = ((-a_f) & 0xFFFFFFFF) & m
-    q = (_hi32(X, a) + corr) & 0xFFFFFFFF
-    q = q - (1 << 32) if q >= (1 << 31) else q
-    return X if alpha == D else q
+def _release_fast(X, alpha, D, bound):
+    """make_biased_release + BiasedRelease.apply (valid when (2 bound + D) D < 2^32)."""
+    B = bound // D + 1
+    BD = (B * D) & 0xFFFFFFFF
+    ident = alpha == D
+    A = 0xFFFFFFFF if ident else ((((alpha << 32) // D) & 0xFFFFFFFF) + 1) & 0xFFFFFFFF
+    add = ((-(B * alpha)) + (1 if ident else 0)) & 0xFFFFFFFF
+    Xp = (X + BD) & 0xFFFFFFFF
+    q = (_hi32(Xp, A) + add) & 0xFFFFFFFF
+    return q - (1 << 32) if q >= (1 << 31) else q
 
 
 def _release_slow(X, alpha, D):
@@ -185,13 +186,14 @@ def _release_slow(X, alpha, D):
 @pytest.mark.parametrize("D", [2, 3, 97, 1024, 1420, 2048, 8030, 65537, (1 << 24) - 3])
 def test_kernel_release_arithmetic(D):
     rng = np.random.default_rng(D)
-    lim_fast = (1 << 32) // D
     alphas = [0, 1, D // 2, D - 1, D] + [int(a) for a in rng.integers(0, D + 1, 40)]
+    max_bound = ((1 << 32) // D - D) // 2          # (2 bound + D) D < 2^32
     for alpha in alphas:
-        xs = [0, 1, -1, lim_fast - 1, -(lim_fast - 1)]
-        xs += [int(x) for x in rng.integers(-(lim_fast - 1), lim_fast, 200)]
-        for X in xs:
-            assert _release_fast(X, alpha, D) == (X * alpha) // D, (X, alpha)
+        if max_bound > 0:
+            for bound in [0, 1, max_bound] + [int(b) for b in rng.integers(0, max_bound + 1, 8)]:
+                xs = [0, 1, -1, bound, -bound] + [int(x) for x in rng.integers(-bound, bound + 1, 40)]
+                for X in xs:
+                    assert _release_fast(X, alpha, D, bound) == (X * alpha) // D, (X, alpha, bound)
         xs = [int(x) for x in rng.integers(-(1 << 31), 1 << 31, 200)] + [(1 << 31) - 1, -(1 << 31)]
         for X in xs:
             assert _release_slow(X, alpha, D) == (X * alpha) // D, (X, alpha)

@@ -1,0 +1,7 @@
+set -x
+QFLASH_ATTN_NWG=2 timeout 900 python -m pytest tests -m gpu -q -x -k "edge or workload or adversarial or full_size" 2>&1 | tail -3
+for n in 4 2; do
+  QFLASH_ATTN_NWG=$n timeout 300 python bench.py --no-cpu-baseline --no-e2e --steps 2000 2>&1 | tail -1 > gpurun_out/bench_a3_n$n.log
+  QFLASH_ATTN_NWG=$n timeout 300 python bench.py --workload A4 --no-cpu-baseline --no-e2e --steps 2000 2>&1 | tail -1 > gpurun_out/bench_a4_n$n.log
+  QFLASH_ATTN_NWG=$n timeout 300 python bench.py --workload L14 --batch 64 --steps 20 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 > gpurun_out/bench_l14_n$n.log
+done
