@@ -80,12 +80,19 @@ typedef struct {
                            CONTRACT: the tiled result depends on B_c (R15).          */
 } qflash_attn_shape;
 
-/* Kernel selection (tests / ablation).  AUTO picks the Swin-packed kernel when
- * N <= 64 and the generic tiled kernel otherwise; both give identical bytes. */
+/* Kernel tiling (tests / ablation); every variant gives identical bytes.
+ *   GENERIC: one 128-row query tile of one problem per work item (ceil(N/128)
+ *            tiles per problem, the last one ragged).
+ *   PACKED:  the query rows of all problems are flattened and cut into 128-row
+ *            tiles that may span up to 4 consecutive problems (Swin windows
+ *            N = 49 pack 2.6 per tile; ViT N = 197 at batch 8 needs 148 tiles
+ *            instead of 192).  Requires seq_len >= 43 and, for head_dim = 128,
+ *            seq_len >= 127 with B_c <= 128; QFLASH_ERR_UNSUPPORTED_SHAPE otherwise.
+ *   AUTO:    PACKED when supported and it needs fewer tiles, else GENERIC. */
 typedef enum {
   QFLASH_VARIANT_AUTO = 0,
   QFLASH_VARIANT_GENERIC = 1,
-  QFLASH_VARIANT_PACKED = 2 /* requires N <= 64 */
+  QFLASH_VARIANT_PACKED = 2
 } qflash_variant;
 
 /* --------------------------------------------------------------------------

@@ -1,25 +1,34 @@
 // qflash_attention.cu -- the fused integer-only attention kernel (Algorithm 1 of
 // arxiv 2604.25306) for B200 / sm_100a.
 //
-// One CTA owns one 128-row query tile (B_r = 128 = the tcgen05 M; TMEM lane r =
-// query row r).  Warp roles (640 threads):
-//   warp 0       TMA producer: Q tile once, K_j / V_j through a 2-stage ring
+// One CTA owns one 128-row query tile at a time (B_r = 128 = the tcgen05 M;
+// TMEM lane r = tile row r) and walks its tiles persistently.  Warp roles:
+//   warp 0       TMA producer: Q tile(s), K_j / V_j through a 2-stage ring
 //   warp 1       MMA issuer:   S_j = Q K_j^T   (tcgen05.mma kind::i8, SS, s32 in TMEM)
 //                              O  += P_j V_j   (kind::i8, TS: P from TMEM, V MN-major)
-//   warp 2       TMEM allocator
-//   warps 4..19  integer softmax in 4 warpgroups, thread = (query row, quarter
-//                of the key columns): rowmax (Eq. 4, combined through shared
-//                memory), ShiftExp2 (Alg. 2, division-free exact quotient),
-//                requantization (Eq. 10), ScaleRelease of O and l (Eq. 14),
-//                normalization (step 11).
+//   warp 2 / 1   TMEM allocator, reciprocal-table loader
+//   softmax      integer softmax in kNWG warpgroups, thread = (query row, a
+//                column chunk): rowmax (Eq. 4, combined through shared memory),
+//                ShiftExp2 (Alg. 2, division-free exact quotient), requantization
+//                (Eq. 10), ScaleRelease of O and l (Eq. 14), normalization (11).
 // The row sum l (Eq. 11) is produced by the tensor core: V is extended with a
 // block of ones (N = d + 16), so TMEM column d of the O accumulator holds
 // floor-released l exactly as the oracle defines it.
 //
-// PACKED (the Swin-window variant, N <= 64): a 128-row tile holds two problems
-// (windows) at rows 0-63 / 64-127 and the KV tile holds their 2 x 64 keys;
-// each thread only evaluates its own window's diagonal block and writes P = 0
-// elsewhere, so P V never mixes windows.  T_c = 1.
+// Tiling (NSEG template parameter):
+//   NSEG = 1  "generic": tile = (problem, 128-row query block); T_r tiles per
+//             problem, the last one ragged.
+//   NSEG > 1  "row-packed": the query rows of all problems are flattened and cut
+//             into 128-row tiles, so a tile spans up to NSEG consecutive problems
+//             (segments).  Segment s gets its own Q tile, loaded by TMA with row
+//             coordinates shifted by -s N so that rows of other problems fall out
+//             of range and are zero-filled; S = sum_s Q_s K_{s,j}^T then holds every
+//             row's score against its OWN problem's keys in one accumulator.  P is
+//             written once per segment (the thread's own segment gets its P, the
+//             others zeros), and O = sum_s P_s [V_{s,j} | 1] again accumulates
+//             each row against its own values.  A3 (N = 197) at batch 8 becomes
+//             148 tiles (one per SM) instead of 192; Swin windows (N = 49) pack
+//             2.6 per tile instead of 2.
 //
 // No floating-point instruction is executed (integer-only audit in tests).
 #include <cuda.h>
@@ -49,6 +58,7 @@ constexpr RecipTable make_recip_table() {
 }
 __device__ const RecipTable g_recip = make_recip_table();
 
+
 constexpr int kStages = 2;
 constexpr int kBlockR = 128;
 
@@ -59,15 +69,15 @@ constexpr int kBlockR = 128;
       args.dbg_t[(slot)] = clock64();                                             \
   } while (0)
 
-template <int D, int BC>
+template <int D, int BC, int NSEG>
 struct SmemLayout {
   static constexpr int kQBytes = kBlockR * D;
   static constexpr int kKVBytes = BC * D;
   static constexpr int kOnesBytes = BC * D;  // second MN atom of the extended V
-  static constexpr int kQ = 0;                          // [2] Q tiles (double buffer)
-  static constexpr int kK = kQ + 2 * kQBytes;
-  static constexpr int kV = kK + kStages * kKVBytes;
-  static constexpr int kOnes = kV + kStages * kKVBytes;
+  static constexpr int kQ = 0;                                  // [2][NSEG] Q tiles
+  static constexpr int kK = kQ + 2 * NSEG * kQBytes;            // [kStages][NSEG]
+  static constexpr int kV = kK + kStages * NSEG * kKVBytes;     // [kStages][NSEG]
+  static constexpr int kOnes = kV + kStages * NSEG * kKVBytes;
   static constexpr int kBar = kOnes + kOnesBytes;
   static constexpr int kNumBars = 2 * kStages + 8;
   static constexpr int kTmemSlot = kBar + kNumBars * 8;
@@ -77,12 +87,8 @@ struct SmemLayout {
   static constexpr int kAlloc = kTotal + 1024;  // slack for 1024-B alignment
 };
 
-__host__ __device__ constexpr uint32_t tmem_cols_for(int BC, int D) {
-  return (BC + D + 16) <= 32    ? 32
-         : (BC + D + 16) <= 64  ? 64
-         : (BC + D + 16) <= 128 ? 128
-         : (BC + D + 16) <= 256 ? 256
-                                : 512;
+__host__ __device__ constexpr uint32_t tmem_cols_pow2(int cols) {
+  return cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
 }
 
 template <int D>
@@ -238,106 +244,125 @@ QF_DEV int32_t floor_div_exact(int32_t O, int32_t l) {
 }
 
 // ---------------------------------------------------------------- configuration
-// Warps 0..3: control (TMA producer, MMA issuer, TMEM allocator, table loader);
-// warps 4..19: four softmax warpgroups.  Warp w >= 4 handles TMEM lane quarter
-// (w & 3), i.e. query rows 32*(w&3) .. +31 (thread = row); its warpgroup
-// g = (w - 4) / 4 owns key columns [g*CW, (g+1)*CW) of every S tile and O
-// columns [g*D/4, (g+1)*D/4) for the release and the normalization.  The row
+// Warps 0..kCtl-1: control (TMA producer, MMA issuer, TMEM allocator, table
+// loader); then kNWG softmax warpgroups.  Softmax warp w handles TMEM lane
+// quarter (w & 3), i.e. tile rows 32*(w&3) .. +31 (thread = row); its warpgroup
+// g owns key columns [g*CW, (g+1)*CW) of every S tile and O columns
+// [g*D/kNWG, (g+1)*D/kNWG) for the release and the normalization.  The row
 // maximum is combined across warpgroups through shared memory (one named
 // barrier per KV tile).
-// MODE 0: one CTA per SM, 4 softmax warpgroups, 4 control warps, double S buffer.
-// MODE 1: two CTAs per SM (when TMEM allows), 2 softmax warpgroups, 2 control warps.
-// MODE 2: two CTAs per SM (when TMEM allows), 4 softmax warpgroups, 2 control
-//         warps, S processed in 16-column chunks to fit ~56 registers per thread.
-template <int D, int BC, bool PACKED, int MODE>
+// MODE 0: one CTA per SM, 4 softmax warpgroups, 4 control warps.
+// MODE 1: two CTAs per SM when TMEM allows, 2 softmax warpgroups, 2 control warps.
+template <int D, int BC, int NSEG, int MODE>
 struct Cfg {
   static constexpr int kNWG = MODE == 1 ? 2 : 4;          // softmax warpgroups
   static constexpr int kCtl = MODE == 0 ? 4 : 2;          // control warps
   static constexpr int kSoftThreads = 128 * kNWG;
   static constexpr int kThreads = 32 * kCtl + kSoftThreads;
-  static constexpr int kCW = (PACKED ? 64 : BC) / kNWG;   // key columns per thread
+  static constexpr int kCW = BC / kNWG;                   // key columns per thread
   static constexpr int kOW = D / kNWG;                    // O columns per thread
-  static constexpr int kChunk = MODE == 2 ? (kCW < 16 ? kCW : 16) : (kCW < 32 ? kCW : 32);
+  static constexpr int kChunk = kCW < 32 ? kCW : 32;
   static constexpr bool kSInRegs = kCW == kChunk;
   static constexpr int kAllocWarp = kCtl == 4 ? 2 : 1;    // TMEM allocator
   static constexpr int kTableWarp = kCtl == 4 ? 3 : 1;    // reciprocal-table loader
-  // TMEM: kNumS S buffers of BC columns (P_j aliases its own S buffer), then O
-  // (D columns) + l (column D) + 15 copies of l from the ones block.
+  // TMEM: kNumS S buffers of BC columns (the P_s of tile j alias S buffer j:
+  // segment s at columns [s BC/4, (s+1) BC/4)), then O (D columns) + l (column
+  // D) + 15 copies of l from the ones block.
   static constexpr int kMinBlocks = (MODE != 0 && BC + D + 16 <= 256) ? 2 : 1;
-  static constexpr int kNumS = (kMinBlocks == 1 && 2 * BC + D + 16 <= 512) ? 2 : 1;
+  static constexpr int kTmemBudget = kMinBlocks == 2 ? 256 : 512;
+  static constexpr int kNumS = (2 * BC + D + 16 <= kTmemBudget) ? 2 : 1;
   static constexpr uint32_t kTmemO = kNumS * BC;
+  static constexpr uint32_t kTmemCols = tmem_cols_pow2(kNumS * BC + D + 16);
+  static_assert(NSEG * (BC / 4) <= BC, "P segments must fit in one S buffer");
 };
 
-// Persistent tile iterator (identical in every role).  Generic: tile t =
-// problem * T_r + query-tile, CTA b visits t = b, b + G, b + 2G, ...  Packed:
-// tile t = windows (2t, 2t + 1).  No runtime division (integer-only kernel):
-// the host supplies G / T_r, G % T_r and a magic for the first tile.
+// Persistent tile iterator (identical in every role); no runtime division
+// (integer-only kernel): the host supplies the magics and the grid-stride
+// quotient/remainder.
+//   generic (NSEG = 1): tile t = problem * T_r + qt, rows [128 qt, 128 qt + 128).
+//   row-packed:         tile t = flattened rows [128 t, 128 t + 128) of [P N].
+// Either way the tile starts at row `off` of problem `problem` and tile row r is
+// flattened row problem * N + off + r.
+template <int NSEG>
 struct TileIter {
-  int problem, qt, i;
-  __device__ void init(const AttnArgs& a, bool packed) {
+  int problem;  // first problem of the tile
+  int off;      // row of tile row 0 inside `problem`
+  int rows;     // live tile rows [0, rows)
+  int nseg;     // problems the tile spans (1..NSEG)
+  int i;        // tiles visited by this CTA
+  __device__ void fill(const AttnArgs& a) {
+    if constexpr (NSEG == 1) {
+      rows = min(kBlockR, a.N - off);
+      nseg = 1;
+    } else {
+      const int64_t left = static_cast<int64_t>(a.P - problem) * a.N - off;
+      rows = left < kBlockR ? static_cast<int>(left) : kBlockR;
+      const int last = off + rows - 1;
+      nseg = 1 + (last >= a.N ? 1 : 0);
+      if constexpr (NSEG > 2) nseg += (last >= 2 * a.N ? 1 : 0) + (last >= 3 * a.N ? 1 : 0);
+    }
+  }
+  __device__ void init(const AttnArgs& a) {
     i = 0;
     const uint32_t t = blockIdx.x;
-    if (packed) {
-      problem = 2 * static_cast<int>(t);
-      qt = 0;
-    } else if (a.Tr == 1) {
-      problem = static_cast<int>(t);
-      qt = 0;
+    if constexpr (NSEG == 1) {
+      problem = a.Tr == 1 ? static_cast<int>(t) : static_cast<int>(__umulhi(t, a.tr_magic));
+      off = (static_cast<int>(t) - problem * a.Tr) * kBlockR;
     } else {
-      problem = static_cast<int>(__umulhi(t, a.tr_magic));  // t / T_r (exact for t < 2^32 / T_r)
-      qt = static_cast<int>(t) - problem * a.Tr;
+      const uint64_t row0 = static_cast<uint64_t>(t) * kBlockR;
+      problem = static_cast<int>(__umul64hi(row0, a.n_magic));  // floor(row0 / N), exact
+      off = static_cast<int>(row0 - static_cast<uint64_t>(problem) * a.N);
     }
+    if (problem < a.P) fill(a);
   }
-  __device__ bool valid(const AttnArgs& a, bool packed) const {
-    return packed ? problem < a.P : problem < a.P;
-  }
-  __device__ void next(const AttnArgs& a, bool packed) {
+  __device__ bool valid(const AttnArgs& a) const { return problem < a.P; }
+  __device__ void next(const AttnArgs& a) {
     ++i;
-    if (packed) {
-      problem += 2 * static_cast<int>(gridDim.x);
-    } else {
-      problem += a.g_div;
-      qt += a.g_mod;
-      if (qt >= a.Tr) {
-        qt -= a.Tr;
-        ++problem;
-      }
+    problem += a.g_div;
+    off += a.g_mod;
+    const int lim = NSEG == 1 ? a.Tr * kBlockR : a.N;
+    if (off >= lim) {
+      off -= lim;
+      ++problem;
     }
+    if (problem < a.P) fill(a);
   }
 };
 
 // ---------------------------------------------------------------- softmax role
-template <int D, int BC, bool PACKED, int MODE, bool FASTQ>
+template <int D, int BC, int NSEG, int MODE, bool FASTQ>
 __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntParams& prm,
                                              uint32_t tmem_base, uint64_t* bar_s_full,
                                              uint64_t* bar_p_full, uint64_t* bar_o_full,
                                              int32_t* red, const uint32_t* recip, int warp,
                                              int lane) {
-  using C = Cfg<D, BC, PACKED, MODE>;
+  using C = Cfg<D, BC, NSEG, MODE>;
   constexpr int CW = C::kCW;
   constexpr int OW = C::kOW;
   const int N = args.N;
-  const int Tc = PACKED ? 1 : args.Tc;
+  const int Tc = args.Tc;
   const int g = (warp - C::kCtl) >> 2;  // warpgroup
   const int quarter = warp & 3;
   const int row = quarter * 32 + lane;  // TMEM lane == tile row
   const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
   const uint32_t tS0 = tmem_base + lane_off;  // S buffer b at + b * BC
   const uint32_t tO = tmem_base + lane_off + C::kTmemO;
-  const int win = PACKED ? (row >> 6) : 0;
-  const int c0 = (PACKED ? win * 64 : 0) + g * CW;  // first key column of this thread
-  const int c0_in_tile = g * CW;                    // ... relative to its window / tile
+  const int c0 = g * CW;  // first key column of this thread
   const bool dbg_cta = blockIdx.x == 0;
 
-  TileIter ti;
-  ti.init(args, PACKED);
-  for (; ti.valid(args, PACKED); ti.next(args, PACKED)) {
-    const int problem = ti.problem;
-    const int q0 = ti.qt * kBlockR;
+  TileIter<NSEG> ti;
+  ti.init(args);
+  for (; ti.valid(args); ti.next(args)) {
     const bool dbg = dbg_cta && ti.i == 0;
-    // rows of a padded tail tile (or of a missing second window) do no work
-    const int rows_valid = PACKED ? ((problem + 1 < args.P) ? 128 : 64) : (N - q0);
-    const bool warp_live = PACKED ? ((quarter >> 1) * 64 < rows_valid) : (quarter * 32 < rows_valid);
+    const bool live = row < ti.rows;              // padded rows of the last tile do no work
+    const bool warp_live = quarter * 32 < ti.rows;
+    int seg = 0;                                  // this row's problem = ti.problem + seg
+    if constexpr (NSEG > 1) {
+      const int x = ti.off + row;
+      seg = (x >= N ? 1 : 0);
+      if constexpr (NSEG > 2) seg += (x >= 2 * N ? 1 : 0) + (x >= 3 * N ? 1 : 0);
+    }
+    const int nseg = ti.nseg;
     int32_t m = -(1 << 21);  // m^(0) = -2^21
     const int it0 = ti.i * Tc;
 
@@ -347,9 +372,9 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
       const uint32_t tS = tS0 + sb * BC;
       mbar_wait(&bar_s_full[sb], (C::kNumS == 2 ? (it >> 1) : it) & 1);
       tc_fence_after();
-      if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(40 + 8 * j);
+      if (dbg && warp == C::kCtl && lane == 0 && j < 7) QF_TS(40 + 8 * j);
       // columns of this thread that exist in KV tile j (ragged last tile, R16)
-      const int valid = (PACKED ? N : min(BC, N - j * BC)) - c0_in_tile;
+      const int valid = min(BC, N - j * BC) - c0;
       constexpr int CK = C::kChunk;
       uint32_t s[C::kSInRegs ? CW : CK];
       int32_t tmax = INT32_MIN;
@@ -387,14 +412,14 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
         int32_t* rb = red + (it & 1) * (C::kNWG * 128);
         rb[g * 128 + row] = tmax;
         named_bar_sync(1, C::kSoftThreads);
-        if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(41 + 8 * j);
+        if (dbg && warp == C::kCtl && lane == 0 && j < 7) QF_TS(41 + 8 * j);
 #pragma unroll
         for (int h = 0; h < C::kNWG; ++h) tmax = max(tmax, rb[h * 128 + row]);
       }
       const int32_t m_new = max(m, tmax);
       // (4) alpha = ShiftExp2(m_old - m_new)
       const int32_t alpha = shift_exp2<FASTQ>(m - m_new, prm);
-      if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(42 + 8 * j);
+      if (dbg && warp == C::kCtl && lane == 0 && j < 7) QF_TS(42 + 8 * j);
 
       // (5)(6) P = Requant(ShiftExp2(S - m_new)), 4 x int8 per TMEM column.
       const uint32_t mu = static_cast<uint32_t>(m_new);
@@ -445,19 +470,26 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
 #pragma unroll
         for (int e = 0; e < CW / 4; ++e) pk[e] = 0u;
       }
-      // P columns [c0/4, (c0+CW)/4) alias S columns of warpgroup 0: every S read
-      // of this tile must be complete.  With S in registers the max-exchange
-      // barrier above already ordered them; otherwise synchronize again.
+      // P_s columns [s BC/4 + c0/4, +CW/4) alias S columns of this buffer: every
+      // S read of this tile must be complete.  With S in registers the
+      // max-exchange barrier above already ordered them; otherwise synchronize again.
       if constexpr (!C::kSInRegs) named_bar_sync(1, C::kSoftThreads);
-      tmem_st<CW / 4>(tS + (c0 >> 2), pk);
-      if constexpr (PACKED) {
-        // zero this group's share of the other window's P columns
-        uint32_t z[CW / 4];
+      if (nseg == 1) {
+        tmem_st<CW / 4>(tS + (c0 >> 2), pk);
+      } else {
+        // segment s gets this row's P if the row belongs to it, zeros otherwise
+        // (rows of dead lanes have pk = 0 already)
 #pragma unroll
-        for (int e = 0; e < CW / 4; ++e) z[e] = 0u;
-        tmem_st<CW / 4>(tS + (((1 - win) * 64 + c0_in_tile) >> 2), z);
+        for (int sg = 0; sg < NSEG; ++sg) {
+          if (sg < nseg) {
+            uint32_t z[CW / 4];
+#pragma unroll
+            for (int e = 0; e < CW / 4; ++e) z[e] = (seg == sg && live) ? pk[e] : 0u;
+            tmem_st<CW / 4>(tS + sg * (BC / 4) + (c0 >> 2), z);
+          }
+        }
       }
-      if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(44 + 8 * j);
+      if (dbg && warp == C::kCtl && lane == 0 && j < 7) QF_TS(44 + 8 * j);
 
       // (7)(8) ScaleRelease of O (this group's columns) and l (group 0) once
       // PV_{j-1} has landed -- after P_j so that PV_{j-1} completes behind the P
@@ -467,14 +499,14 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
       if (j > 0) {
         mbar_wait(bar_o_full, (it - 1) & 1);
         tc_fence_after();
-        if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(45 + 8 * j);
+        if (dbg && warp == C::kCtl && lane == 0 && j < 7) QF_TS(45 + 8 * j);
         if (warp_live && __any_sync(0xffffffffu, alpha != prm.s_inv)) {
           uint32_t o[OW];
           tmem_ld<OW>(tO + g * OW, o);
           uint32_t lcol;
           tmem_ld1(tO + D, lcol);
           tmem_wait_ld();
-          if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(46 + 8 * j);
+          if (dbg && warp == C::kCtl && lane == 0 && j < 7) QF_TS(46 + 8 * j);
           // Fast exact path when every row of the warp satisfies |X| s_inv < 2^32
           // for all its accumulators X (bound |O| <= 128 (l + 2 T_c), DESIGN.md
           // "Kernel arithmetic"): floor(X alpha / s_inv) is then the high word of
@@ -498,7 +530,7 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
               tmem_st1(tO + D, lcol);
             }
           }
-          if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(47 + 8 * j);
+          if (dbg && warp == C::kCtl && lane == 0 && j < 7) QF_TS(47 + 8 * j);
         }
       }
 
@@ -517,14 +549,14 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_p_full);
-      if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0 && j < 7) QF_TS(43 + 8 * j);
+      if (dbg && warp == C::kCtl && lane == 0 && j < 7) QF_TS(43 + 8 * j);
       m = m_new;
     }
 
     // (11) O_i = floor(O / l), saturated to int8 (R14); this group's O columns.
     mbar_wait(bar_o_full, (it0 + Tc - 1) & 1);
     tc_fence_after();
-    if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0) QF_TS(100);
+    if (dbg && warp == C::kCtl && lane == 0) QF_TS(100);
     if (ti.i == 0) named_bar_sync(2, C::kSoftThreads + 32);  // reciprocal table ready
     if (warp_live) {
       uint32_t lraw;
@@ -536,31 +568,21 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
         for (int e = 0; e < OW; ++e) args.dbg_o[row * (D + 1) + g * OW + e] = static_cast<int32_t>(o[e]);
         if (g == 0) args.dbg_o[row * (D + 1) + D] = static_cast<int32_t>(lraw);
       }
-      const Recip rc = make_recip(static_cast<int32_t>(lraw), recip);
-      int32_t qv[OW];
-      bool bad = false;
+      if (live) {
+        const Recip rc = make_recip(static_cast<int32_t>(lraw), recip);
+        int32_t qv[OW];
+        bool bad = false;
 #pragma unroll
-      for (int e = 0; e < OW; ++e) qv[e] = floor_div(static_cast<int32_t>(o[e]), rc, bad);
-      if (__any_sync(0xffffffffu, bad)) {
+        for (int e = 0; e < OW; ++e) qv[e] = floor_div(static_cast<int32_t>(o[e]), rc, bad);
+        if (bad) {
 #pragma unroll
-        for (int e = 0; e < OW; ++e) qv[e] = floor_div_exact(static_cast<int32_t>(o[e]), rc.l);
-      }
-      uint32_t w[OW / 4];
+          for (int e = 0; e < OW; ++e) qv[e] = floor_div_exact(static_cast<int32_t>(o[e]), rc.l);
+        }
+        uint32_t w[OW / 4];
 #pragma unroll
-      for (int e = 0; e < OW; e += 4) w[e / 4] = pack4_sat_s8(qv[e], qv[e + 1], qv[e + 2], qv[e + 3]);
-      int out_problem, out_row;
-      bool ok;
-      if constexpr (PACKED) {
-        out_problem = problem + win;
-        out_row = row & 63;
-        ok = out_row < N && out_problem < args.P;
-      } else {
-        out_problem = problem;
-        out_row = q0 + row;
-        ok = out_row < N;
-      }
-      if (ok) {
-        int8_t* dst = args.out + (static_cast<int64_t>(out_problem) * N + out_row) * D + g * OW;
+        for (int e = 0; e < OW; e += 4) w[e / 4] = pack4_sat_s8(qv[e], qv[e + 1], qv[e + 2], qv[e + 3]);
+        // flattened output row problem * N + off + row (row-packed tiles included)
+        int8_t* dst = args.out + (static_cast<int64_t>(ti.problem) * N + ti.off + row) * D + g * OW;
         if constexpr (OW == 8) {
           *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
         } else {
@@ -570,22 +592,21 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
         }
       }
     }
-    if (dbg && warp == C::kCtl + (4 - C::kCtl % 4) % 4 && lane == 0) QF_TS(101);
+    if (dbg && warp == C::kCtl && lane == 0) QF_TS(101);
     // The O/l loads above completed (wait::ld) before this thread's next p_full
     // arrival, so the next tile's first PV (which overwrites O) cannot race them.
   }
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int D, int BC, bool PACKED, int MODE>
-__global__ void __launch_bounds__(Cfg<D, BC, PACKED, MODE>::kThreads, Cfg<D, BC, PACKED, MODE>::kMinBlocks)
+template <int D, int BC, int NSEG, int MODE>
+__global__ void __launch_bounds__(Cfg<D, BC, NSEG, MODE>::kThreads, Cfg<D, BC, NSEG, MODE>::kMinBlocks)
     qflash_attn_kernel(const __grid_constant__ CUtensorMap tm_q,
                        const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, const AttnArgs args) {
-  using L = SmemLayout<D, BC>;
-  using C = Cfg<D, BC, PACKED, MODE>;
-  constexpr uint32_t kTmemCols = tmem_cols_for(C::kNumS * BC, D);
-  static_assert(kTmemCols >= C::kNumS * BC + D + 16, "TMEM budget");
+  using L = SmemLayout<D, BC, NSEG>;
+  using C = Cfg<D, BC, NSEG, MODE>;
+  constexpr uint32_t kTmemCols = C::kTmemCols;
   constexpr uint32_t kSwz = swizzle_layout<D>();
   constexpr int kNO = D + 16;  // extended PV width (O columns + ones block)
   constexpr uint32_t kIdescQK = make_idesc_i8(128, BC, 0, 0);
@@ -594,9 +615,9 @@ __global__ void __launch_bounds__(Cfg<D, BC, PACKED, MODE>::kThreads, Cfg<D, BC,
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint8_t* sQ = smem + L::kQ;  // [2]
-  uint8_t* sK = smem + L::kK;
-  uint8_t* sV = smem + L::kV;
+  uint8_t* sQ = smem + L::kQ;  // [2][NSEG]
+  uint8_t* sK = smem + L::kK;  // [kStages][NSEG]
+  uint8_t* sV = smem + L::kV;  // [kStages][NSEG]
   uint8_t* sOnes = smem + L::kOnes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* bar_kv_full = bars;              // [kStages]
@@ -613,7 +634,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, PACKED, MODE>::kThreads, Cfg<D, BC,
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0 && blockIdx.x == 0) QF_TS(0);
-  const int Tc = PACKED ? 1 : args.Tc;
+  const int Tc = args.Tc;
 
   // ------------------------------------------------------------- setup
   if (warp == 0 && lane == 0) {
@@ -663,24 +684,28 @@ __global__ void __launch_bounds__(Cfg<D, BC, PACKED, MODE>::kThreads, Cfg<D, BC,
     if (warp == 0) {
       // ========================================================= TMA producer
       if (lane == 0) {
-        TileIter ti;
-        ti.init(args, PACKED);
+        TileIter<NSEG> ti;
+        ti.init(args);
         int it = 0;
-        for (; ti.valid(args, PACKED); ti.next(args, PACKED)) {
+        for (; ti.valid(args); ti.next(args)) {
           const int qb = ti.i & 1;
           if (ti.i >= 2) mbar_wait(&bar_q_empty[qb], ((ti.i >> 1) - 1) & 1);
-          mbar_arrive_expect_tx(&bar_q_full[qb], L::kQBytes);
-          if constexpr (PACKED)
-            tma_load_3d(sQ + qb * L::kQBytes, &tm_q, &bar_q_full[qb], 0, 0, ti.problem);  // box {D,64,2}
-          else
-            tma_load_3d(sQ + qb * L::kQBytes, &tm_q, &bar_q_full[qb], 0, ti.qt * kBlockR, ti.problem);
+          mbar_arrive_expect_tx(&bar_q_full[qb], ti.nseg * L::kQBytes);
+          // segment s: rows of problem + s land at their tile rows, every other
+          // tile row is out of range (row < 0 or >= N) and zero-filled
+          for (int s = 0; s < ti.nseg; ++s)
+            tma_load_3d(sQ + (qb * NSEG + s) * L::kQBytes, &tm_q, &bar_q_full[qb], 0,
+                        ti.off - s * args.N, ti.problem + s);
           for (int j = 0; j < Tc; ++j, ++it) {
             const int st = it % kStages;
             if (it >= kStages) mbar_wait(&bar_kv_empty[st], ((it / kStages) - 1) & 1);
-            mbar_arrive_expect_tx(&bar_kv_full[st], 2 * L::kKVBytes);
-            const int kv_row = PACKED ? 0 : j * BC;
-            tma_load_3d(sK + st * L::kKVBytes, &tm_k, &bar_kv_full[st], 0, kv_row, ti.problem);
-            tma_load_3d(sV + st * L::kKVBytes, &tm_v, &bar_kv_full[st], 0, kv_row, ti.problem);
+            mbar_arrive_expect_tx(&bar_kv_full[st], ti.nseg * 2 * L::kKVBytes);
+            for (int s = 0; s < ti.nseg; ++s) {
+              tma_load_3d(sK + (st * NSEG + s) * L::kKVBytes, &tm_k, &bar_kv_full[st], 0, j * BC,
+                          ti.problem + s);
+              tma_load_3d(sV + (st * NSEG + s) * L::kKVBytes, &tm_v, &bar_kv_full[st], 0, j * BC,
+                          ti.problem + s);
+            }
           }
         }
       }
@@ -695,11 +720,11 @@ __global__ void __launch_bounds__(Cfg<D, BC, PACKED, MODE>::kThreads, Cfg<D, BC,
       if (lane == 0) {
         const uint32_t tO = tmem_base + C::kTmemO;
         const uint32_t ones_addr = smem_u32(sOnes);
-        TileIter ti;
-        ti.init(args, PACKED);
-        for (; ti.valid(args, PACKED); ti.next(args, PACKED)) {
+        TileIter<NSEG> ti;
+        ti.init(args);
+        for (; ti.valid(args); ti.next(args)) {
           const int qb = ti.i & 1;
-          const uint32_t q_addr = smem_u32(sQ + qb * L::kQBytes);
+          const int nseg = ti.nseg;
           const int it0 = ti.i * Tc;
           mbar_wait(&bar_q_full[qb], (ti.i >> 1) & 1);
           tc_fence_after();
@@ -711,13 +736,16 @@ __global__ void __launch_bounds__(Cfg<D, BC, PACKED, MODE>::kThreads, Cfg<D, BC,
             mbar_wait(&bar_kv_full[st], (it / kStages) & 1);
             tc_fence_after();
             if (ti.i == 0 && blockIdx.x == 0 && j < 7) QF_TS(3 + 4 * j);
-            const uint32_t k_addr = smem_u32(sK + st * L::kKVBytes);
-            // (1) S = Q K_j^T : M=128, N=BC, K=D in steps of 32 bytes.
+            // (1) S = sum_s Q_s K_{s,j}^T : M=128, N=BC, K=D in steps of 32 bytes.
+            for (int s = 0; s < nseg; ++s) {
+              const uint32_t q_addr = smem_u32(sQ + (qb * NSEG + s) * L::kQBytes);
+              const uint32_t k_addr = smem_u32(sK + (st * NSEG + s) * L::kKVBytes);
 #pragma unroll
-            for (int kk = 0; kk < D / 32; ++kk) {
-              const uint64_t da = make_smem_desc(q_addr + 32 * kk, 16, 8 * D, kSwz);
-              const uint64_t db = make_smem_desc(k_addr + 32 * kk, 16, 8 * D, kSwz);
-              mma_i8_ss(tmem_base + sb * BC, da, db, kIdescQK, kk > 0 ? 1u : 0u);
+              for (int kk = 0; kk < D / 32; ++kk) {
+                const uint64_t da = make_smem_desc(q_addr + 32 * kk, 16, 8 * D, kSwz);
+                const uint64_t db = make_smem_desc(k_addr + 32 * kk, 16, 8 * D, kSwz);
+                mma_i8_ss(tmem_base + sb * BC, da, db, kIdescQK, (s > 0 || kk > 0) ? 1u : 0u);
+              }
             }
             mma_commit(&bar_s_full[sb]);
             if (j == Tc - 1) mma_commit(&bar_q_empty[qb]);  // last read of this Q tile
@@ -726,16 +754,19 @@ __global__ void __launch_bounds__(Cfg<D, BC, PACKED, MODE>::kThreads, Cfg<D, BC,
             const int it = it0 + j;
             const int st = it % kStages;
             const int sb = (C::kNumS == 2) ? (it & 1) : 0;
-            const uint32_t v_addr = smem_u32(sV + st * L::kKVBytes);
-            // (8) O (+)= P_j [V_j | 1] : M=128, N=D+16, K=BC in steps of 32 keys.
+            // (8) O (+)= sum_s P_s [V_{s,j} | 1] : M=128, N=D+16, K=BC in steps of 32 keys.
             mbar_wait(bar_p_full, it & 1);
             tc_fence_after();
             if (ti.i == 0 && blockIdx.x == 0 && j < 7) QF_TS(4 + 4 * j);
+            for (int s = 0; s < nseg; ++s) {
+              const uint32_t v_addr = smem_u32(sV + (st * NSEG + s) * L::kKVBytes);
 #pragma unroll
-            for (int kk = 0; kk < BC / 32; ++kk) {
-              const uint32_t vk = v_addr + 32 * kk * D;
-              const uint64_t db = make_smem_desc(vk, ones_addr - v_addr, 8 * D, kSwz);
-              mma_i8_ts(tO, tmem_base + sb * BC + 8 * kk, db, kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
+              for (int kk = 0; kk < BC / 32; ++kk) {
+                const uint32_t vk = v_addr + 32 * kk * D;
+                const uint64_t db = make_smem_desc(vk, ones_addr - v_addr, 8 * D, kSwz);
+                mma_i8_ts(tO, tmem_base + sb * BC + s * (BC / 4) + 8 * kk, db, kIdescPV,
+                          (j > 0 || s > 0 || kk > 0) ? 1u : 0u);
+              }
             }
             mma_commit(&bar_kv_empty[st]);
             mma_commit(bar_o_full);
@@ -750,11 +781,11 @@ __global__ void __launch_bounds__(Cfg<D, BC, PACKED, MODE>::kThreads, Cfg<D, BC,
       }
     } else if (warp >= C::kCtl) {
       if (prm.q_shift == 0 && static_cast<uint64_t>(prm.s_inv) * static_cast<uint64_t>(prm.m_p) < (1ull << 32))
-        softmax_role<D, BC, PACKED, MODE, true>(args, prm, tmem_base, bar_s_full, bar_p_full,
-                                               bar_o_full, red, recip, warp, lane);
+        softmax_role<D, BC, NSEG, MODE, true>(args, prm, tmem_base, bar_s_full, bar_p_full,
+                                              bar_o_full, red, recip, warp, lane);
       else
-        softmax_role<D, BC, PACKED, MODE, false>(args, prm, tmem_base, bar_s_full, bar_p_full,
-                                                bar_o_full, red, recip, warp, lane);
+        softmax_role<D, BC, NSEG, MODE, false>(args, prm, tmem_base, bar_s_full, bar_p_full,
+                                               bar_o_full, red, recip, warp, lane);
     }
   }
 
@@ -769,12 +800,13 @@ __global__ void __launch_bounds__(Cfg<D, BC, PACKED, MODE>::kThreads, Cfg<D, BC,
 // ----------------------------------------------------------------------------
 // Host-side launch helpers (called by qflash_host.cu).  `tiles` = number of work
 // tiles; the persistent grid is min(tiles, CTAs-per-SM x SMs).
-template <int D, int BC, bool PACKED, int MODE>
+template <int D, int BC, int NSEG, int MODE>
 cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                           AttnArgs args, int64_t tiles, int sms, cudaStream_t stream) {
-  using L = SmemLayout<D, BC>;
-  using C = Cfg<D, BC, PACKED, MODE>;
-  auto kern = qflash_attn_kernel<D, BC, PACKED, MODE>;
+  using L = SmemLayout<D, BC, NSEG>;
+  using C = Cfg<D, BC, NSEG, MODE>;
+  static_assert(L::kAlloc <= 227 * 1024, "shared memory budget");
+  auto kern = qflash_attn_kernel<D, BC, NSEG, MODE>;
   static int configured[16] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -785,43 +817,60 @@ cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CU
   }
   const int64_t cap = static_cast<int64_t>(C::kMinBlocks) * sms;
   const int64_t G = tiles < cap ? tiles : cap;
-  const int64_t Tr = args.Tr;
-  args.tr_magic = Tr > 1 ? static_cast<uint32_t>(((1ull << 32) + Tr - 1) / Tr) : 0u;
-  args.g_div = static_cast<int32_t>(G / Tr);
-  args.g_mod = static_cast<int32_t>(G % Tr);
+  if (NSEG == 1) {
+    const int64_t Tr = args.Tr;
+    args.tr_magic = Tr > 1 ? static_cast<uint32_t>(((1ull << 32) + Tr - 1) / Tr) : 0u;
+    args.g_div = static_cast<int32_t>(G / Tr);
+    args.g_mod = static_cast<int32_t>((G % Tr) * kBlockR);
+  } else {
+    const uint64_t n = static_cast<uint64_t>(args.N);  // N >= 2 here
+    args.n_magic = ~0ull / n + 1ull;  // ceil(2^64 / N): floor(x / N) = hi64(x * n_magic), x < 2^32
+    const int64_t step = G * kBlockR;
+    args.g_div = static_cast<int32_t>(step / args.N);
+    args.g_mod = static_cast<int32_t>(step % args.N);
+  }
   kern<<<dim3(static_cast<unsigned>(G)), C::kThreads, L::kAlloc, stream>>>(tq, tk, tv, args);
   return cudaGetLastError();
 }
 
+// Supported instantiations (qflash_host.cu selects within them):
+//   NSEG 1: D in {32, 64, 128} x BC in {64, 128, 256}
+//   NSEG 2: D in {32, 64} x BC in {64, 128, 256}, D = 128 x BC in {64, 128}
+//   NSEG 4: D in {32, 64} x BC in {64, 128}
+bool attention_config_supported(int D, int BC, int nseg) {
+  if (D != 32 && D != 64 && D != 128) return false;
+  if (BC != 64 && BC != 128 && BC != 256) return false;
+  if (nseg == 1) return true;
+  if (nseg == 2) return D != 128 || BC != 256;
+  if (nseg == 4) return D != 128 && BC != 256;
+  return false;
+}
+
 template <int MODE>
-static cudaError_t launch_attention_mode(int D, int BC, bool packed, const CUtensorMap& tq,
+static cudaError_t launch_attention_mode(int D, int BC, int nseg, const CUtensorMap& tq,
                                         const CUtensorMap& tk, const CUtensorMap& tv,
                                         const AttnArgs& args, int64_t tiles, int sms,
                                         cudaStream_t stream) {
-  if (packed) {
-    // T_c = 1 and the KV tile is 2 x 64 keys regardless of block_kv.
-    switch (D) {
-      case 32: return launch_attn_t<32, 128, true, MODE>(tq, tk, tv, args, tiles, sms, stream);
-      case 64: return launch_attn_t<64, 128, true, MODE>(tq, tk, tv, args, tiles, sms, stream);
-      case 128: return launch_attn_t<128, 128, true, MODE>(tq, tk, tv, args, tiles, sms, stream);
-    }
-    return cudaErrorInvalidValue;
-  }
-#define QF_CASE(d, bc) \
-  if (D == d && BC == bc) return launch_attn_t<d, bc, false, MODE>(tq, tk, tv, args, tiles, sms, stream);
-  QF_CASE(32, 64) QF_CASE(32, 128) QF_CASE(32, 256)
-  QF_CASE(64, 64) QF_CASE(64, 128) QF_CASE(64, 256)
-  QF_CASE(128, 64) QF_CASE(128, 128) QF_CASE(128, 256)
+#define QF_CASE(d, bc, ns)                     \
+  if (D == d && BC == bc && nseg == ns)        \
+    return launch_attn_t<d, bc, ns, MODE>(tq, tk, tv, args, tiles, sms, stream);
+  QF_CASE(32, 64, 1) QF_CASE(32, 128, 1) QF_CASE(32, 256, 1)
+  QF_CASE(64, 64, 1) QF_CASE(64, 128, 1) QF_CASE(64, 256, 1)
+  QF_CASE(128, 64, 1) QF_CASE(128, 128, 1) QF_CASE(128, 256, 1)
+  QF_CASE(32, 64, 2) QF_CASE(32, 128, 2) QF_CASE(32, 256, 2)
+  QF_CASE(64, 64, 2) QF_CASE(64, 128, 2) QF_CASE(64, 256, 2)
+  QF_CASE(128, 64, 2) QF_CASE(128, 128, 2)
+  QF_CASE(32, 64, 4) QF_CASE(32, 128, 4)
+  QF_CASE(64, 64, 4) QF_CASE(64, 128, 4)
 #undef QF_CASE
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_attention(int D, int BC, bool packed, const CUtensorMap& tq,
-                             const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& args,
-                             int64_t tiles, int sms, int mode, cudaStream_t stream) {
-  if (mode == 1) return launch_attention_mode<1>(D, BC, packed, tq, tk, tv, args, tiles, sms, stream);
-  if (mode == 2) return launch_attention_mode<2>(D, BC, packed, tq, tk, tv, args, tiles, sms, stream);
-  return launch_attention_mode<0>(D, BC, packed, tq, tk, tv, args, tiles, sms, stream);
+cudaError_t launch_attention(int D, int BC, int nseg, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
+                             int mode, cudaStream_t stream) {
+  if (mode == 1) return launch_attention_mode<1>(D, BC, nseg, tq, tk, tv, args, tiles, sms, stream);
+  return launch_attention_mode<0>(D, BC, nseg, tq, tk, tv, args, tiles, sms, stream);
 }
 
 }  // namespace qf

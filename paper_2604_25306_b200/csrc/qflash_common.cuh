@@ -28,20 +28,21 @@ static_assert(sizeof(IntParams) == 72, "IntParams layout");
 struct AttnArgs {
   int32_t N;        // sequence length
   int32_t P;        // number of problems
-  int32_t Tc;       // ceil(N / B_c) KV tiles (generic kernel)
-  int32_t Tr;       // ceil(N / 128) query tiles per problem (generic kernel)
+  int32_t Tc;       // ceil(N / B_c) KV tiles
+  int32_t Tr;       // ceil(N / 128) query tiles per problem (generic tiling)
   uint32_t tr_magic;  // ceil(2^32 / Tr): t / Tr == umulhi(t, tr_magic) for t < 2^32 / Tr
-  int32_t g_div;    // gridDim.x / Tr
-  int32_t g_mod;    // gridDim.x % Tr
+  int32_t g_div;    // grid stride in whole problems (generic: G / Tr; packed: 128 G / N)
+  int32_t g_mod;    // ... and the leftover rows (generic: 128 (G % Tr); packed: 128 G % N)
   int32_t pad0;
+  uint64_t n_magic;  // ceil(2^64 / N) (row-packed tiling)
   IntParams prm;    // used when dev_prm == nullptr
   const IntParams* dev_prm;  // device-derived constants (dscale path) or nullptr
   int8_t* out;
-  // bring-up dumps for CTA (problem 0, tile 0) only; nullptr in production:
+  // bring-up dumps for CTA 0's first tile only; nullptr in production:
   int32_t* dbg_s;  // [128][BC] raw S of KV tile 0
   int32_t* dbg_p;  // [128][BC/4] packed P words of KV tile 0
   int32_t* dbg_o;  // [128][D+1] final O and l before normalization
-  long long* dbg_t;  // [128] clock64 timeline of CTA (0, 0) (see QF_TS slots)
+  long long* dbg_t;  // [128] clock64 timeline of CTA 0 (see QF_TS slots)
 };
 
 // Up to three tensors quantized by one launch pair (Q/K/V fusion).

@@ -18,9 +18,10 @@
 #include "qflash_params.cuh"
 
 namespace qf {
-cudaError_t launch_attention(int D, int BC, bool packed, const CUtensorMap& tq,
-                             const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& args,
-                             int64_t tiles, int sms, int mode, cudaStream_t stream);
+cudaError_t launch_attention(int D, int BC, int nseg, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
+                             int mode, cudaStream_t stream);
+bool attention_config_supported(int D, int BC, int nseg);
 cudaError_t launch_quantize(const QuantTensors& t, int ntensors, int dtype, int64_t numel,
                             IntParams* prm_out, int32_t head_dim, cudaStream_t stream,
                             float* partial);
@@ -100,7 +101,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-// 3-D int8 tensor map over [P][N][d] with box {d, rows, probs}.
+// 3-D int8 tensor map over [P][N][d] with box {d, rows, probs}.  Rows outside
+// [0, N) of a box are zero-filled by the TMA unit (ragged tiles, row-packed Q).
 qflash_status make_tmap(CUtensorMap* m, const int8_t* base, int P, int N, int d, int rows,
                         int probs) {
   auto enc = get_encode_fn();
@@ -160,39 +162,26 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
                             int32_t* dbg_s = nullptr, int32_t* dbg_p = nullptr,
                             int32_t* dbg_o = nullptr, long long* dbg_t = nullptr) {
   const int P = shape->num_problems, N = shape->seq_len, d = shape->head_dim;
-  bool packed;
-  switch (variant) {
-    case QFLASH_VARIANT_AUTO: packed = (N <= 64); break;
-    case QFLASH_VARIANT_GENERIC: packed = false; break;
-    case QFLASH_VARIANT_PACKED:
-      if (N > 64) return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "packed variant needs seq_len <= 64");
-      packed = true;
-      break;
-    default: return fail(QFLASH_ERR_INVALID_ARGUMENT, "unknown variant %d", static_cast<int>(variant));
+  // KV block: with T_c = 1 every B_c >= N gives the same result (one block), so
+  // take the smallest supported one; otherwise B_c = block_kv as requested.
+  const int bc_eff = N <= bc ? (N <= 64 ? 64 : N <= 128 ? 128 : 256) : bc;
+  // Row-packed tiling: 128 consecutive flattened rows span at most
+  // floor((N + 126) / N) + 1 problems; supported up to 4 segments.
+  const int seg_need = N >= 2 ? (N + 126) / N + 1 : 129;
+  const int nseg_tpl = seg_need <= 2 ? 2 : 4;
+  const bool packable = seg_need <= 4 && qf::attention_config_supported(d, bc_eff, nseg_tpl);
+  const int64_t Tr = (N + 127) / 128;
+  const int64_t tiles_generic = static_cast<int64_t>(P) * Tr;
+  const int64_t tiles_packed = (static_cast<int64_t>(P) * N + 127) / 128;
+  // Kernel configuration (qflash_attention.cu "MODE"): small tiles (B_c = 64,
+  // d = 32: the Swin windows) run two CTAs per SM with two softmax warpgroups;
+  // everything else one CTA per SM with four.  QFLASH_ATTN_MODE=0/1 overrides.
+  static int mode_env = -2;
+  if (mode_env == -2) {
+    const char* env = getenv("QFLASH_ATTN_MODE");
+    mode_env = (env != nullptr && (env[0] == '0' || env[0] == '1')) ? env[0] - '0' : -1;
   }
-  CUtensorMap tq, tk, tv;
-  const int rows = packed ? 64 : 128;
-  const int probs = packed ? 2 : 1;
-  const int kv_rows = packed ? 64 : bc;
-  qflash_status st;
-  if ((st = make_tmap(&tq, q, P, N, d, rows, probs)) != QFLASH_OK) return st;
-  if ((st = make_tmap(&tk, k, P, N, d, kv_rows, probs)) != QFLASH_OK) return st;
-  if ((st = make_tmap(&tv, v, P, N, d, kv_rows, probs)) != QFLASH_OK) return st;
-  qf::AttnArgs args;
-  memset(&args, 0, sizeof(args));
-  args.N = N;
-  args.P = P;
-  args.Tc = (N + bc - 1) / bc;
-  if (host_prm) args.prm = *host_prm;
-  args.dev_prm = dev_prm;
-  args.out = o;
-  args.dbg_s = dbg_s;
-  args.dbg_p = dbg_p;
-  args.dbg_o = dbg_o;
-  args.dbg_t = dbg_t;
-  // Persistent grid: one CTA per SM, each walking tiles b, b + G, b + 2G, ...
-  const int64_t Tr = packed ? 1 : (N + 127) / 128;
-  const int64_t tiles = packed ? (P + 1) / 2 : static_cast<int64_t>(P) * Tr;
+  const int mode = mode_env >= 0 ? mode_env : ((bc_eff == 64 && d == 32) ? 1 : 0);
   int sms = 0;
   {
     int dev = 0;
@@ -206,18 +195,48 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
       if (dev >= 0 && dev < 64) sm_cache[dev] = sms;
     }
   }
-  args.Tr = static_cast<int32_t>(Tr);
-  // Kernel configuration (qflash_attention.cu "MODE"): packed windows run two
-  // CTAs per SM with two softmax warpgroups (fastest there); the generic kernel
-  // one CTA per SM with four.  QFLASH_ATTN_MODE=0/1/2 overrides (experiments).
-  static int mode_env = -2;
-  if (mode_env == -2) {
-    const char* env = getenv("QFLASH_ATTN_MODE");
-    mode_env = (env != nullptr && env[0] >= '0' && env[0] <= '2') ? env[0] - '0' : -1;
+  // AUTO packs rows only when that saves a wave of the persistent grid: a
+  // row-packed tile costs a little more (one TMA load and MMA per segment).
+  const int64_t slots = static_cast<int64_t>(sms) * ((mode == 1 && bc_eff + d + 16 <= 256) ? 2 : 1);
+  const int64_t waves_generic = (tiles_generic + slots - 1) / slots;
+  const int64_t waves_packed = (tiles_packed + slots - 1) / slots;
+  bool packed;
+  switch (variant) {
+    case QFLASH_VARIANT_AUTO: packed = packable && waves_packed < waves_generic; break;
+    case QFLASH_VARIANT_GENERIC: packed = false; break;
+    case QFLASH_VARIANT_PACKED:
+      if (!packable)
+        return fail(QFLASH_ERR_UNSUPPORTED_SHAPE,
+                    "row-packed variant needs seq_len >= 43 (<= 4 problems per 128-row tile) "
+                    "and a supported (head_dim, block) pair");
+      packed = true;
+      break;
+    default: return fail(QFLASH_ERR_INVALID_ARGUMENT, "unknown variant %d", static_cast<int>(variant));
   }
-  const int mode = mode_env >= 0 ? mode_env : (packed ? 1 : 0);
-  cudaError_t e = qf::launch_attention(d, packed ? 128 : bc, packed, tq, tk, tv, args, tiles, sms,
-                                       mode, stream);
+  const int nseg = packed ? nseg_tpl : 1;
+  if (static_cast<int64_t>(P) * N >= (1ll << 31) - 256)
+    return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "num_problems * seq_len must be < 2^31");
+  CUtensorMap tq, tk, tv;
+  qflash_status st;
+  if ((st = make_tmap(&tq, q, P, N, d, 128, 1)) != QFLASH_OK) return st;
+  if ((st = make_tmap(&tk, k, P, N, d, bc_eff, 1)) != QFLASH_OK) return st;
+  if ((st = make_tmap(&tv, v, P, N, d, bc_eff, 1)) != QFLASH_OK) return st;
+  qf::AttnArgs args;
+  memset(&args, 0, sizeof(args));
+  args.N = N;
+  args.P = P;
+  args.Tc = (N + bc_eff - 1) / bc_eff;
+  if (host_prm) args.prm = *host_prm;
+  args.dev_prm = dev_prm;
+  args.out = o;
+  args.dbg_s = dbg_s;
+  args.dbg_p = dbg_p;
+  args.dbg_o = dbg_o;
+  args.dbg_t = dbg_t;
+  // Persistent grid: kMinBlocks CTAs per SM, each walking tiles b, b + G, b + 2G, ...
+  const int64_t tiles = packed ? tiles_packed : tiles_generic;
+  args.Tr = static_cast<int32_t>(Tr);
+  cudaError_t e = qf::launch_attention(d, bc_eff, nseg, tq, tk, tv, args, tiles, sms, mode, stream);
   if (e != cudaSuccess) return cuda_fail(e, "attention launch");
   return QFLASH_OK;
 }

@@ -39,6 +39,21 @@ def _gpu_attention(q, k, v, sq, sk, sv=0.03, block_kv=128, variant="auto"):
 N_GRID = [1, 2, 31, 32, 33, 48, 49, 50, 63, 64, 65, 127, 128, 129, 196, 197, 255, 256, 257]
 
 
+def _packable(N, d, bkv):
+    """Mirror of qflash_host.cu: the row-packed tiling needs <= 4 problems per
+    128-row tile and an instantiated (d, B_c, NSEG) kernel."""
+    if N < 2:
+        return False
+    bc = (64 if N <= 64 else 128 if N <= 128 else 256) if N <= bkv else bkv
+    seg = (N + 126) // N + 1
+    if seg > 4:
+        return False
+    nseg = 2 if seg <= 2 else 4
+    if nseg == 2:
+        return not (d == 128 and bc == 256)
+    return d != 128 and bc != 256
+
+
 @pytest.mark.parametrize("N", N_GRID)
 @pytest.mark.parametrize("d", [32, 64, 128])
 def test_edge_seq_lengths(orc, N, d):
@@ -47,9 +62,29 @@ def test_edge_seq_lengths(orc, N, d):
         ref = orc.attention(q, k, v, 0.05, 0.05, block_kv=bkv)
         got = _gpu_attention(q, k, v, 0.05, 0.05, block_kv=bkv, variant="generic")
         assert np.array_equal(got, ref), (N, d, bkv, int((got != ref).sum()))
-        if N <= 64:
+        if _packable(N, d, bkv):
             got_p = _gpu_attention(q, k, v, 0.05, 0.05, block_kv=bkv, variant="packed")
-            assert np.array_equal(got_p, ref)
+            assert np.array_equal(got_p, ref), (N, d, bkv, int((got_p != ref).sum()))
+        else:
+            with pytest.raises(_lib.QFlashError) as e:
+                _gpu_attention(q, k, v, 0.05, 0.05, block_kv=bkv, variant="packed")
+            assert e.value.status == _lib.QFLASH_ERR_UNSUPPORTED_SHAPE
+
+
+@pytest.mark.parametrize("N,d,P", [(43, 32, 61), (49, 32, 97), (49, 64, 40), (64, 32, 33),
+                                   (100, 64, 29), (127, 32, 7), (197, 64, 151), (300, 64, 9),
+                                   (1025, 64, 3)])
+def test_row_packed_alignments(orc, N, d, P):
+    # many problems: tiles start at every residue of 128 t mod N, span 1..4
+    # segments, and (P N / 128 > 148 for some shapes) CTAs walk several tiles
+    q, k, v = gen_int8_qkv(P, N, d, seed=N * 7 + P)
+    for bkv in (64, 128):
+        if not _packable(N, d, bkv):
+            continue
+        ref = orc.attention(q, k, v, 0.05, 0.05, block_kv=bkv)
+        got = _gpu_attention(q, k, v, 0.05, 0.05, block_kv=bkv, variant="packed")
+        bad = np.argwhere((got != ref).any(axis=2))
+        assert bad.size == 0, (N, d, P, bkv, bad[:8].tolist())
 
 
 @pytest.mark.parametrize("kind", ["uniform", "all_min", "constant_rows", "one_hot", "ties", "zeros"])
@@ -300,5 +335,6 @@ def test_validation_errors():
     with pytest.raises(_lib.QFlashError) as e:
         qf.qflash_attention_int8(q48, q48, q48, 0.05, 0.05, 0.05)
     assert e.value.status == _lib.QFLASH_ERR_UNSUPPORTED_SHAPE
+    q1 = torch.zeros((4, 20, 64), dtype=torch.int8, device="cuda")
     with pytest.raises(_lib.QFlashError):
-        qf.qflash_attention_int8(q, q, q, 0.05, 0.05, 0.05, variant="packed")   # N > 64
+        qf.qflash_attention_int8(q1, q1, q1, 0.05, 0.05, 0.05, variant="packed")  # N < 43

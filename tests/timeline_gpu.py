@@ -24,8 +24,8 @@ for j in range(7):
     NAMES[110 + j] = f"softmax: wait_st{j} done"
     NAMES[43 + 8 * j] = f"softmax: P{j} arrived"
 
-for (P, N, d, variant, label) in [(96, 197, 64, 1, "A3 b8"), (1536, 49, 32, 2, "A4 b8 packed"),
-                                  (1024, 1025, 64, 1, "L14 b64")]:
+for (P, N, d, variant, label) in [(96, 197, 64, 0, "A3 b8"), (1536, 49, 32, 0, "A4 b8"),
+                                  (1024, 1025, 64, 0, "L14 b64")]:
     q, k, v = gen_int8_qkv(P, N, d, seed=1)
     dq, dk, dv = (torch.from_numpy(t).cuda() for t in (q, k, v))
     o = torch.empty_like(dq)
