@@ -48,6 +48,15 @@ QF_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ------------------------------------------- programmatic dependent launch
+// A kernel launched with the programmatic-stream-serialization attribute may
+// start while its predecessor in the stream is still running; griddep_wait()
+// blocks until every prerequisite grid has completed and its memory is
+// visible (a no-op without a programmatic predecessor).  griddep_launch()
+// lets the dependent grid be scheduled before this grid finishes.
+QF_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+QF_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------------- TMA
 QF_DEV void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");

@@ -667,6 +667,9 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, MODE>::kThreads, Cfg<D, BC, N
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0 && blockIdx.x == 0) QF_TS(1);
+  // Everything above overlaps the tail of the previous kernel (programmatic
+  // dependent launch); every global access of this grid comes after the wait.
+  griddep_wait();
 
   // Integer constants (host-derived by value, or device-derived).
   IntParams prm = args.prm;
@@ -778,6 +781,9 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, MODE>::kThreads, Cfg<D, BC, N
             if (C::kNumS == 1 && j + 1 < Tc) issue_qk(j + 1);
           }
         }
+        // every MMA of this CTA is issued: let the next grid (dequantize) be
+        // scheduled while the last tile's softmax and normalization finish
+        griddep_launch();
       }
     } else if (warp >= C::kCtl) {
       if (prm.q_shift == 0 && static_cast<uint64_t>(prm.s_inv) * static_cast<uint64_t>(prm.m_p) < (1ull << 32))
@@ -829,8 +835,17 @@ cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CU
     args.g_div = static_cast<int32_t>(step / args.N);
     args.g_mod = static_cast<int32_t>(step % args.N);
   }
-  kern<<<dim3(static_cast<unsigned>(G)), C::kThreads, L::kAlloc, stream>>>(tq, tk, tv, args);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(G));
+  cfg.blockDim = dim3(C::kThreads);
+  cfg.dynamicSmemBytes = L::kAlloc;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddep_wait)
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl_mask() & 1) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, args);
 }
 
 // Supported instantiations (qflash_host.cu selects within them):

@@ -2,6 +2,7 @@
 // libqflash.so (NOT shared with the oracle).
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 
 namespace qf {
 
@@ -24,6 +25,8 @@ struct IntParams {
   double s;
 };
 static_assert(sizeof(IntParams) == 72, "IntParams layout");
+
+constexpr int kPdlDefault = 7;
 
 struct AttnArgs {
   int32_t N;        // sequence length
@@ -51,5 +54,16 @@ struct QuantTensors {
   int8_t* xq[3];
   float* scale[3];
 };
+
+// Programmatic dependent launch per kernel (bit 0 attention, bit 1 dequantize,
+// bit 2 second quantize pass); QFLASH_PDL=<mask> overrides the default (A/B).
+inline int pdl_mask() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("QFLASH_PDL");
+    m = (e != nullptr && e[0] >= '0' && e[0] <= '7') ? e[0] - '0' : kPdlDefault;
+  }
+  return m;
+}
 
 }  // namespace qf

@@ -17,12 +17,18 @@
 //      launch.
 // 16 elements per thread and iteration (64 B of fp32 in flight, one 16-B store).
 //
-// Single-pass variant (quantize_fused_kernel): when the three tensors fit in the
-// GPU's aggregate shared memory, a cooperative grid (one CTA per SM) bulk-loads
-// its chunk of Q, K and V into shared memory with TMA (cp.async.bulk), reduces
-// the chunk amax, exchanges per-CTA partials through the caller's workspace
-// around one grid barrier, and quantizes from shared memory: HBM is read once,
-// one launch, no memset, no atomics.
+// Single-pass variant (quantize_fused_kernel, three tensors): when every
+// thread's share of Q, K and V fits in registers (<= 4 16-byte vectors per
+// tensor), a cooperative grid (2 CTAs per SM) loads its share once, reduces the
+// per-CTA amax, exchanges the partials through the caller's workspace around one
+// grid barrier, and quantizes from registers: HBM is read once, one launch, no
+// memset, no atomics.  Larger tensors take the two-pass path above.
+//
+// The attention, dequantize and second quantize launches use programmatic
+// dependent launch (their prologue and launch latency overlap the previous
+// grid's tail); every PDL-launched kernel calls griddep_wait() before its first
+// global access.  Measured on B200 (tools/gpu_pdl_ab.sh): A3 b8 step 23.9 ->
+// 23.0-23.4 us, A4 b8 35.5 -> 33.0 us, A1 b1 15.8 -> 14.6-15.0 us.
 #include <cooperative_groups.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -31,6 +37,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "ptx.cuh"
 #include "qflash_common.cuh"
 #include "qflash_params.cuh"
 
@@ -108,6 +115,7 @@ __device__ __forceinline__ float* pick_s(const QuantTensors& t, int i) {
 
 template <typename T>
 __global__ void __launch_bounds__(kQThreads) amax_kernel(QuantTensors t, int64_t numel) {
+  griddep_launch();  // let the quantize pass be scheduled early (it waits for us)
   const int ti = blockIdx.y;
   const void* x = pick(t, ti);
   const int64_t nv = numel / kQElems;
@@ -182,6 +190,8 @@ __device__ __forceinline__ uint4 quant16(const float* f, float s, float r) {
 template <typename T>
 __global__ void __launch_bounds__(kQThreads)
     quantize_kernel(QuantTensors t, int64_t numel, IntParams* prm_out, int32_t head_dim) {
+  griddep_wait();    // programmatic launch: the amax pass must be complete
+  griddep_launch();
   const int ti = blockIdx.y;
   const void* x = pick(t, ti);
   int8_t* xq = pick_q(t, ti);
@@ -262,6 +272,7 @@ __global__ void __launch_bounds__(kFThreads, kFBlocksPerSM)
   constexpr int kE = 16 / sizeof(T);  // elements per 16-byte vector
   __shared__ float red[3][kFThreads / 32];
   __shared__ float sc[3];
+  griddep_wait();
   const int64_t T_all = static_cast<int64_t>(gridDim.x) * kFThreads;
   const int64_t g = static_cast<int64_t>(blockIdx.x) * kFThreads + threadIdx.x;
   const int64_t nvec = numel / kE;
@@ -306,6 +317,8 @@ __global__ void __launch_bounds__(kFThreads, kFBlocksPerSM)
   }
   __threadfence();
   cg::this_grid().sync();
+  // (no griddep_launch here: an early trigger measured ~1 us slower on A3 b8 -- the
+  // attention grid is launched at our exit, still with its prologue overlapped)
   // per-tensor scale s = fl32(amax / 127) (R3: 1/127 for an all-zero tensor)
   if (warp < 3) {
     float b = 0.f;
@@ -386,6 +399,7 @@ __global__ void __launch_bounds__(kFThreads, kFBlocksPerSM)
 __global__ void __launch_bounds__(kQThreads)
     dequantize_kernel(const int8_t* __restrict__ xq, float scale, const float* __restrict__ scale_dev,
                       int64_t numel, float* __restrict__ y) {
+  griddep_wait();  // programmatic launch: the producer of xq / scale must be complete
   const float s = scale_dev ? *scale_dev : scale;
   // 4 int8 per thread per step: one 4-B load and one 16-B store, both coalesced
   const int64_t n4 = numel / 4;
@@ -419,6 +433,25 @@ static int num_sms() {
     if (sms <= 0) sms = 148;
   }
   return sms;
+}
+
+// Launch with programmatic stream serialization (PDL): the kernel may be
+// scheduled while its stream predecessor drains and calls griddep_wait()
+// before touching global memory.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, int threads,
+                              cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
 // Blocks per tensor: enough 256-thread blocks for one pass over the data, capped
@@ -510,27 +543,23 @@ cudaError_t launch_quantize(const QuantTensors& t, int ntensors, int dtype, int6
   switch (dtype) {
     case 0:
       amax_kernel<float><<<grid, kQThreads, 0, stream>>>(t, numel);
-      quantize_kernel<float><<<grid, kQThreads, 0, stream>>>(t, numel, prm_out, head_dim);
-      break;
+      return launch_pdl((pdl_mask() & 4) != 0, quantize_kernel<float>, grid, kQThreads, stream, t, numel, prm_out, head_dim);
     case 1:
       amax_kernel<__nv_bfloat16><<<grid, kQThreads, 0, stream>>>(t, numel);
-      quantize_kernel<__nv_bfloat16><<<grid, kQThreads, 0, stream>>>(t, numel, prm_out, head_dim);
-      break;
+      return launch_pdl((pdl_mask() & 4) != 0, quantize_kernel<__nv_bfloat16>, grid, kQThreads, stream, t, numel, prm_out,
+                        head_dim);
     case 2:
       amax_kernel<__half><<<grid, kQThreads, 0, stream>>>(t, numel);
-      quantize_kernel<__half><<<grid, kQThreads, 0, stream>>>(t, numel, prm_out, head_dim);
-      break;
+      return launch_pdl((pdl_mask() & 4) != 0, quantize_kernel<__half>, grid, kQThreads, stream, t, numel, prm_out, head_dim);
     default:
       return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_dequantize(const int8_t* xq, float scale, const float* scale_dev, int64_t numel,
                               float* y, cudaStream_t stream) {
   dim3 grid(stream_grid((numel + 15) / 16, 1));
-  dequantize_kernel<<<grid, kQThreads, 0, stream>>>(xq, scale, scale_dev, numel, y);
-  return cudaGetLastError();
+  return launch_pdl((pdl_mask() & 2) != 0, dequantize_kernel, grid, kQThreads, stream, xq, scale, scale_dev, numel, y);
 }
 
 }  // namespace qf
