@@ -1,8 +1,8 @@
 # One GPU session: parity tests, smoke, bench, ncu launch list + full capture.
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
-timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -30 | tee gpurun_out/pytest_gpu.log
-timeout 120 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -30 | tee gpurun_out/pytest_gpu.log
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3 | tee gpurun_out/smoke.log
 timeout 300 python bench.py 2>&1 | tail -3 | tee gpurun_out/bench_default.log
 timeout 300 python bench.py --workload L14 --batch 64 --steps 20 --warmup 3 --no-cpu-baseline 2>&1 | tail -2 | tee gpurun_out/bench_l14.log
 timeout 300 python bench.py --workload A4 --batch 8 --steps 2000 --no-cpu-baseline 2>&1 | tail -2 | tee gpurun_out/bench_a4.log
