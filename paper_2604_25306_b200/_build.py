@@ -9,8 +9,10 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_objs")
 LIB = os.path.join(PKG, "libqflash.so")
-SOURCES = ["qflash_attention.cu", "qflash_quant.cu", "qflash_host.cu"]
-HEADERS = ["ptx.cuh", "qflash_common.cuh", "qflash_params.cuh"]
+SOURCES = ["qflash_attn_d32.cu", "qflash_attn_d64.cu", "qflash_attn_d128.cu", "qflash_attn_dbg.cu",
+           "qflash_quant.cu", "qflash_host.cu"]
+HEADERS = ["ptx.cuh", "qflash_common.cuh", "qflash_params.cuh", "qflash_attn_kernel.cuh",
+           "qflash_attn_inst.cuh"]
 PUBLIC_HEADERS = ["qflash.h", "qflash_debug.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

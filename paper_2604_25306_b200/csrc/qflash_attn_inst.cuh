@@ -1,0 +1,50 @@
+// qflash_attn_inst.cuh -- instantiation helper: one translation unit per head
+// dimension (qflash_attn_d32.cu, ...) defines launch_attention_d<D>() over every
+// supported (B_c, NSEG, CS, QT) so the heavy kernel instantiations compile in
+// parallel.  Configurations that do not fit TMEM / shared memory report
+// cudaErrorNotSupported without instantiating anything.
+#pragma once
+#include "qflash_attn_kernel.cuh"
+
+namespace qf {
+
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG>
+cudaError_t try_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                       const AttnArgs& args, int64_t tiles, int sms, cudaStream_t stream) {
+  if constexpr (config_fits<D, BC, NSEG, CS, QT>()) {
+    return launch_attn_t<D, BC, NSEG, CS, QT, DBG>(tq, tk, tv, args, tiles, sms, stream);
+  } else {
+    return cudaErrorNotSupported;
+  }
+}
+
+// cfg 0: CS = 4 column splits x QT = 1 (one query tile in flight, 16 softmax warps)
+// cfg 1: CS = 2 x QT = 2 (two ping-ponging query tiles, 8 softmax warps each)
+template <int D, bool DBG>
+cudaError_t launch_attention_d(int BC, int nseg, int cfg, const CUtensorMap& tq,
+                               const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& args,
+                               int64_t tiles, int sms, cudaStream_t stream) {
+#define QF_BC_SEG(bc, ns)                                                                      \
+  if (BC == bc && nseg == ns)                                                                  \
+    return cfg == 1 ? try_launch<D, bc, ns, 2, 2, DBG>(tq, tk, tv, args, tiles, sms, stream)   \
+                    : try_launch<D, bc, ns, 4, 1, DBG>(tq, tk, tv, args, tiles, sms, stream);
+  QF_BC_SEG(64, 1) QF_BC_SEG(128, 1) QF_BC_SEG(256, 1)
+  QF_BC_SEG(64, 2) QF_BC_SEG(128, 2) QF_BC_SEG(256, 2)
+  QF_BC_SEG(64, 4) QF_BC_SEG(128, 4)
+#undef QF_BC_SEG
+  return cudaErrorNotSupported;
+}
+
+template <int D>
+constexpr bool supported_d(int BC, int nseg, int cfg) {
+#define QF_FITS(bc, ns)                                                                 \
+  if (BC == bc && nseg == ns)                                                           \
+    return cfg == 1 ? config_fits<D, bc, ns, 2, 2>() : config_fits<D, bc, ns, 4, 1>();
+  QF_FITS(64, 1) QF_FITS(128, 1) QF_FITS(256, 1)
+  QF_FITS(64, 2) QF_FITS(128, 2) QF_FITS(256, 2)
+  QF_FITS(64, 4) QF_FITS(128, 4)
+#undef QF_FITS
+  return false;
+}
+
+}  // namespace qf

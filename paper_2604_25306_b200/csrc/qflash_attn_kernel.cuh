@@ -1,0 +1,927 @@
+// qflash_attn_kernel.cuh -- the fused integer-only attention kernel (Algorithm 1
+// of arxiv 2604.25306) for B200 / sm_100a, as a template included by
+// the instantiation units (qflash_attention.cu, qflash_attention_dbg.cu).
+//
+// A CTA (one per SM, persistent) runs QT independent "groups"; each group walks
+// its own sequence of 128-row query tiles (B_r = 128 = the tcgen05 M; TMEM lane
+// r = tile row r) with its own TMA producer warp, MMA issuer warp, shared-memory
+// ring, TMEM region and mbarriers.  Two groups (QT = 2) ping-pong: while one
+// group's softmax warps wait for its P V / Q K^T round trip on the tensor core,
+// the other group's warps compute, so the integer ALUs stay busy.
+//
+// Warps 0..3 are control warps: warp g (< QT) is group g's TMA producer, warp
+// 2 + g (< 2 + QT) its MMA issuer; warp 2 also allocates TMEM and warp 3 loads
+// the reciprocal table of step (11) before taking their roles.  Then QT x CS
+// softmax warpgroups: group g's CS warpgroups split every KV tile's B_c key
+// columns (B_c / CS per thread) and the d output columns; thread = (query row,
+// column slice).  Per KV tile j a softmax thread
+//   (2)(3) loads its S columns from TMEM (tcgen05.ld 32x32b), takes their row max
+//          (VIMNMX3) and combines it with the group's other warpgroups through
+//          shared memory (one named barrier per group);
+//   (4)    alpha = ShiftExp2(m_old - m_new);
+//   (5)(6) P = Requant(ShiftExp2(S - m_new)), packed 4 x int8 per TMEM column
+//          (cvt.pack.sat) and stored over the consumed S columns;
+//   (7)(8) ScaleRelease of its O columns and l once P V_{j-1} has landed;
+//   then arrives on the group's p_full barrier, which releases the MMA warp to
+//   issue O += P [V_j | 1] (the ones block makes TMEM column d the row sum l).
+// After the last KV tile: (11) O = floor(O / l), saturated, 16-byte row stores.
+//
+// Tiling (NSEG):
+//   NSEG = 1  "generic": tile = (problem, 128-row query block).
+//   NSEG > 1  "row-packed": query rows of all problems are flattened and cut into
+//             128-row tiles spanning up to NSEG problems (segments).  Segment s
+//             gets its own Q tile, loaded by TMA with row coordinates shifted by
+//             -s N so rows of other problems fall out of range and are zero-filled;
+//             S = sum_s Q_s K_{s,j}^T then holds every row's scores against its
+//             own problem's keys.  P is stored once per segment (own segment: the
+//             row's P, others: zeros) and O = sum_s P_s [V_{s,j} | 1].
+//
+// The production instantiations (DBG = false) execute no floating-point
+// instruction (tests/test_abi_cpu.py audits the SASS).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ptx.cuh"
+#include "qflash_common.cuh"
+
+namespace qf {
+
+// ----------------------------------------------------------------------------
+// Reciprocal table for step (11): kRecip[i] = floor(2^62 / (2^31 + (2i+1) 2^20)),
+// the reciprocal of the midpoint of the i-th of 1024 buckets of a normalised
+// l in [2^31, 2^32).  Built at compile time (no runtime division anywhere).
+struct RecipTable {
+  uint32_t v[1024];
+};
+constexpr RecipTable make_recip_table() {
+  RecipTable t{};
+  for (int i = 0; i < 1024; ++i) {
+    const unsigned long long den = (1ull << 31) + ((2ull * i + 1ull) << 20);
+    t.v[i] = static_cast<uint32_t>((1ull << 62) / den);
+  }
+  return t;
+}
+static __device__ const RecipTable g_recip = make_recip_table();
+
+constexpr int kStages = 2;
+constexpr int kBlockR = 128;
+
+__host__ __device__ constexpr uint32_t tmem_cols_pow2(int cols) {
+  return cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+}
+template <int D>
+__host__ __device__ constexpr uint32_t swizzle_layout() {
+  return D == 32 ? 6u : D == 64 ? 4u : 2u;  // UMMA layout: SW32 / SW64 / SW128
+}
+
+// ---------------------------------------------------------------- configuration
+template <int D, int BC, int NSEG, int CS, int QT>
+struct Cfg {
+  static constexpr int kNWG = CS * QT;            // softmax warpgroups
+  static constexpr int kCtl = 4;                  // control warps
+  static constexpr int kThreads = 32 * kCtl + 128 * kNWG;
+  static constexpr int kGroupThreads = 128 * CS;  // softmax threads of one group
+  static constexpr int kCW = BC / CS;             // key columns per thread
+  static constexpr int kOW = D / CS;              // O columns per thread
+  // TMEM per group: kNumS S buffers of BC columns (P_s of KV tile j aliases S
+  // buffer j: segment s at columns [s BC/4, (s+1) BC/4)), then O (D columns),
+  // l (column D) and 15 copies of l from the ones block.
+  static constexpr int kNumS = (QT == 1 && 2 * BC + D + 16 <= 512) ? 2 : 1;
+  static constexpr int kGroupCols = kNumS * BC + D + 16;
+  static constexpr uint32_t kTmemCols = tmem_cols_pow2(QT * kGroupCols);
+  // shared memory (offsets from the 1024-aligned base)
+  static constexpr int kQBytes = kBlockR * D;
+  static constexpr int kKVBytes = BC * D;
+  static constexpr int kGroupSmem = 2 * NSEG * kQBytes + 2 * kStages * NSEG * kKVBytes;
+  static constexpr int kQ = 0;                               // [2][NSEG] (+ g kGroupSmem)
+  static constexpr int kK = 2 * NSEG * kQBytes;              // [kStages][NSEG]
+  static constexpr int kV = kK + kStages * NSEG * kKVBytes;  // [kStages][NSEG]
+  static constexpr int kOnes = QT * kGroupSmem;              // second MN atom of [V | 1]
+  static constexpr int kBarsPerGroup = 2 * kStages + 4 + kNumS + 2;
+  static constexpr int kBar = kOnes + BC * D;
+  static constexpr int kTmemSlot = kBar + QT * kBarsPerGroup * 8;
+  static constexpr int kRed = (kTmemSlot + 16 + 15) / 16 * 16;  // [QT][2][CS][128] int32
+  static constexpr int kRecip = kRed + QT * 2 * CS * 128 * 4;   // [1024] u32
+  static constexpr int kTotal = kRecip + 1024 * 4;
+  static constexpr int kAlloc = kTotal + 1024;                  // slack for 1024-B alignment
+  static_assert(QT * kGroupCols <= 512, "TMEM budget");
+  static_assert(NSEG * (BC / 4) <= BC, "P segments must fit in one S buffer");
+  static_assert(kCW == 16 || kCW == 32 || kCW == 64, "columns per thread");
+  static_assert(kOW % 8 == 0, "O columns per thread");
+};
+
+template <int D, int BC, int NSEG, int CS, int QT>
+constexpr bool config_fits() {
+  return (QT * (((QT == 1 && 2 * BC + D + 16 <= 512) ? 2 : 1) * BC + D + 16) <= 512) &&
+         (BC / CS == 16 || BC / CS == 32 || BC / CS == 64) && ((D / CS) % 8 == 0) &&
+         (NSEG * (BC / 4) <= BC) &&
+         (QT * (2 * NSEG * kBlockR * D + 2 * kStages * NSEG * BC * D) + BC * D + 64 * 8 +
+              QT * 2 * CS * 512 + 4096 + 2048 <=
+          227 * 1024);
+}
+
+// Group barriers (8 B each): kv_full[kStages], kv_empty[kStages], q_full[2],
+// q_empty[2], s_full[kNumS], p_full, o_full.
+template <int NUMS>
+struct GroupBars {
+  uint64_t* base;
+  QF_DEV uint64_t* kv_full(int s) const { return base + s; }
+  QF_DEV uint64_t* kv_empty(int s) const { return base + kStages + s; }
+  QF_DEV uint64_t* q_full(int b) const { return base + 2 * kStages + b; }
+  QF_DEV uint64_t* q_empty(int b) const { return base + 2 * kStages + 2 + b; }
+  QF_DEV uint64_t* s_full(int b) const { return base + 2 * kStages + 4 + b; }
+  QF_DEV uint64_t* p_full() const { return base + 2 * kStages + 4 + NUMS; }
+  QF_DEV uint64_t* o_full() const { return base + 2 * kStages + 5 + NUMS; }
+};
+
+
+// TMEM column (within an S buffer) of the packed P of warpgroup c, segment s:
+// CW >= 32 "own range" (inside the warpgroup's own S columns), CW = 16 contiguous.
+template <int BC, int CW>
+__host__ __device__ constexpr int p_col(int c, int s) {
+  return CW >= 32 ? c * CW + s * (CW / 4) : s * (BC / 4) + c * (CW / 4);
+}
+// ... and of the 8 columns (32 keys) consumed by K-step kk of the P V MMA.
+template <int BC, int CW>
+__host__ __device__ constexpr int p_col_k(int kk, int s) {
+  return CW >= 32 ? p_col<BC, CW>((32 * kk) / CW, s) + (((32 * kk) % CW) / 32) * 8
+                  : s * (BC / 4) + 8 * kk;
+}
+
+// ---------------------------------------------------------------- the math
+
+// ShiftExp2 + requantization of one score (steps 5-6 for one element).
+//   d1 = m + s_inv - S  (>= s_inv),  q1 = floor(d1 / s_inv) = q + 1  (exact magic)
+//   y  = (q1 s_inv + S + s_inv - m) >> q1  ==  ((r >> 1) + s_inv) >> q   (Alg. 2)
+//   P  = floor(y M_P / 2^r_P)                                            (Eq. 10)
+// Per element: 2 IADD3 + SHF (+ SHF) on the ALU pipe, IMAD.HI + IMAD (+ IMAD) on
+// the FMA pipe.  ALT = true computes u = S + (s_inv - m) with IMAD instead of
+// IADD3, so alternating the forms balances the two pipes.
+template <bool FASTQ, bool ALT>
+QF_DEV int32_t shift_exp2_requant(int32_t S, uint32_t m, uint32_t nm, uint32_t c3, uint32_t one,
+                                  const IntParams& p) {
+  const uint32_t s_inv = static_cast<uint32_t>(p.s_inv);
+  const uint32_t d1 = iadd3(m, static_cast<uint32_t>(-S), s_inv);
+  uint32_t q1 = umulhi(d1, p.q_magic);
+  if constexpr (!FASTQ) q1 >>= p.q_shift;
+  uint32_t u;
+  if constexpr (ALT) {
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(u) : "r"(static_cast<uint32_t>(S)), "r"(one), "r"(c3));
+  } else {
+    u = iadd3(static_cast<uint32_t>(S), s_inv, nm);
+  }
+  const uint32_t num = q1 * s_inv + u;
+  uint32_t y = shr_clamp(num, q1);
+  if constexpr (FASTQ) {
+    // y M_P < 2^32 (host-checked: s_inv M_P < 2^32): IMAD + SHF instead of IMAD.HI
+    return static_cast<int32_t>((y * static_cast<uint32_t>(p.m_p)) >> p.r_p);
+  } else {
+    y <<= p.p_pre;
+    return static_cast<int32_t>(umulhi(y, p.p_mul));
+  }
+}
+
+// alpha = ShiftExp2(m_old - m_new) (step 4) -- same formula, x = m_old - m_new <= 0.
+template <bool FASTQ>
+QF_DEV int32_t shift_exp2(int32_t x, const IntParams& p) {
+  const uint32_t d1 = static_cast<uint32_t>(p.s_inv - x);
+  uint32_t q1 = umulhi(d1, p.q_magic);
+  if constexpr (!FASTQ) q1 >>= p.q_shift;
+  const uint32_t num = q1 * static_cast<uint32_t>(p.s_inv) + static_cast<uint32_t>(x + p.s_inv);
+  return static_cast<int32_t>(shr_clamp(num, q1));
+}
+
+// floor(alpha 2^32 / s_inv) for 0 <= alpha <= s_inv < 2^25, exactly, via the
+// 64-bit release magic (floor(n / s_inv) = hi64(n mg) >> rel_shift, n < 2^56):
+// hi64((alpha 2^32) (mh 2^32 + ml)) = alpha mh + hi32(alpha ml).
+QF_DEV uint64_t alpha_over_sinv_2p32(uint32_t alpha, const IntParams& p) {
+  const uint64_t hi = static_cast<uint64_t>(alpha) * p.rel_magic_hi + __umulhi(alpha, p.rel_magic_lo);
+  return hi >> p.rel_shift;
+}
+
+// Fast exact ScaleRelease (Eq. 14 realised per P:L408, reading R10):
+// floor(X alpha / s_inv) for |X| <= bound.  With B = (bound >> k) + 1, 2^k <= s_inv,
+// X' = X + B s_inv lies in [1, 3 bound + s_inv); whenever X' s_inv < 2^32 (the
+// per-launch threshold `rel_lthr` on l guarantees it),
+//   floor(X alpha / s_inv) = floor(X' alpha / s_inv) - B alpha = hi(X' A_c) - B alpha,
+// A_c = floor(alpha 2^32 / s_inv) + 1: the ceiling error X' (A_c 2^-32 - alpha / s_inv)
+// < 1 / s_inv cannot cross an integer (the fraction of X' alpha / s_inv is a
+// multiple of 1 / s_inv).  alpha = s_inv (identity) uses A = 2^32 - 1:
+// hi(X' (2^32 - 1)) = X' - 1, corrected by +1.  Per element: IADD3 + IMAD.HI (with
+// the addend folded in).
+struct BiasedRelease {
+  uint32_t bias;  // B s_inv
+  uint32_t mul;   // A_c (or 2^32 - 1 for identity rows)
+  uint32_t add;   // -B alpha (+1 for identity rows)
+  QF_DEV uint32_t apply(uint32_t X) const {
+    uint32_t r;
+    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(X + bias), "r"(mul), "r"(add));
+    return r;
+  }
+};
+QF_DEV BiasedRelease make_biased_release(int32_t alpha, uint32_t bound, const IntParams& p,
+                                         int sinv_log2) {
+  const uint32_t B = (bound >> sinv_log2) + 1u;
+  const bool ident = alpha == p.s_inv;
+  BiasedRelease r;
+  r.bias = B * static_cast<uint32_t>(p.s_inv);
+  r.mul = ident ? 0xFFFFFFFFu : static_cast<uint32_t>(alpha_over_sinv_2p32(alpha, p)) + 1u;
+  r.add = (0u - B * static_cast<uint32_t>(alpha)) + (ident ? 1u : 0u);
+  return r;
+}
+
+// A = min(floor(alpha 2^31 / s_inv), 2^31 - 1): per-row constant of the general release.
+QF_DEV int32_t release_factor(int32_t alpha, const IntParams& p) {
+  uint64_t a = alpha_over_sinv_2p32(static_cast<uint32_t>(alpha), p) >> 1;
+  if (a > 0x7FFFFFFFull) a = 0x7FFFFFFFull;
+  return static_cast<int32_t>(a);
+}
+// General exact ScaleRelease of one accumulator: q0 = floor(X A / 2^31) is within
+// one of the answer; the remainder X alpha - q0 s_inv (exact mod 2^32, true value
+// in [-s_inv, 2 s_inv)) corrects it.
+QF_DEV int32_t scale_release(int32_t X, int32_t alpha, int32_t A, int32_t s_inv) {
+  int32_t q0 = mul_shr31(X, A);
+  const int32_t rem = X * alpha - q0 * s_inv;
+  q0 += (rem >= s_inv) ? 1 : 0;
+  q0 += rem >> 31;  // -1 if rem < 0
+  return q0;
+}
+
+// Step (11): floor(O / l) exactly.  R = kRecip[...] approximates 2^(62-k)/l to
+// 2^-11; q0 = floor(O R / 2^(62-k)) is within one of the answer because
+// |O / l| < 2^11; the remainder corrects it.
+struct Recip {
+  int32_t R;
+  int32_t sh;
+  int32_t l;
+};
+QF_DEV Recip make_recip(int32_t l, const uint32_t* table) {
+  const int32_t k = __clz(l);                         // l >= 2  =>  1 <= k <= 30
+  const uint32_t ln = static_cast<uint32_t>(l) << k;  // [2^31, 2^32)
+  Recip r;
+  r.R = static_cast<int32_t>(table[(ln >> 21) & 1023u]);
+  r.sh = 30 - k;
+  r.l = l;
+  return r;
+}
+QF_DEV int32_t floor_div(int32_t O, const Recip& r, bool& bad) {
+  int32_t q0 = __mulhi(O, r.R) >> r.sh;
+  const int32_t rem = O - q0 * r.l;
+  q0 += (rem >= r.l) ? 1 : 0;
+  q0 += rem >> 31;  // -1 if rem < 0
+  bad |= (rem >= 2 * r.l) | (rem < -r.l);
+  return q0;
+}
+QF_DEV int32_t floor_div_exact(int32_t O, int32_t l) {
+  int64_t d = l;
+  int64_t qq = 0, acc = 0;
+  const bool neg = O < 0;
+  const uint64_t un = neg ? static_cast<uint64_t>(-(static_cast<int64_t>(O) + 1)) : static_cast<uint64_t>(O);
+#pragma unroll 1
+  for (int b = 31; b >= 0; --b) {
+    acc = (acc << 1) | static_cast<int64_t>((un >> b) & 1u);
+    if (acc >= d) {
+      acc -= d;
+      qq |= (1ll << b);
+    }
+  }
+  return static_cast<int32_t>(neg ? ~qq : qq);  // floor(O/l) = ~floor(~O/l) for O < 0
+}
+
+QF_DEV void sts32(uint32_t addr, int32_t v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+QF_DEV int32_t lds32(uint32_t addr) {
+  int32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+// Persistent tile iterator (identical in every role of a group); no runtime
+// division: the host supplies the magics and the stride quotient/remainder.
+//   generic (NSEG = 1): tile t = problem * T_r + qt, rows [128 qt, 128 qt + 128).
+//   row-packed:         tile t = flattened rows [128 t, 128 t + 128) of [P N].
+// Group g of CTA b visits tiles b + g G, then steps by QT G.
+template <int NSEG>
+struct TileIter {
+  int problem;  // first problem of the tile
+  int off;      // row of tile row 0 inside `problem`
+  int rows;     // live tile rows [0, rows)
+  int nseg;     // problems the tile spans (1..NSEG)
+  int i;        // tiles visited by this group
+  __device__ void fill(const AttnArgs& a) {
+    if constexpr (NSEG == 1) {
+      rows = min(kBlockR, a.N - off);
+      nseg = 1;
+    } else {
+      const int64_t left = static_cast<int64_t>(a.P - problem) * a.N - off;
+      rows = left < kBlockR ? static_cast<int>(left) : kBlockR;
+      const int last = off + rows - 1;
+      nseg = 1 + (last >= a.N ? 1 : 0);
+      if constexpr (NSEG > 2) nseg += (last >= 2 * a.N ? 1 : 0) + (last >= 3 * a.N ? 1 : 0);
+    }
+  }
+  __device__ void init(const AttnArgs& a, uint32_t t) {
+    i = 0;
+    if constexpr (NSEG == 1) {
+      problem = a.Tr == 1 ? static_cast<int>(t) : static_cast<int>(__umulhi(t, a.tr_magic));
+      off = (static_cast<int>(t) - problem * a.Tr) * kBlockR;
+    } else {
+      const uint64_t row0 = static_cast<uint64_t>(t) * kBlockR;
+      problem = static_cast<int>(__umul64hi(row0, a.n_magic));  // floor(row0 / N), exact
+      off = static_cast<int>(row0 - static_cast<uint64_t>(problem) * a.N);
+    }
+    if (problem < a.P) fill(a);
+  }
+  __device__ bool valid(const AttnArgs& a) const { return problem < a.P; }
+  __device__ void next(const AttnArgs& a) {
+    ++i;
+    problem += a.g_div;
+    off += a.g_mod;
+    const int lim = NSEG == 1 ? a.Tr * kBlockR : a.N;
+    if (off >= lim) {
+      off -= lim;
+      ++problem;
+    }
+    if (problem < a.P) fill(a);
+  }
+};
+
+// Bring-up timeline: clock64() stamps of CTA 0, group 0, first tile (DBG only).
+#define QF_TS(slot)                                         \
+  do {                                                      \
+    if constexpr (DBG) {                                    \
+      if (args.dbg_t != nullptr && (slot) < 128)            \
+        args.dbg_t[(slot)] = clock64();                     \
+    }                                                       \
+  } while (0)
+
+// ---------------------------------------------------------------- softmax role
+// Masked 8-column groups: column group k of a thread is fully valid, partial
+// (the ragged edge), or absent; `valid` is warp-uniform so the branches are too.
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FASTQ>
+__device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntParams& prm,
+                                             uint32_t tmem_group, GroupBars<Cfg<D, BC, NSEG, CS, QT>::kNumS> gb,
+                                             uint32_t red_group, const uint32_t* recip, int g,
+                                             int c, int quarter, int lane) {
+  using C = Cfg<D, BC, NSEG, CS, QT>;
+  constexpr int CW = C::kCW;
+  constexpr int OW = C::kOW;
+  const int N = args.N;
+  const int Tc = args.Tc;
+  const int row = quarter * 32 + lane;  // TMEM lane == tile row
+  const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+  const uint32_t tS0 = tmem_group + lane_off;  // S buffer b at + b * BC
+  const uint32_t tO = tS0 + C::kNumS * BC;
+  const int c0 = c * CW;  // first key column of this thread
+  const bool dbg_on = DBG && blockIdx.x == 0 && g == 0;
+  const bool ts_warp = dbg_on && c == 0 && quarter == 0 && lane == 0;
+  const uint32_t s_inv = static_cast<uint32_t>(prm.s_inv);
+  const int sinv_log2 = 31 - __clz(prm.s_inv);
+  // fast-release threshold on l: (3 * 128 (l + 2 T_c) + s_inv) s_inv < 2^32, i.e.
+  // 384 (l + 2 T_c) + s_inv <= floor((2^32 - 1) / s_inv) (64-bit magic, n < 2^56)
+  int32_t rel_lthr;
+  {
+    const uint64_t mg = (static_cast<uint64_t>(prm.rel_magic_hi) << 32) | prm.rel_magic_lo;
+    const uint64_t A = __umul64hi(0xFFFFFFFFull, mg) >> prm.rel_shift;
+    const int64_t t = (static_cast<int64_t>(A) - static_cast<int64_t>(s_inv)) / 384 - 2 * Tc;
+    rel_lthr = t < 0 ? -1 : (t > 0x7FFFFFFF ? 0x7FFFFFFF : static_cast<int32_t>(t));
+  }
+  named_bar_sync(15, C::kNWG * 128 + 32);  // reciprocal table of step (11) ready
+
+  TileIter<NSEG> ti;
+  ti.init(args, blockIdx.x + g * gridDim.x);
+  int it0 = 0;  // KV iterations of this group so far
+  for (; ti.valid(args); ti.next(args)) {
+    const bool dbg = dbg_on && ti.i == 0;
+    const bool live = row < ti.rows;  // padded rows of the last tile do no work
+    const bool warp_live = quarter * 32 < ti.rows;
+    int seg = 0;  // this row's problem = ti.problem + seg
+    if constexpr (NSEG > 1) {
+      const int x = ti.off + row;
+      seg = (x >= N ? 1 : 0);
+      if constexpr (NSEG > 2) seg += (x >= 2 * N ? 1 : 0) + (x >= 3 * N ? 1 : 0);
+    }
+    const int nseg = ti.nseg;
+    int32_t m = -(1 << 21);  // m^(0) = -2^21
+
+    for (int j = 0; j < Tc; ++j) {
+      const int it = it0 + j;
+      const int sb = (C::kNumS == 2) ? (it & 1) : 0;
+      const uint32_t tS = tS0 + sb * BC;
+      mbar_wait(gb.s_full(sb), (C::kNumS == 2 ? (it >> 1) : it) & 1);
+      tc_fence_after();
+      if (dbg && ts_warp && j < 7) QF_TS(40 + 8 * j);
+      // columns of this thread that exist in KV tile j (ragged last tile, R16)
+      const int valid = min(BC, N - j * BC) - c0;
+      // S columns of this thread: CW <= 32 stay in registers for the P pass;
+      // CW = 64 is loaded whole for the max and reloaded per 32-column chunk.
+      constexpr int HW = CW < 32 ? CW : 32;  // chunk width
+      constexpr int NH = CW / HW;            // chunks
+      uint32_t s[CW];
+      int32_t tmax = INT32_MIN;
+      if (warp_live && valid > 0) {
+        if constexpr (CW == 16) {
+          tmem_ld16(tS + c0, s);
+        } else {
+#pragma unroll
+          for (int h = 0; h < NH; ++h) tmem_ld32(tS + c0 + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(s + 32 * h));
+        }
+        tmem_wait_ld();
+        if constexpr (DBG) {
+          if (args.dbg_s != nullptr && dbg && j == 0)
+            for (int e = 0; e < CW; ++e) args.dbg_s[row * BC + c0 + e] = static_cast<int32_t>(s[e]);
+        }
+        if (valid >= CW) {
+#pragma unroll
+          for (int e = 0; e < CW; ++e) tmax = max(tmax, static_cast<int32_t>(s[e]));
+        } else {
+#pragma unroll
+          for (int k = 0; k < CW / 8; ++k) {
+            if (8 * k + 8 <= valid) {
+#pragma unroll
+              for (int e = 8 * k; e < 8 * k + 8; ++e) tmax = max(tmax, static_cast<int32_t>(s[e]));
+            } else if (8 * k < valid) {
+#pragma unroll
+              for (int e = 8 * k; e < 8 * k + 8; ++e)
+                if (e < valid) tmax = max(tmax, static_cast<int32_t>(s[e]));
+            }
+          }
+        }
+      }
+      // (2)(3) combine the partial maxima of the group's CS warpgroups
+      if constexpr (CS > 1) {
+        const uint32_t rb = red_group + static_cast<uint32_t>((it & 1) * (CS * 128) * 4);
+        sts32(rb + static_cast<uint32_t>((c * 128 + row) * 4), tmax);
+        named_bar_sync(1 + g, C::kGroupThreads);
+#pragma unroll
+        for (int h = 0; h < CS; ++h)
+          if (h != c) tmax = max(tmax, lds32(rb + static_cast<uint32_t>((h * 128 + row) * 4)));
+      }
+      if (dbg && ts_warp && j < 7) QF_TS(41 + 8 * j);
+      const int32_t m_new = max(m, tmax);
+      // (4) alpha = ShiftExp2(m_old - m_new)
+      const int32_t alpha = shift_exp2<FASTQ>(m - m_new, prm);
+
+      // (5)(6) P = Requant(ShiftExp2(S - m_new)), 4 x int8 per TMEM column.
+      const uint32_t mu = static_cast<uint32_t>(m_new);
+      const uint32_t nmu = static_cast<uint32_t>(-m_new);
+      const uint32_t c3 = s_inv - mu;
+      const uint32_t one = static_cast<uint32_t>(prm.one);
+      // Computed in chunks of HW <= 32 columns (CW = 64 reloads each chunk from
+      // TMEM); all P words are stored after the last chunk's S load.  Layout of
+      // the packed P of segment s in the S buffer (kernel_p_col): CW >= 32 puts
+      // each warpgroup's P inside its own S columns ("own range", no other
+      // warpgroup reads them); CW = 16 packs the row contiguously, which is safe
+      // because every warpgroup's S loads completed before the max exchange.
+      uint32_t pk[CW / 4];
+#pragma unroll
+      for (int e = 0; e < CW / 4; ++e) pk[e] = 0u;
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        const int hv = valid - h * HW;  // valid columns of this chunk (warp-uniform)
+        if (warp_live && hv > 0) {
+          uint32_t sc[HW];
+          if constexpr (NH == 1) {
+#pragma unroll
+            for (int e = 0; e < HW; ++e) sc[e] = s[e];
+          } else {
+            tmem_ld32(tS + c0 + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(sc));
+            tmem_wait_ld();
+          }
+          uint32_t* pw = pk + h * (HW / 4);
+          if (hv >= HW) {
+#pragma unroll
+            for (int e = 0; e < HW; e += 4)
+              pw[e / 4] = pack4_sat_s8(
+                  shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e]), mu, nmu, c3, one, prm),
+                  shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 1]), mu, nmu, c3, one, prm),
+                  shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e + 2]), mu, nmu, c3, one, prm),
+                  shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 3]), mu, nmu, c3, one, prm));
+          } else {
+#pragma unroll
+            for (int k = 0; k < HW / 8; ++k) {
+              if (8 * k + 8 <= hv) {
+#pragma unroll
+                for (int e = 8 * k; e < 8 * k + 8; e += 4)
+                  pw[e / 4] = pack4_sat_s8(
+                      shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e]), mu, nmu, c3, one, prm),
+                      shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 1]), mu, nmu, c3, one, prm),
+                      shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e + 2]), mu, nmu, c3, one, prm),
+                      shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 3]), mu, nmu, c3, one, prm));
+              } else if (8 * k < hv) {
+#pragma unroll
+                for (int e = 8 * k; e < 8 * k + 8; e += 4) {
+                  int32_t pv[4];
+#pragma unroll
+                  for (int u = 0; u < 4; ++u) {
+                    const int32_t x = shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e + u]), mu, nmu, c3, one, prm);
+                    pv[u] = (e + u < hv) ? x : 0;
+                  }
+                  pw[e / 4] = pack4_sat_s8(pv[0], pv[1], pv[2], pv[3]);
+                }
+              }
+            }
+          }
+        }
+      }
+      if (nseg == 1) {
+        tmem_st<CW / 4>(tS + p_col<BC, CW>(c, 0), pk);
+      } else {
+        // segment s gets this row's P if the row belongs to it, zeros otherwise
+#pragma unroll
+        for (int sg = 0; sg < NSEG; ++sg) {
+          if (sg < nseg) {
+            uint32_t z[CW / 4];
+#pragma unroll
+            for (int e = 0; e < CW / 4; ++e) z[e] = (seg == sg && live) ? pk[e] : 0u;
+            tmem_st<CW / 4>(tS + p_col<BC, CW>(c, sg), z);
+          }
+        }
+      }
+      if (dbg && ts_warp && j < 7) QF_TS(44 + 8 * j);
+
+      // (7)(8) ScaleRelease of O (this warpgroup's columns) and l (warpgroup 0)
+      // once P V_{j-1} has landed -- after P_j so that P V_{j-1} completes behind
+      // the P computation; skipped for j = 0 (O = l = 0) and for warps whose rows
+      // all kept their maximum (alpha = s_inv is the identity, R10).  P V_j is
+      // issued only after every warp's p_full arrival below, i.e. after the release.
+      if (j > 0) {
+        mbar_wait(gb.o_full(), (it - 1) & 1);
+        tc_fence_after();
+        if (dbg && ts_warp && j < 7) QF_TS(45 + 8 * j);
+        if (warp_live && __any_sync(0xffffffffu, alpha != prm.s_inv)) {
+          uint32_t o[OW];
+          if constexpr (OW == 8) tmem_ld8(tO + c * OW, o);
+          else if constexpr (OW == 16) tmem_ld16(tO + c * OW, o);
+          else tmem_ld<OW>(tO + c * OW, o);
+          // l for this warpgroup's bound: warpgroup 0 reads (and later rewrites)
+          // column D, the released l; warpgroup c > 0 reads its own copy D + c of
+          // the ones block, never released -- an upper bound of l, so a valid
+          // bound -- because column D may already hold warpgroup 0's released l.
+          uint32_t lcol;
+          tmem_ld1(tO + D + c, lcol);
+          tmem_wait_ld();
+          if (dbg && ts_warp && j < 7) QF_TS(46 + 8 * j);
+          // Fast exact path when every row of the warp has l <= rel_lthr
+          // (bound |O| <= 128 (l + 2 T_c)).
+          if (__all_sync(0xffffffffu, static_cast<int32_t>(lcol) <= rel_lthr)) {
+            const uint32_t bound = 128u * (lcol + 2u * static_cast<uint32_t>(Tc));
+            const BiasedRelease br = make_biased_release(alpha, bound, prm, sinv_log2);
+#pragma unroll
+            for (int e = 0; e < OW; ++e) o[e] = br.apply(o[e]);
+            tmem_st<OW>(tO + c * OW, o);
+            if (c == 0) tmem_st1(tO + D, br.apply(lcol));
+          } else {
+            const int32_t A = release_factor(alpha, prm);
+#pragma unroll
+            for (int e = 0; e < OW; ++e)
+              o[e] = static_cast<uint32_t>(scale_release(static_cast<int32_t>(o[e]), alpha, A, prm.s_inv));
+            tmem_st<OW>(tO + c * OW, o);
+            if (c == 0)
+              tmem_st1(tO + D, static_cast<uint32_t>(scale_release(static_cast<int32_t>(lcol), alpha, A, prm.s_inv)));
+          }
+          if (dbg && ts_warp && j < 7) QF_TS(47 + 8 * j);
+        }
+      }
+
+      tmem_wait_st();
+      if constexpr (DBG) {
+        if (args.dbg_p != nullptr && dbg && j == 0) {
+          if constexpr (CS > 1) named_bar_sync(1 + g, C::kGroupThreads);
+          if (c == 0) {
+            for (int kk = 0; kk < BC / 32; ++kk) {
+              uint32_t pw[8];
+              tmem_ld8(tS + p_col_k<BC, CW>(kk, 0), pw);
+              tmem_wait_ld();
+              for (int e = 0; e < 8; ++e) args.dbg_p[row * (BC / 4) + 8 * kk + e] = static_cast<int32_t>(pw[e]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(gb.p_full());
+      if (dbg && ts_warp && j < 7) QF_TS(43 + 8 * j);
+      m = m_new;
+    }
+
+    // (11) O_i = floor(O / l), saturated to int8 (R14); this warpgroup's O columns.
+    const int itl = it0 + Tc - 1;
+    mbar_wait(gb.o_full(), itl & 1);
+    tc_fence_after();
+    if (dbg && ts_warp) QF_TS(100);
+    if (warp_live) {
+      uint32_t lraw;
+      uint32_t o[OW];
+      tmem_ld1(tO + D, lraw);
+      if constexpr (OW == 8) tmem_ld8(tO + c * OW, o);
+      else if constexpr (OW == 16) tmem_ld16(tO + c * OW, o);
+      else tmem_ld<OW>(tO + c * OW, o);
+      tmem_wait_ld();
+      if constexpr (DBG) {
+        if (args.dbg_o != nullptr && dbg) {
+          for (int e = 0; e < OW; ++e) args.dbg_o[row * (D + 1) + c * OW + e] = static_cast<int32_t>(o[e]);
+          if (c == 0) args.dbg_o[row * (D + 1) + D] = static_cast<int32_t>(lraw);
+        }
+      }
+      if (live) {
+        const Recip rc = make_recip(static_cast<int32_t>(lraw), recip);
+        bool bad = false;
+        uint32_t w[OW / 4];
+#pragma unroll
+        for (int e = 0; e < OW; e += 4)
+          w[e / 4] = pack4_sat_s8(floor_div(static_cast<int32_t>(o[e]), rc, bad),
+                                  floor_div(static_cast<int32_t>(o[e + 1]), rc, bad),
+                                  floor_div(static_cast<int32_t>(o[e + 2]), rc, bad),
+                                  floor_div(static_cast<int32_t>(o[e + 3]), rc, bad));
+        if (bad) {  // (theoretical) quotient outside the table's exact range: long division
+#pragma unroll
+          for (int e = 0; e < OW; e += 4)
+            w[e / 4] = pack4_sat_s8(floor_div_exact(static_cast<int32_t>(o[e]), rc.l),
+                                    floor_div_exact(static_cast<int32_t>(o[e + 1]), rc.l),
+                                    floor_div_exact(static_cast<int32_t>(o[e + 2]), rc.l),
+                                    floor_div_exact(static_cast<int32_t>(o[e + 3]), rc.l));
+        }
+        // flattened output row problem * N + off + row (row-packed tiles included)
+        int8_t* dst = args.out + (static_cast<int64_t>(ti.problem) * N + ti.off + row) * D + c * OW;
+        if constexpr (OW == 8) {
+          *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < OW / 16; ++e)
+            reinterpret_cast<uint4*>(dst)[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+        }
+      }
+    }
+    if (dbg && ts_warp) QF_TS(101);
+    // The O/l loads above completed (wait::ld) before this thread's next p_full
+    // arrival, so the next tile's first P V (which overwrites O) cannot race them.
+    it0 += Tc;
+  }
+}
+
+// ---------------------------------------------------------------- the kernel
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG>
+__global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
+    qflash_attn_kernel(const __grid_constant__ CUtensorMap tm_q,
+                       const __grid_constant__ CUtensorMap tm_k,
+                       const __grid_constant__ CUtensorMap tm_v, const AttnArgs args) {
+  using C = Cfg<D, BC, NSEG, CS, QT>;
+  constexpr uint32_t kTmemCols = C::kTmemCols;
+  constexpr uint32_t kSwz = swizzle_layout<D>();
+  constexpr int kNO = D + 16;  // extended PV width (O columns + ones block)
+  constexpr uint32_t kIdescQK = make_idesc_i8(128, BC, 0, 0);
+  constexpr uint32_t kIdescPV = make_idesc_i8(128, kNO, 0, 1);
+  using Bars = GroupBars<C::kNumS>;
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sOnes = smem + C::kOnes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBar);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kTmemSlot);
+  uint32_t* recip = reinterpret_cast<uint32_t*>(smem + C::kRecip);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0 && blockIdx.x == 0) QF_TS(0);
+  const int Tc = args.Tc;
+
+  // ------------------------------------------------------------- setup
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm_q);
+    prefetch_tmap(&tm_k);
+    prefetch_tmap(&tm_v);
+    for (int g = 0; g < QT; ++g) {
+      const Bars gb{bars + g * C::kBarsPerGroup};
+      for (int s = 0; s < kStages; ++s) {
+        mbar_init(gb.kv_full(s), 1);
+        mbar_init(gb.kv_empty(s), 1);
+      }
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(gb.q_full(b), 1);
+        mbar_init(gb.q_empty(b), 1);
+      }
+      for (int b = 0; b < C::kNumS; ++b) mbar_init(gb.s_full(b), 1);
+      mbar_init(gb.p_full(), C::kGroupThreads / 32);
+      mbar_init(gb.o_full(), 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, kTmemCols);
+    tmem_relinquish();
+  }
+  // ones block of the extended V operand (any layout: every byte is 1)
+  for (int i = threadIdx.x; i < BC * D / 16; i += C::kThreads)
+    reinterpret_cast<uint4*>(sOnes)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0 && blockIdx.x == 0) QF_TS(1);
+  // Everything above overlaps the tail of the previous kernel (programmatic
+  // dependent launch); every global access of this grid comes after the wait.
+  griddep_wait();
+
+  // Integer constants (host-derived by value, or device-derived).
+  IntParams prm = args.prm;
+  if (args.dev_prm != nullptr) prm = *args.dev_prm;
+  const bool run = (prm.status == 0);
+
+  if (run) {
+    if (warp < 2) {
+      // ========================================================= TMA producer of group `warp`
+      const int g = warp;
+      if (g < QT && lane == 0) {
+        const Bars gb{bars + g * C::kBarsPerGroup};
+        uint8_t* sQ = smem + g * C::kGroupSmem + C::kQ;
+        uint8_t* sK = smem + g * C::kGroupSmem + C::kK;
+        uint8_t* sV = smem + g * C::kGroupSmem + C::kV;
+        TileIter<NSEG> ti;
+        ti.init(args, blockIdx.x + g * gridDim.x);
+        int it = 0;
+        for (; ti.valid(args); ti.next(args)) {
+          const int qb = ti.i & 1;
+          if (ti.i >= 2) mbar_wait(gb.q_empty(qb), ((ti.i >> 1) - 1) & 1);
+          mbar_arrive_expect_tx(gb.q_full(qb), ti.nseg * C::kQBytes);
+          // segment s: rows of problem + s land at their tile rows, every other
+          // tile row is out of range (row < 0 or >= N) and zero-filled
+          for (int s = 0; s < ti.nseg; ++s)
+            tma_load_3d(sQ + (qb * NSEG + s) * C::kQBytes, &tm_q, gb.q_full(qb), 0,
+                        ti.off - s * args.N, ti.problem + s);
+          for (int j = 0; j < Tc; ++j, ++it) {
+            const int st = it % kStages;
+            if (it >= kStages) mbar_wait(gb.kv_empty(st), ((it / kStages) - 1) & 1);
+            mbar_arrive_expect_tx(gb.kv_full(st), ti.nseg * 2 * C::kKVBytes);
+            for (int s = 0; s < ti.nseg; ++s) {
+              tma_load_3d(sK + (st * NSEG + s) * C::kKVBytes, &tm_k, gb.kv_full(st), 0, j * BC,
+                          ti.problem + s);
+              tma_load_3d(sV + (st * NSEG + s) * C::kKVBytes, &tm_v, gb.kv_full(st), 0, j * BC,
+                          ti.problem + s);
+            }
+          }
+        }
+      }
+    } else if (warp < 4) {
+      if (warp == 3) {
+        // reciprocal table for step (11) -> shared memory, off the critical path:
+        // the softmax warps sync on named barrier 15 before their first normalization.
+        for (int i = lane; i < 1024; i += 32) recip[i] = g_recip.v[i];
+        __threadfence_block();
+        named_bar_arrive(15, C::kNWG * 128 + 32);
+      }
+      // ========================================================= MMA issuer of group `warp - 2`
+      // Issue order within a tile (tcgen05.mma of one thread execute in order,
+      // which also orders every TMEM WAR hazard between P V and a later Q K^T):
+      //   two S buffers:  QK_0 | QK_1 PV_0 | QK_2 PV_1 | ... | PV_last
+      //   one S buffer:   QK_0 | PV_0 QK_1 | PV_1 QK_2 | ... | PV_last
+      // The next tile's QK_0 follows PV_last, so the TMA loads and QK_0 of tile
+      // i+1 overlap the normalization of tile i.
+      const int g = warp - 2;
+      if (g < QT && lane == 0) {
+        const Bars gb{bars + g * C::kBarsPerGroup};
+        const uint32_t tG = tmem_base + g * C::kGroupCols;
+        const uint32_t tO = tG + C::kNumS * BC;
+        const uint32_t ones_addr = smem_u32(sOnes);
+        uint8_t* sQ = smem + g * C::kGroupSmem + C::kQ;
+        uint8_t* sK = smem + g * C::kGroupSmem + C::kK;
+        uint8_t* sV = smem + g * C::kGroupSmem + C::kV;
+        TileIter<NSEG> ti;
+        ti.init(args, blockIdx.x + g * gridDim.x);
+        for (; ti.valid(args); ti.next(args)) {
+          const int qb = ti.i & 1;
+          const int nseg = ti.nseg;
+          const int it0 = ti.i * Tc;
+          mbar_wait(gb.q_full(qb), (ti.i >> 1) & 1);
+          tc_fence_after();
+          if (ti.i == 0 && blockIdx.x == 0 && g == 0) QF_TS(2);
+          auto issue_qk = [&](int j) {
+            const int it = it0 + j;
+            const int st = it % kStages;
+            const int sb = (C::kNumS == 2) ? (it & 1) : 0;
+            mbar_wait(gb.kv_full(st), (it / kStages) & 1);
+            tc_fence_after();
+            if (ti.i == 0 && blockIdx.x == 0 && g == 0 && j < 7) QF_TS(3 + 4 * j);
+            // (1) S = sum_s Q_s K_{s,j}^T : M=128, N=BC, K=D in steps of 32 bytes.
+            for (int s = 0; s < nseg; ++s) {
+              const uint32_t q_addr = smem_u32(sQ + (qb * NSEG + s) * C::kQBytes);
+              const uint32_t k_addr = smem_u32(sK + (st * NSEG + s) * C::kKVBytes);
+#pragma unroll
+              for (int kk = 0; kk < D / 32; ++kk) {
+                const uint64_t da = make_smem_desc(q_addr + 32 * kk, 16, 8 * D, kSwz);
+                const uint64_t db = make_smem_desc(k_addr + 32 * kk, 16, 8 * D, kSwz);
+                mma_i8_ss(tG + sb * BC, da, db, kIdescQK, (s > 0 || kk > 0) ? 1u : 0u);
+              }
+            }
+            mma_commit(gb.s_full(sb));
+            if (j == Tc - 1) mma_commit(gb.q_empty(qb));  // last read of this Q tile
+          };
+          auto issue_pv = [&](int j) {
+            const int it = it0 + j;
+            const int st = it % kStages;
+            const int sb = (C::kNumS == 2) ? (it & 1) : 0;
+            // (8) O (+)= sum_s P_s [V_{s,j} | 1] : M=128, N=D+16, K=BC in steps of 32 keys.
+            mbar_wait(gb.p_full(), it & 1);
+            tc_fence_after();
+            if (ti.i == 0 && blockIdx.x == 0 && g == 0 && j < 7) QF_TS(4 + 4 * j);
+            for (int s = 0; s < nseg; ++s) {
+              const uint32_t v_addr = smem_u32(sV + (st * NSEG + s) * C::kKVBytes);
+#pragma unroll
+              for (int kk = 0; kk < BC / 32; ++kk) {
+                const uint32_t vk = v_addr + 32 * kk * D;
+                const uint64_t db = make_smem_desc(vk, ones_addr - v_addr, 8 * D, kSwz);
+                mma_i8_ts(tO, tG + sb * BC + p_col_k<BC, C::kCW>(kk, s), db, kIdescPV,
+                          (j > 0 || s > 0 || kk > 0) ? 1u : 0u);
+              }
+            }
+            mma_commit(gb.kv_empty(st));
+            mma_commit(gb.o_full());
+          };
+          issue_qk(0);
+          for (int j = 0; j < Tc; ++j) {
+            if (C::kNumS == 2 && j + 1 < Tc) issue_qk(j + 1);
+            issue_pv(j);
+            if (C::kNumS == 1 && j + 1 < Tc) issue_qk(j + 1);
+          }
+        }
+        // every MMA of this group is issued: let the next grid (dequantize) be
+        // scheduled while the last tiles' softmax and normalization finish
+        griddep_launch();
+      }
+    } else {
+      const int sw = warp - C::kCtl;
+      const int wg = sw >> 2;
+      const int g = wg / CS;
+      const int c = wg - g * CS;
+      const Bars gb{bars + g * C::kBarsPerGroup};
+      const uint32_t red_group = smem_u32(smem + C::kRed) + static_cast<uint32_t>(g * 2 * CS * 128 * 4);
+      const uint32_t tG = tmem_base + g * C::kGroupCols;
+      if (prm.q_shift == 0 && static_cast<uint64_t>(prm.s_inv) * static_cast<uint64_t>(prm.m_p) < (1ull << 32))
+        softmax_role<D, BC, NSEG, CS, QT, DBG, true>(args, prm, tG, gb, red_group, recip, g, c, warp & 3, lane);
+      else
+        softmax_role<D, BC, NSEG, CS, QT, DBG, false>(args, prm, tG, gb, red_group, recip, g, c, warp & 3, lane);
+    }
+  }
+
+  // ------------------------------------------------------------- teardown
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0 && blockIdx.x == 0) QF_TS(102);
+  if (warp == 2) tmem_dealloc(tmem_base, kTmemCols);
+}
+
+// ----------------------------------------------------------------------------
+// Host-side launch (called by the instantiation units).  `tiles` = number of
+// work tiles; the persistent grid is G = min(ceil(tiles / QT), SMs) CTAs whose
+// group g visits tiles b + g G, b + g G + QT G, ...
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG>
+cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                          AttnArgs args, int64_t tiles, int sms, cudaStream_t stream) {
+  using C = Cfg<D, BC, NSEG, CS, QT>;
+  static_assert(C::kAlloc <= 227 * 1024, "shared memory budget");
+  auto kern = qflash_attn_kernel<D, BC, NSEG, CS, QT, DBG>;
+  static int configured[16] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 16 || !configured[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kAlloc);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 16) configured[dev] = 1;
+  }
+  const int64_t need = (tiles + QT - 1) / QT;
+  const int64_t G = need < sms ? need : sms;
+  const int64_t stride = QT * G;  // tiles between consecutive visits of one group
+  if (NSEG == 1) {
+    const int64_t Tr = args.Tr;
+    args.tr_magic = Tr > 1 ? static_cast<uint32_t>(((1ull << 32) + Tr - 1) / Tr) : 0u;
+    args.g_div = static_cast<int32_t>(stride / Tr);
+    args.g_mod = static_cast<int32_t>((stride % Tr) * kBlockR);
+  } else {
+    const uint64_t n = static_cast<uint64_t>(args.N);  // N >= 2 here
+    args.n_magic = ~0ull / n + 1ull;  // ceil(2^64 / N): floor(x / N) = hi64(x * n_magic), x < 2^32
+    const int64_t step = stride * kBlockR;
+    args.g_div = static_cast<int32_t>(step / args.N);
+    args.g_mod = static_cast<int32_t>(step % args.N);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(G));
+  cfg.blockDim = dim3(C::kThreads);
+  cfg.dynamicSmemBytes = C::kAlloc;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddep_wait)
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl_mask() & 1) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, args);
+}
+
+#undef QF_TS
+
+}  // namespace qf

@@ -18,10 +18,35 @@
 #include "qflash_params.cuh"
 
 namespace qf {
-cudaError_t launch_attention(int D, int BC, int nseg, const CUtensorMap& tq, const CUtensorMap& tk,
-                             const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
-                             int mode, cudaStream_t stream);
-bool attention_config_supported(int D, int BC, int nseg);
+#define QF_DECL_D(D)                                                                      \
+  cudaError_t launch_attention_d##D(int BC, int nseg, int cfg, const CUtensorMap& tq,      \
+                                    const CUtensorMap& tk, const CUtensorMap& tv,          \
+                                    const AttnArgs& args, int64_t tiles, int sms,          \
+                                    cudaStream_t stream);                                  \
+  bool attention_supported_d##D(int BC, int nseg, int cfg);
+QF_DECL_D(32)
+QF_DECL_D(64)
+QF_DECL_D(128)
+#undef QF_DECL_D
+cudaError_t launch_attention_dbg(int D, int BC, int nseg, int cfg, const CUtensorMap& tq,
+                                 const CUtensorMap& tk, const CUtensorMap& tv,
+                                 const AttnArgs& args, int64_t tiles, int sms,
+                                 cudaStream_t stream);
+inline bool attention_supported(int D, int BC, int nseg, int cfg) {
+  return D == 32 ? attention_supported_d32(BC, nseg, cfg)
+       : D == 64 ? attention_supported_d64(BC, nseg, cfg)
+       : D == 128 ? attention_supported_d128(BC, nseg, cfg) : false;
+}
+inline cudaError_t launch_attention(int D, int BC, int nseg, int cfg, const CUtensorMap& tq,
+                                    const CUtensorMap& tk, const CUtensorMap& tv,
+                                    const AttnArgs& args, int64_t tiles, int sms, bool dbg,
+                                    cudaStream_t stream) {
+  if (dbg) return launch_attention_dbg(D, BC, nseg, cfg, tq, tk, tv, args, tiles, sms, stream);
+  if (D == 32) return launch_attention_d32(BC, nseg, cfg, tq, tk, tv, args, tiles, sms, stream);
+  if (D == 64) return launch_attention_d64(BC, nseg, cfg, tq, tk, tv, args, tiles, sms, stream);
+  if (D == 128) return launch_attention_d128(BC, nseg, cfg, tq, tk, tv, args, tiles, sms, stream);
+  return cudaErrorNotSupported;
+}
 cudaError_t launch_quantize(const QuantTensors& t, int ntensors, int dtype, int64_t numel,
                             IntParams* prm_out, int32_t head_dim, cudaStream_t stream,
                             float* partial);
@@ -169,19 +194,11 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   // floor((N + 126) / N) + 1 problems; supported up to 4 segments.
   const int seg_need = N >= 2 ? (N + 126) / N + 1 : 129;
   const int nseg_tpl = seg_need <= 2 ? 2 : 4;
-  const bool packable = seg_need <= 4 && qf::attention_config_supported(d, bc_eff, nseg_tpl);
+  const bool packable = seg_need <= 4 && (qf::attention_supported(d, bc_eff, nseg_tpl, 0) ||
+                                          qf::attention_supported(d, bc_eff, nseg_tpl, 1));
   const int64_t Tr = (N + 127) / 128;
   const int64_t tiles_generic = static_cast<int64_t>(P) * Tr;
   const int64_t tiles_packed = (static_cast<int64_t>(P) * N + 127) / 128;
-  // Kernel configuration (qflash_attention.cu "MODE"): small tiles (B_c = 64,
-  // d = 32: the Swin windows) run two CTAs per SM with two softmax warpgroups;
-  // everything else one CTA per SM with four.  QFLASH_ATTN_MODE=0/1 overrides.
-  static int mode_env = -2;
-  if (mode_env == -2) {
-    const char* env = getenv("QFLASH_ATTN_MODE");
-    mode_env = (env != nullptr && (env[0] == '0' || env[0] == '1')) ? env[0] - '0' : -1;
-  }
-  const int mode = mode_env >= 0 ? mode_env : ((bc_eff == 64 && d == 32) ? 1 : 0);
   int sms = 0;
   {
     int dev = 0;
@@ -195,11 +212,10 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
       if (dev >= 0 && dev < 64) sm_cache[dev] = sms;
     }
   }
-  // AUTO packs rows only when that saves a wave of the persistent grid: a
+  // AUTO packs rows only when that saves a wave of one-tile-per-SM work: a
   // row-packed tile costs a little more (one TMA load and MMA per segment).
-  const int64_t slots = static_cast<int64_t>(sms) * ((mode == 1 && bc_eff + d + 16 <= 256) ? 2 : 1);
-  const int64_t waves_generic = (tiles_generic + slots - 1) / slots;
-  const int64_t waves_packed = (tiles_packed + slots - 1) / slots;
+  const int64_t waves_generic = (tiles_generic + sms - 1) / sms;
+  const int64_t waves_packed = (tiles_packed + sms - 1) / sms;
   bool packed;
   switch (variant) {
     case QFLASH_VARIANT_AUTO: packed = packable && waves_packed < waves_generic; break;
@@ -214,8 +230,20 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
     default: return fail(QFLASH_ERR_INVALID_ARGUMENT, "unknown variant %d", static_cast<int>(variant));
   }
   const int nseg = packed ? nseg_tpl : 1;
-  if (static_cast<int64_t>(P) * N >= (1ll << 31) - 256)
-    return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "num_problems * seq_len must be < 2^31");
+  const int64_t tiles = packed ? tiles_packed : tiles_generic;
+  // Kernel configuration (qflash_attn_kernel.cuh): cfg 1 (two ping-ponging
+  // query tiles per CTA, 2 column splits) when there is more than one wave of
+  // tiles and it fits TMEM / shared memory; else cfg 0 (one tile, 4 column
+  // splits: lowest latency per tile).  QFLASH_ATTN_CFG=0/1 overrides.
+  static int cfg_env = -2;
+  if (cfg_env == -2) {
+    const char* env = getenv("QFLASH_ATTN_CFG");
+    cfg_env = (env != nullptr && (env[0] == '0' || env[0] == '1')) ? env[0] - '0' : -1;
+  }
+  int cfg = (tiles > sms && qf::attention_supported(d, bc_eff, nseg, 1)) ? 1 : 0;
+  if (cfg_env >= 0 && qf::attention_supported(d, bc_eff, nseg, cfg_env)) cfg = cfg_env;
+  if (!qf::attention_supported(d, bc_eff, nseg, cfg))
+    return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "no kernel configuration for d=%d block=%d", d, bc_eff);
   CUtensorMap tq, tk, tv;
   qflash_status st;
   if ((st = make_tmap(&tq, q, P, N, d, 128, 1)) != QFLASH_OK) return st;
@@ -233,10 +261,10 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   args.dbg_p = dbg_p;
   args.dbg_o = dbg_o;
   args.dbg_t = dbg_t;
-  // Persistent grid: kMinBlocks CTAs per SM, each walking tiles b, b + G, b + 2G, ...
-  const int64_t tiles = packed ? tiles_packed : tiles_generic;
+  // Persistent grid: one CTA per SM, its groups walking tiles b + g G, + QT G, ...
   args.Tr = static_cast<int32_t>(Tr);
-  cudaError_t e = qf::launch_attention(d, bc_eff, nseg, tq, tk, tv, args, tiles, sms, mode, stream);
+  const bool dbg = dbg_s != nullptr || dbg_p != nullptr || dbg_o != nullptr || dbg_t != nullptr;
+  cudaError_t e = qf::launch_attention(d, bc_eff, nseg, cfg, tq, tk, tv, args, tiles, sms, dbg, stream);
   if (e != cudaSuccess) return cuda_fail(e, "attention launch");
   return QFLASH_OK;
 }

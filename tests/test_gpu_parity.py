@@ -39,9 +39,19 @@ def _gpu_attention(q, k, v, sq, sk, sv=0.03, block_kv=128, variant="auto"):
 N_GRID = [1, 2, 31, 32, 33, 48, 49, 50, 63, 64, 65, 127, 128, 129, 196, 197, 255, 256, 257]
 
 
+def _config_fits(D, BC, NSEG, CS, QT):
+    """Mirror of config_fits<> in qflash_attn_kernel.cuh (TMEM columns, columns per
+    thread, shared memory)."""
+    nums = 2 if (QT == 1 and 2 * BC + D + 16 <= 512) else 1
+    smem = (QT * (2 * NSEG * 128 * D + 2 * 2 * NSEG * BC * D) + BC * D + 64 * 8
+            + QT * 2 * CS * 512 + 4096 + 2048)
+    return (QT * (nums * BC + D + 16) <= 512 and BC // CS in (16, 32, 64) and (D // CS) % 8 == 0
+            and NSEG * (BC // 4) <= BC and smem <= 227 * 1024)
+
+
 def _packable(N, d, bkv):
     """Mirror of qflash_host.cu: the row-packed tiling needs <= 4 problems per
-    128-row tile and an instantiated (d, B_c, NSEG) kernel."""
+    128-row tile and an instantiated (d, B_c, NSEG) kernel in either configuration."""
     if N < 2:
         return False
     bc = (64 if N <= 64 else 128 if N <= 128 else 256) if N <= bkv else bkv
@@ -49,9 +59,7 @@ def _packable(N, d, bkv):
     if seg > 4:
         return False
     nseg = 2 if seg <= 2 else 4
-    if nseg == 2:
-        return not (d == 128 and bc == 256)
-    return d != 128 and bc != 256
+    return _config_fits(d, bc, nseg, 4, 1) or _config_fits(d, bc, nseg, 2, 2)
 
 
 @pytest.mark.parametrize("N", N_GRID)

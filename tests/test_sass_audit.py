@@ -1,0 +1,52 @@
+"""SASS audit of libqflash.so (CPU only, cuobjdump): every production instantiation
+of the fused attention kernel is integer-only -- no floating-point instruction
+(the north star's "integer softmax epilogue ... that never touches floating
+point") -- and uses the tcgen05 tensor-core / TMEM / TMA path."""
+from __future__ import annotations
+
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+from paper_2604_25306_b200 import _build
+
+FP_OPCODES = {
+    "FADD", "FADD32I", "FMUL", "FMUL32I", "FFMA", "FFMA32I", "FMNMX", "FSETP", "FSET", "FSEL",
+    "FCHK", "FRND", "FCMP", "FSWZADD", "F2I", "F2F", "F2FP", "I2F", "I2FP", "MUFU", "DADD",
+    "DMUL", "DFMA", "DSETP", "DMNMX", "HADD2", "HMUL2", "HFMA2", "HSETP2", "HMNMX2",
+}
+
+
+def _functions():
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    lib = _build.build()
+    out = subprocess.run([exe, "-sass", lib], capture_output=True, text=True, check=True).stdout
+    funcs, cur = {}, None
+    for line in out.splitlines():
+        m = re.match(r"\s*Function : (\S+)", line)
+        if m:
+            cur = m.group(1)
+            funcs[cur] = []
+            continue
+        m = re.match(r"\s*/\*[0-9a-f]{4,}\*/\s+(@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]*)", line)
+        if m and cur:
+            funcs[cur].append(m.group(2))
+    return funcs
+
+
+def test_attention_kernels_integer_only_and_tensor_core():
+    funcs = _functions()
+    prod = {n: ops for n, ops in funcs.items() if "qflash_attn_kernel" in n and "ELb0E" in n}
+    assert len(prod) >= 20, sorted(funcs)[:10]
+    for name, ops in prod.items():
+        fp = sorted({o for o in ops if o.split(".")[0] in FP_OPCODES})
+        assert not fp, f"{name}: floating-point SASS {fp}"
+        base = {o.split(".")[0] for o in ops}
+        assert "UTCIMMA" in base or any(o.startswith("UTC") and "MMA" in o for o in ops), name
+        assert "LDTM" in base and "STTM" in base, name
+        assert "UTMALDG" in base, name
