@@ -138,6 +138,7 @@ def algorithmic(P, N, d):
 # ALU roofline of the integer softmax: 10 int32 ops per
 # score element against 148 SMs x 128 int32 lanes x clock.
 ALU_OPS_PER_ELEM = 10.0
+
 SMS, INT32_LANES = 148, 128
 
 
@@ -233,6 +234,8 @@ def main():
     ap.add_argument("--ref-problems", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="fused", choices=["fused", "two", "three"],
+                    help="step form: one cooperative launch (default), or 2 / 3 launches")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -271,7 +274,8 @@ def main():
         # distinct bytes per set (sign flips keep the distribution and the scales)
         sgn = -1.0 if (i % 2) else 1.0
         sets.append([(t * sgn).roll(shifts=i, dims=1).contiguous() for t in base])
-    pipes = [qfl.QFlashPipeline(P_local, N, d, block_kv=args.block_kv, device=dev) for _ in range(n_sets)]
+    pipes = [qfl.QFlashPipeline(P_local, N, d, block_kv=args.block_kv, device=dev, mode=args.mode)
+             for _ in range(n_sets)]
 
     stream = torch.cuda.Stream(device=dev)
     graphs = []
@@ -324,8 +328,11 @@ def main():
     value = ops_all / (elapsed_ms * 1e-3) / 1e12
     clocks = sampler.summary(t_host0, t_host1)
 
-    # ---- dominant kernel (attention) measured alone with events on its stream
+    # ---- dominant kernel measured alone with events on its stream: the fused
+    # step kernel (quantize prologue + attention + dequantize epilogue) when the
+    # step is one launch, else the attention kernel with the fused dequantize
     k_launch = min(args.steps, 2000)
+    one_launch = pipes[0].launches() == 1
     ka, kb = [], []
     with torch.cuda.stream(stream):
         # head start covering the host cost of every eager launch (<= 50 us each),
@@ -335,8 +342,12 @@ def main():
             p = pipes[i % n_sets]
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            qfl.qflash_attention_int8_prepared(p.qkv_q[0], p.qkv_q[1], p.qkv_q[2], p.workspace,
-                                               args.block_kv, out=p.o_q, stream=stream)
+            if one_launch:
+                p(*sets[i % n_sets], stream=stream)
+            else:
+                qfl.qflash_attention_dequant_prepared(p.qkv_q[0], p.qkv_q[1], p.qkv_q[2],
+                                                      p.workspace, args.block_kv, out=p.out,
+                                                      stream=stream)
             b.record(stream)
             ka.append(a)
             kb.append(b)
@@ -344,8 +355,7 @@ def main():
     durs = sorted(x.elapsed_time(y) for x, y in zip(ka, kb))
     attn_ms = statistics.mean(durs[: max(1, int(0.9 * len(durs)))])  # drop the slowest 10 %
 
-    # ---- per-stage breakdown of one step (eager, events between the launches)
-    from paper_2604_25306_b200 import _lib as _l
+    # ---- for context: the two-launch form of the step, stage by stage (eager)
     k_bd = min(args.steps, 500)
     evs = []
     with torch.cuda.stream(stream):
@@ -353,25 +363,23 @@ def main():
         for i in range(k_bd):
             p = pipes[i % n_sets]
             s_in = sets[i % n_sets]
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             e[0].record(stream)
             qfl.qflash_quantize_qkv_prepare(*s_in, outs=p.qkv_q, scales=p.scales,
                                             workspace=p.workspace, stream=stream)
             e[1].record(stream)
-            qfl.qflash_attention_int8_prepared(p.qkv_q[0], p.qkv_q[1], p.qkv_q[2], p.workspace,
-                                               args.block_kv, out=p.o_q, stream=stream)
+            qfl.qflash_attention_dequant_prepared(p.qkv_q[0], p.qkv_q[1], p.qkv_q[2], p.workspace,
+                                                  args.block_kv, out=p.out, stream=stream)
             e[2].record(stream)
-            qfl.qflash_dequantize(p.o_q, p.scales[2:3], out=p.out, stream=stream)
-            e[3].record(stream)
             evs.append(e)
     torch.cuda.synchronize()
     def _med(a, b):
         return statistics.median(x[a].elapsed_time(x[b]) for x in evs) * 1e3
-    breakdown = {"quantize_qkv_us": _med(0, 1), "attention_us": _med(1, 2),
-                 "dequantize_us": _med(2, 3),
+    breakdown = {"two_launch_quantize_qkv_us": _med(0, 1), "two_launch_attention_dequant_us": _med(1, 2),
                  "note": "eager launches, GPU kept busy; medians over %d steps" % k_bd}
     # share of the step (the ncu launch list must agree on this share)
     attn_share = attn_ms / ms_per_step
+    launches_per_step = pipes[0].launches()
 
     pk = peaks()
     sm_clk_ghz = (pk.get("sm_max_mhz") or 1965.0) / 1e3
@@ -379,7 +387,9 @@ def main():
     alu_achieved = ALU_OPS_PER_ELEM * alg["score_elems"] / (attn_ms * 1e-3) / 1e12
     int8_peak_tops = 2.0 * pk.get("bf16_tflops", 1674.9)          # measured bf16 x nominal 2x
     roofline = {
-        "kernel": "qflash_attn_kernel", "bound": "alu", "achieved": alu_achieved,
+        "kernel": ("qflash_attn_kernel<FQ> (fused step: quantize prologue + attention + dequantize)"
+                   if one_launch else "qflash_attn_kernel (fused dequantize epilogue)"),
+        "bound": "alu", "achieved": alu_achieved,
         "peak": alu_peak, "unit": "T int32-op/s", "frac": alu_achieved / alu_peak,
         "traffic": None,
         "per_unit": "10 int32 ops per score element (SURVEY 8(d)); units = N^2 P per launch",
@@ -454,9 +464,10 @@ def main():
             "config": {"workload": f"{name} b{batch} ({w.source})", "problems": P_total,
                        "problems_per_rank": P_local, "seq_len": N, "head_dim": d,
                        "block_kv": args.block_kv, "parallelism": f"independent problems x{world}",
-                       "step": "quantize_qkv_prepare (amax + quantize) + attention_int8_prepared + dequantize (CUDA graph)",
+                       "step": ("qflash_forward_fused (CUDA graph, 1 cooperative launch)" if launches_per_step == 1
+                                else "quantize_qkv_prepare + attention_dequant_prepared (CUDA graph)"),
                        "l2": f"rotating {n_sets} input sets ({n_sets * set_bytes / 2**20:.0f} MiB > 2x L2)"},
-            "gpu_launches": 4 * args.steps,
+            "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         }
         print(json.dumps(line))

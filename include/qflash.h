@@ -128,7 +128,7 @@ QFLASH_API qflash_status qflash_attention_int8_ex(const int8_t* q, const int8_t*
  * are out of range nothing is written to o and the int32 at workspace_dev[0]
  * holds QFLASH_ERR_SCALE_RANGE (QFLASH_OK otherwise).  s_O = s_V stays in
  * scales_dev[2]. */
-#define QFLASH_DSCALE_WORKSPACE_BYTES 4096
+#define QFLASH_DSCALE_WORKSPACE_BYTES 8192
 QFLASH_API qflash_status qflash_attention_int8_dscale(const int8_t* q, const int8_t* k, const int8_t* v,
                                            const float* scales_dev,
                                            const qflash_attn_shape* shape, qflash_variant variant,
@@ -140,7 +140,8 @@ QFLASH_API qflash_status qflash_attention_int8_dscale(const int8_t* q, const int
  * attention's integer constants from the final (s_q, s_k) on the device (block 0
  * of the quantize kernel, same fp64 expression as qflash_derive_params) into
  * workspace_dev (QFLASH_DSCALE_WORKSPACE_BYTES, 16-byte aligned; int32 status at
- * offset 0; bytes 256.. hold per-CTA amax partials).  When Q, K and V fit in the
+ * offset 0; bytes 256..4095 hold per-CTA amax partials, bytes 4096..5119 the
+ * 256-entry dequantization table fl32(s_V * i), i = -128..127).  When Q, K and V fit in the
  * GPU's aggregate shared memory the quantization is a single cooperative pass
  * (HBM read once); otherwise amax and quantize are two streaming launches.  qflash_attention_int8_prepared then runs Algorithm 1 with the
  * constants found in workspace_dev (nothing is written to o if the status is
@@ -156,6 +157,41 @@ QFLASH_API qflash_status qflash_attention_int8_prepared(const int8_t* q, const i
                                                         qflash_variant variant, int8_t* o,
                                                         const void* workspace_dev,
                                                         qflash_stream_t stream);
+
+/* Algorithm 1 fused with the dequantization of its output (the DQ step): after
+ * qflash_quantize_qkv_prepare, writes y = fl32(s_V * (float)O^) (fp32 [P, N, d],
+ * s_O = s_V) straight from the attention epilogue -- bit-identical to
+ * qflash_attention_int8_prepared followed by qflash_dequantize_dscale, one launch
+ * and one HBM pass fewer.  The epilogue stays integer-only: the fp32 bit pattern
+ * of every int8 value comes from a 256-entry table that the quantize kernel
+ * computed with the same IEEE multiply (workspace_dev bytes 4096..5119).  o (int8
+ * [P, N, d]) may be NULL; if given it receives O^ as well.  Nothing is written if
+ * the device-derived status is not QFLASH_OK. */
+QFLASH_API qflash_status qflash_attention_dequant_prepared(const int8_t* q, const int8_t* k,
+                                                           const int8_t* v,
+                                                           const qflash_attn_shape* shape,
+                                                           qflash_variant variant, int8_t* o,
+                                                           float* y, const void* workspace_dev,
+                                                           qflash_stream_t stream);
+
+/* The whole hot path in ONE launch (fp32 inputs): per-tensor quantization of Q,
+ * K, V (Eq. 2, dynamic scales P:L703) in a cooperative prologue of the attention
+ * kernel (amax over a grid-stride share, grid barrier, scales + integer
+ * constants + dequant table derived identically in every CTA, int8 codes written
+ * to q_q / k_q / v_q, grid barrier), then Algorithm 1 on those codes and the
+ * fused dequantization y = fl32(s_V * O^).  Bit-identical to
+ * qflash_quantize_qkv_prepare + qflash_attention_dequant_prepared.  q, k, v:
+ * device fp32 [P, N, d]; q_q, k_q, v_q: device int8 [P, N, d] (written); o:
+ * optional int8 O^; y: device fp32 [P, N, d]; scales_dev: device float[3]
+ * (written: s_q, s_k, s_v); workspace_dev: QFLASH_DSCALE_WORKSPACE_BYTES (same
+ * layout as the prepare path).  All pointers 16-byte aligned, outputs must not
+ * alias inputs.  Launched cooperatively (every CTA resident, one per SM). */
+QFLASH_API qflash_status qflash_forward_fused(const float* q, const float* k, const float* v,
+                                              const qflash_attn_shape* shape,
+                                              qflash_variant variant, int8_t* q_q, int8_t* k_q,
+                                              int8_t* v_q, int8_t* o, float* y,
+                                              float* scales_dev, void* workspace_dev,
+                                              qflash_stream_t stream);
 
 /* Inverse of Eq. 2: y = fl32(scale * (float)x^).  x_q device int8[numel],
  * y device float[numel]. */

@@ -11,6 +11,9 @@ import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libqflash.so")
+# A/B experiments (tools/) may point at an alternative in-tree build of the same ABI.
+if os.environ.get("QFLASH_LIB"):
+    LIB_PATH = os.path.join(_PKG, os.path.basename(os.environ["QFLASH_LIB"]))
 
 QFLASH_OK = 0
 QFLASH_ERR_INVALID_ARGUMENT = 1
@@ -21,7 +24,7 @@ QFLASH_ERR_UNSUPPORTED_DEVICE = 5
 
 QFLASH_F32, QFLASH_BF16, QFLASH_F16 = 0, 1, 2
 VARIANTS = {"auto": 0, "generic": 1, "packed": 2}
-DSCALE_WORKSPACE_BYTES = 4096
+DSCALE_WORKSPACE_BYTES = 8192
 
 EXPORTED = [
     "qflash_quantize_per_tensor", "qflash_quantize_qkv", "qflash_attention_int8",
@@ -29,6 +32,7 @@ EXPORTED = [
     "qflash_dequantize_dscale", "qflash_derive_params", "qflash_partition",
     "qflash_status_string", "qflash_last_error", "qflash_version",
     "qflash_quantize_qkv_prepare", "qflash_attention_int8_prepared",
+    "qflash_attention_dequant_prepared", "qflash_forward_fused",
 ]
 
 
@@ -81,6 +85,12 @@ def lib():
     L.qflash_attention_int8_prepared.restype = st
     L.qflash_attention_int8_prepared.argtypes = [vp, vp, vp, ctypes.POINTER(AttnShape), st, vp,
                                                  vp, vp]
+    L.qflash_attention_dequant_prepared.restype = st
+    L.qflash_attention_dequant_prepared.argtypes = [vp, vp, vp, ctypes.POINTER(AttnShape), st, vp,
+                                                    vp, vp, vp]
+    L.qflash_forward_fused.restype = st
+    L.qflash_forward_fused.argtypes = [vp, vp, vp, ctypes.POINTER(AttnShape), st, vp, vp, vp, vp,
+                                       vp, vp, vp, vp]
     L.qflash_dequantize.restype = st
     L.qflash_dequantize.argtypes = [vp, f32, i64, vp, vp]
     L.qflash_dequantize_dscale.restype = st

@@ -142,17 +142,63 @@ def qflash_attention_int8_prepared(q: torch.Tensor, k: torch.Tensor, v: torch.Te
     return out
 
 
+def qflash_attention_dequant_prepared(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                                      workspace: torch.Tensor, block_kv: int = 128,
+                                      variant: str = "auto", out: torch.Tensor | None = None,
+                                      out_int8: torch.Tensor | None = None, stream=None):
+    """Algorithm 1 with the dequantization fused into its epilogue: fp32
+    y = s_V * O^ (and optionally the int8 O^), constants and dequant table from
+    `workspace` (qflash_quantize_qkv_prepare)."""
+    out = torch.empty(q.shape, dtype=torch.float32, device=q.device) if out is None else out
+    shape = _shape(q, block_kv)
+    check(lib().qflash_attention_dequant_prepared(
+        _dev_ptr(q), _dev_ptr(k), _dev_ptr(v), ctypes.byref(shape), _lib.VARIANTS[variant],
+        _dev_ptr(out_int8) if out_int8 is not None else None, _dev_ptr(out), _dev_ptr(workspace),
+        _stream(stream)))
+    return out
+
+
+def qflash_forward_fused(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, block_kv: int = 128,
+                         variant: str = "auto", out: torch.Tensor | None = None, codes=None,
+                         scales: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+                         out_int8: torch.Tensor | None = None, stream=None):
+    """The whole hot path in one cooperative launch: fp32 Q, K, V [P, N, d] ->
+    quantize (in the kernel's prologue) -> integer attention -> fp32 output."""
+    assert q.shape == k.shape == v.shape and q.dim() == 3
+    assert q.dtype == k.dtype == v.dtype == torch.float32
+    dev = q.device
+    out = torch.empty(q.shape, dtype=torch.float32, device=dev) if out is None else out
+    if codes is None:
+        codes = [torch.empty(q.shape, dtype=torch.int8, device=dev) for _ in range(3)]
+    scales = torch.empty(3, dtype=torch.float32, device=dev) if scales is None else scales
+    if workspace is None:
+        workspace = torch.empty(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=dev)
+    shape = _shape(q, block_kv)
+    check(lib().qflash_forward_fused(
+        _dev_ptr(q), _dev_ptr(k), _dev_ptr(v), ctypes.byref(shape), _lib.VARIANTS[variant],
+        _dev_ptr(codes[0]), _dev_ptr(codes[1]), _dev_ptr(codes[2]),
+        _dev_ptr(out_int8) if out_int8 is not None else None, _dev_ptr(out), _dev_ptr(scales),
+        _dev_ptr(workspace), _stream(stream)))
+    return out
+
+
 class QFlashPipeline:
-    """The whole hot path for one [P, N, d] workload with preallocated buffers:
-    fused Q/K/V quantization (+ device-side constant derivation) -> integer
-    attention -> dequantization.  Four of the library's kernels per call
-    (amax, quantize, attention, dequantize) and no host synchronization."""
+    """The whole hot path for one [P, N, d] workload with preallocated buffers.
+
+    mode "fused" (default for fp32 inputs): one cooperative launch -- quantize in
+    the attention kernel's prologue, integer attention, dequantized epilogue.
+    mode "two":   qflash_quantize_qkv_prepare + attention with the fused
+                  dequantize epilogue (two launches; any input dtype).
+    mode "three": prepare + int8 attention + qflash_dequantize.
+    No host synchronization in any mode; all are bit-identical."""
 
     def __init__(self, P: int, N: int, d: int, block_kv: int = 128, device="cuda",
-                 variant: str = "auto"):
+                 variant: str = "auto", mode: str = "fused"):
+        assert mode in ("fused", "two", "three")
         self.shape = (P, N, d)
         self.block_kv = block_kv
         self.variant = variant
+        self.mode = mode
         dev = torch.device(device)
         self.qkv_q = [torch.empty(self.shape, dtype=torch.int8, device=dev) for _ in range(3)]
         self.scales = torch.empty(3, dtype=torch.float32, device=dev)
@@ -160,12 +206,30 @@ class QFlashPipeline:
         self.workspace = torch.empty(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=dev)
         self.out = torch.empty(self.shape, dtype=torch.float32, device=dev)
 
+    def launches(self, dtype=torch.float32) -> int:
+        """Kernel launches per call (bench.py's gpu_launches)."""
+        if self.mode == "fused" and dtype == torch.float32:
+            return 1
+        P, N, d = self.shape
+        quant = 1 if (dtype == torch.float32 and P * N * d <= 148 * 2 * 256 * 4 * 4) else 2
+        return quant + (1 if self.mode == "two" else 2)
+
     def __call__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, stream=None):
+        if self.mode == "fused" and q.dtype == torch.float32:
+            return qflash_forward_fused(q, k, v, self.block_kv, self.variant, out=self.out,
+                                        codes=self.qkv_q, scales=self.scales,
+                                        workspace=self.workspace, stream=stream)
         qflash_quantize_qkv_prepare(q, k, v, outs=self.qkv_q, scales=self.scales,
                                     workspace=self.workspace, stream=stream)
-        qflash_attention_int8_prepared(self.qkv_q[0], self.qkv_q[1], self.qkv_q[2], self.workspace,
-                                       self.block_kv, self.variant, out=self.o_q, stream=stream)
-        qflash_dequantize(self.o_q, self.scales[2:3], out=self.out, stream=stream)
+        if self.mode != "three":
+            qflash_attention_dequant_prepared(self.qkv_q[0], self.qkv_q[1], self.qkv_q[2],
+                                              self.workspace, self.block_kv, self.variant,
+                                              out=self.out, stream=stream)
+        else:
+            qflash_attention_int8_prepared(self.qkv_q[0], self.qkv_q[1], self.qkv_q[2],
+                                           self.workspace, self.block_kv, self.variant,
+                                           out=self.o_q, stream=stream)
+            qflash_dequantize(self.o_q, self.scales[2:3], out=self.out, stream=stream)
         return self.out
 
 

@@ -57,6 +57,12 @@ QF_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
 QF_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 QF_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+QF_DEV long long globaltimer_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ---------------------------------------------------------------------- TMA
 QF_DEV void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
@@ -69,6 +75,10 @@ QF_DEV void tma_load_3d(void* smem_dst, const void* tmap, uint64_t* bar, int32_t
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+// Generic-proxy global writes of this thread ordered with async-proxy (TMA) accesses.
+QF_DEV void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 // Generic-proxy smem writes -> visible to the async proxy (TMA / tensor core).
 QF_DEV void fence_proxy_async_smem() {

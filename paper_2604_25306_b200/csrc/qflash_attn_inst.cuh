@@ -8,11 +8,11 @@
 
 namespace qf {
 
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FQ>
 cudaError_t try_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const AttnArgs& args, int64_t tiles, int sms, cudaStream_t stream) {
   if constexpr (config_fits<D, BC, NSEG, CS, QT>()) {
-    return launch_attn_t<D, BC, NSEG, CS, QT, DBG>(tq, tk, tv, args, tiles, sms, stream);
+    return launch_attn_t<D, BC, NSEG, CS, QT, DBG, FQ>(tq, tk, tv, args, tiles, sms, stream);
   } else {
     return cudaErrorNotSupported;
   }
@@ -20,14 +20,14 @@ cudaError_t try_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUten
 
 // cfg 0: CS = 4 column splits x QT = 1 (one query tile in flight, 16 softmax warps)
 // cfg 1: CS = 2 x QT = 2 (two ping-ponging query tiles, 8 softmax warps each)
-template <int D, bool DBG>
+template <int D, bool DBG, bool FQ = false>
 cudaError_t launch_attention_d(int BC, int nseg, int cfg, const CUtensorMap& tq,
                                const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& args,
                                int64_t tiles, int sms, cudaStream_t stream) {
 #define QF_BC_SEG(bc, ns)                                                                      \
   if (BC == bc && nseg == ns)                                                                  \
-    return cfg == 1 ? try_launch<D, bc, ns, 2, 2, DBG>(tq, tk, tv, args, tiles, sms, stream)   \
-                    : try_launch<D, bc, ns, 4, 1, DBG>(tq, tk, tv, args, tiles, sms, stream);
+    return cfg == 1 ? try_launch<D, bc, ns, 2, 2, DBG, FQ>(tq, tk, tv, args, tiles, sms, stream) \
+                    : try_launch<D, bc, ns, 4, 1, DBG, FQ>(tq, tk, tv, args, tiles, sms, stream);
   QF_BC_SEG(64, 1) QF_BC_SEG(128, 1) QF_BC_SEG(256, 1)
   QF_BC_SEG(64, 2) QF_BC_SEG(128, 2) QF_BC_SEG(256, 2)
   QF_BC_SEG(64, 4) QF_BC_SEG(128, 4)

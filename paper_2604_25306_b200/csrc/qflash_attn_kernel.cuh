@@ -44,8 +44,12 @@
 
 #include <cstdint>
 
+#include <cooperative_groups.h>
+
 #include "ptx.cuh"
 #include "qflash_common.cuh"
+#include "qflash_params.cuh"
+#include "qflash_quant_elem.cuh"
 
 namespace qf {
 
@@ -104,8 +108,10 @@ struct Cfg {
   static constexpr int kBar = kOnes + BC * D;
   static constexpr int kTmemSlot = kBar + QT * kBarsPerGroup * 8;
   static constexpr int kRed = (kTmemSlot + 16 + 15) / 16 * 16;  // [QT][2][CS][128] int32
-  static constexpr int kRecip = kRed + QT * 2 * CS * 128 * 4;   // [1024] u32
-  static constexpr int kTotal = kRecip + 1024 * 4;
+  static constexpr int kRecip = kRed + QT * 2 * CS * 128 * 4;   // [1024] u32 + [256] dequant
+  static constexpr int kPrm = kRecip + 1280 * 4;                // IntParams (fused step)
+  static constexpr int kScratch = kPrm + 128;                    // [3][32] f32 + [3] scales
+  static constexpr int kTotal = kScratch + 512;
   static constexpr int kAlloc = kTotal + 1024;                  // slack for 1024-B alignment
   static_assert(QT * kGroupCols <= 512, "TMEM budget");
   static_assert(NSEG * (BC / 4) <= BC, "P segments must fit in one S buffer");
@@ -119,7 +125,7 @@ constexpr bool config_fits() {
          (BC / CS == 16 || BC / CS == 32 || BC / CS == 64) && ((D / CS) % 8 == 0) &&
          (NSEG * (BC / 4) <= BC) &&
          (QT * (2 * NSEG * kBlockR * D + 2 * kStages * NSEG * BC * D) + BC * D + 64 * 8 +
-              QT * 2 * CS * 512 + 4096 + 2048 <=
+              QT * 2 * CS * 512 + 5120 + 640 + 2048 <=
           227 * 1024);
 }
 
@@ -390,7 +396,7 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
     const int64_t t = (static_cast<int64_t>(A) - static_cast<int64_t>(s_inv)) / 384 - 2 * Tc;
     rel_lthr = t < 0 ? -1 : (t > 0x7FFFFFFF ? 0x7FFFFFFF : static_cast<int32_t>(t));
   }
-  named_bar_sync(15, C::kNWG * 128 + 32);  // reciprocal table of step (11) ready
+  bool tables_ready = false;  // named barrier 15: step (11) / dequant tables in smem
 
   TileIter<NSEG> ti;
   ti.init(args, blockIdx.x + g * gridDim.x);
@@ -614,6 +620,10 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
     mbar_wait(gb.o_full(), itl & 1);
     tc_fence_after();
     if (dbg && ts_warp) QF_TS(100);
+    if (!tables_ready) {
+      named_bar_sync(15, C::kNWG * 128 + 32);
+      tables_ready = true;
+    }
     if (warp_live) {
       uint32_t lraw;
       uint32_t o[OW];
@@ -647,13 +657,32 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
                                     floor_div_exact(static_cast<int32_t>(o[e + 3]), rc.l));
         }
         // flattened output row problem * N + off + row (row-packed tiles included)
-        int8_t* dst = args.out + (static_cast<int64_t>(ti.problem) * N + ti.off + row) * D + c * OW;
-        if constexpr (OW == 8) {
-          *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
-        } else {
+        const int64_t orow = static_cast<int64_t>(ti.problem) * N + ti.off + row;
+        if (args.out != nullptr) {
+          int8_t* dst = args.out + orow * D + c * OW;
+          if constexpr (OW == 8) {
+            *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+          } else {
 #pragma unroll
-          for (int e = 0; e < OW / 16; ++e)
-            reinterpret_cast<uint4*>(dst)[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+            for (int e = 0; e < OW / 16; ++e)
+              reinterpret_cast<uint4*>(dst)[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+          }
+        }
+        if (args.out_f32 != nullptr) {
+          // fused dequantization y = s_V * O^ (DQ row): the fp32 bit pattern of
+          // every int8 value comes from a 256-entry table the quantize kernel
+          // computed with the same IEEE multiply as qflash_dequantize -- the
+          // attention kernel itself stays integer-only.
+          const uint32_t dqt = smem_u32(recip + 1024);
+          uint32_t* ydst = reinterpret_cast<uint32_t*>(args.out_f32 + orow * D + c * OW);
+#pragma unroll
+          for (int e = 0; e < OW / 4; ++e) {
+            uint32_t y4[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              y4[b] = static_cast<uint32_t>(lds32(dqt + ((((w[e] >> (8 * b)) & 0xFFu) ^ 0x80u) << 2)));
+            reinterpret_cast<uint4*>(ydst)[e] = make_uint4(y4[0], y4[1], y4[2], y4[3]);
+          }
         }
       }
     }
@@ -662,10 +691,180 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
     // arrival, so the next tile's first P V (which overwrites O) cannot race them.
     it0 += Tc;
   }
+  if (!tables_ready) named_bar_arrive(15, C::kNWG * 128 + 32);  // a group without tiles
+}
+
+// ---------------------------------------------------------------- fused-step prologue
+// Q0 for the fused step (FQ): every thread of the cooperative grid takes part.
+//  1. per-tensor amax over a grid-stride share of Q, K, V (fp32, one FMNMX per
+//     element), block reduce, per-CTA partial to global memory; grid barrier;
+//  2. every CTA reduces the partials to the same s = fl32(amax / 127) (R2, R3),
+//     derives the integer constants (derive_core, the fp64 expression of
+//     qflash_derive_params) and the 256-entry dequant table fl32(s_V * i) into
+//     shared memory (CTA 0 also publishes scales, constants and table);
+//  3. quantizes its share (inputs re-read from L2) with the exact element
+//     quantizer of qflash_quant.cu into the int8 buffers the TMA maps point at;
+//     proxy fence + grid barrier, after which the attention roles start.
+#ifdef QF_FQ_TIMING
+// experiment builds: globaltimer stamps of CTA 0 in the workspace (bytes 6144..)
+#define QF_FQ_TS(a, k)                                                                      \
+  do {                                                                                     \
+    if (blockIdx.x == 0 && threadIdx.x == 0)                                               \
+      reinterpret_cast<long long*>(reinterpret_cast<char*>((a).prm_out) + 6144)[k] = globaltimer_ns(); \
+  } while (0)
+#else
+#define QF_FQ_TS(a, k) \
+  do {                 \
+  } while (0)
+#endif
+// Quantize one float4 (4 elements) -> 4 packed int8 codes (exact, see qflash_quant_elem.cuh).
+__device__ __forceinline__ uint32_t quant4(const float4& v, float s, float r) {
+  int32_t q[4];
+  bool bad = false;
+  q[0] = quant_fast(v.x, r, bad);
+  q[1] = quant_fast(v.y, r, bad);
+  q[2] = quant_fast(v.z, r, bad);
+  q[3] = quant_fast(v.w, r, bad);
+  if (bad) {
+    q[0] = quant_exact(v.x, s);
+    q[1] = quant_exact(v.y, s);
+    q[2] = quant_exact(v.z, s);
+    q[3] = quant_exact(v.w, s);
+  }
+  return pack4_sat_s8(q[0], q[1], q[2], q[3]);
+}
+__device__ __forceinline__ float amax4(float m, const float4& v) {
+  return fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+}
+
+template <int D>
+__device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float* scratch,
+                                                       IntParams* sprm, uint32_t* dq_table) {
+  namespace cg = cooperative_groups;
+  constexpr int kVR = 4;  // register-resident 16-B vectors per tensor and thread
+  QF_FQ_TS(a, 0);
+  const int nthr_blk = blockDim.x;
+  const int64_t nthr = static_cast<int64_t>(gridDim.x) * nthr_blk;
+  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * nthr_blk + threadIdx.x;
+  const int64_t nvec = a.numel >> 2;
+  const bool resident = nvec <= kVR * nthr;  // the whole share stays in registers
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float m[3] = {0.f, 0.f, 0.f};
+  float4 reg[3][kVR];
+  if (resident) {
+    // every load of all three tensors in flight before the first reduction
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
+#pragma unroll
+      for (int u = 0; u < kVR; ++u) {
+        const int64_t i = gtid + u * nthr;
+        reg[t][u] = i < nvec ? __ldg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+#pragma unroll
+      for (int u = 0; u < kVR; ++u) m[t] = amax4(m[t], reg[t][u]);
+  } else {
+    for (int64_t i = gtid; i < nvec; i += 2 * nthr) {  // 6 16-B loads in flight
+      float4 v[3][2];
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
+        v[t][0] = __ldg(src + i);
+        v[t][1] = i + nthr < nvec ? __ldg(src + i + nthr) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int t = 0; t < 3; ++t) m[t] = amax4(amax4(m[t], v[t][0]), v[t][1]);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m[t] = fmaxf(m[t], __shfl_xor_sync(0xffffffffu, m[t], o));
+    if (lane == 0) scratch[t * 32 + warp] = m[t];
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    float b = 0.f;
+    for (int w = 0; w < nthr_blk / 32; ++w) b = fmaxf(b, scratch[threadIdx.x * 32 + w]);
+    a.partial[threadIdx.x * gridDim.x + blockIdx.x] = b;
+  }
+  QF_FQ_TS(a, 1);
+  __threadfence();
+  cg::this_grid().sync();
+  QF_FQ_TS(a, 2);
+  // 2. global scales (every CTA, identical): s = fl32(amax / 127), R3 for zeros
+  if (warp < 3) {
+    float b = 0.f;
+    for (int j = lane; j < static_cast<int>(gridDim.x); j += 32) b = fmaxf(b, __ldcg(&a.partial[warp * gridDim.x + j]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+    if (lane == 0) {
+      float sc = __fdiv_rn(b, 127.0f);
+      if (sc == 0.0f) sc = 1.0f / 127.0f;  // all-zero tensor (R3)
+      scratch[96 + warp] = sc;
+    }
+  }
+  __syncthreads();
+  const float s3[3] = {scratch[96], scratch[97], scratch[98]};
+  // the integer constants (one thread, ~1.3 us of fp64) overlap the quantization
+  // of every other warp; the roles read *sprm only after the final __syncthreads
+  if (threadIdx.x == 0) {
+    IntParams p;
+    const int st = derive_core(s3[0], s3[1], D, &p, nullptr);
+    if (st != QFLASH_OK) {
+      memset(&p, 0, sizeof(p));
+      p.status = st;
+    }
+    *sprm = p;
+    QF_FQ_TS(a, 3);
+    if (blockIdx.x == 0) {
+      *a.prm_out = p;
+      for (int t = 0; t < 3; ++t) a.scales_out[t] = s3[t];
+    }
+  } else if (threadIdx.x >= 32 && threadIdx.x < 32 + 256) {
+    // dequant table of the epilogue: fl32(s_V * i), i = -128..127
+    const int i = static_cast<int>(threadIdx.x) - 32 - 128;
+    const uint32_t bits = __float_as_uint(__fmul_rn(s3[2], static_cast<float>(i)));
+    dq_table[i + 128] = bits;
+    if (blockIdx.x == 0) a.table_out[i + 128] = bits;
+  }
+  // 3. quantize this thread's share (registers, or an L2-resident re-read)
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const float s = s3[t];
+    const float r = __frcp_rn(s);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(a.xq[t]);
+    if (resident) {
+#pragma unroll
+      for (int u = 0; u < kVR; ++u) {
+        const int64_t i = gtid + u * nthr;
+        if (i < nvec) dst[i] = quant4(reg[t][u], s, r);
+      }
+    } else {
+      const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
+      for (int64_t i = gtid; i < nvec; i += 2 * nthr) {
+        const float4 v0 = __ldcg(src + i);
+        const bool two = i + nthr < nvec;
+        const float4 v1 = two ? __ldcg(src + i + nthr) : make_float4(0.f, 0.f, 0.f, 0.f);
+        dst[i] = quant4(v0, s, r);
+        if (two) dst[i + nthr] = quant4(v1, s, r);
+      }
+    }
+  }
+  // int8 codes (generic-proxy stores) -> TMA loads of other CTAs after the barrier
+  QF_FQ_TS(a, 4);
+  fence_proxy_async_global();
+  __threadfence();
+  cg::this_grid().sync();
+  fence_proxy_async_global();
+  QF_FQ_TS(a, 5);
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FQ = false>
 __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
     qflash_attn_kernel(const __grid_constant__ CUtensorMap tm_q,
                        const __grid_constant__ CUtensorMap tm_k,
@@ -688,6 +887,10 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0 && blockIdx.x == 0) QF_TS(0);
+  if constexpr (FQ) QF_FQ_TS(args, 8);
+  if constexpr (DBG) {
+    if (threadIdx.x == 0 && args.dbg_t != nullptr) args.dbg_t[128 + 2 * blockIdx.x] = globaltimer_ns();
+  }
   const int Tc = args.Tc;
 
   // ------------------------------------------------------------- setup
@@ -727,51 +930,99 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
   // Everything above overlaps the tail of the previous kernel (programmatic
   // dependent launch); every global access of this grid comes after the wait.
   griddep_wait();
+  IntParams* sprm = reinterpret_cast<IntParams*>(smem + C::kPrm);
+  if constexpr (FQ) {
+    fused_quantize_prologue<D>(args, reinterpret_cast<float*>(smem + C::kScratch), sprm, recip + 1024);
+    __syncthreads();
+  }
+  const IntParams* dprm = FQ ? sprm : args.dev_prm;  // constants in memory, or nullptr (by value)
+
+  if (warp < 2) {
+    // ========================================================= TMA producer of group `warp`
+    // Starts before the integer constants are read: the first Q tile and KV
+    // stages load while the constants arrive; the device-derived status is
+    // checked before the first wait on a consumer (empty) barrier, and an
+    // out-of-range launch drains the loads already issued and stops.
+    const int g = warp;
+    if (g < QT && lane == 0) {
+      const Bars gb{bars + g * C::kBarsPerGroup};
+      uint8_t* sQ = smem + g * C::kGroupSmem + C::kQ;
+      uint8_t* sK = smem + g * C::kGroupSmem + C::kK;
+      uint8_t* sV = smem + g * C::kGroupSmem + C::kV;
+      int nq = 0, nkv = 0;  // loads issued before the status check
+      bool checked = false;
+      auto status_ok = [&]() -> bool {
+        if (checked) return true;
+        checked = true;
+        const int st = dprm != nullptr ? *reinterpret_cast<const volatile int32_t*>(&dprm->status)
+                                       : args.prm.status;
+        if (st == 0) return true;
+        for (int b = 0; b < nq; ++b) mbar_wait(gb.q_full(b), 0);
+        for (int b = 0; b < nkv; ++b) mbar_wait(gb.kv_full(b), 0);
+        return false;
+      };
+      TileIter<NSEG> ti;
+      ti.init(args, blockIdx.x + g * gridDim.x);
+      int it = 0;
+      bool ok = true;
+      for (; ok && ti.valid(args); ti.next(args)) {
+        const int qb = ti.i & 1;
+        if (ti.i >= 2) {
+          if (!(ok = status_ok())) break;
+          mbar_wait(gb.q_empty(qb), ((ti.i >> 1) - 1) & 1);
+        }
+        mbar_arrive_expect_tx(gb.q_full(qb), ti.nseg * C::kQBytes);
+        // segment s: rows of problem + s land at their tile rows, every other
+        // tile row is out of range (row < 0 or >= N) and zero-filled
+        for (int s = 0; s < ti.nseg; ++s)
+          tma_load_3d(sQ + (qb * NSEG + s) * C::kQBytes, &tm_q, gb.q_full(qb), 0,
+                      ti.off - s * args.N, ti.problem + s);
+        if (!checked) ++nq;
+        for (int j = 0; j < Tc; ++j, ++it) {
+          const int st = it % kStages;
+          if (it >= kStages) {
+            if (!(ok = status_ok())) break;
+            mbar_wait(gb.kv_empty(st), ((it / kStages) - 1) & 1);
+          }
+          mbar_arrive_expect_tx(gb.kv_full(st), ti.nseg * 2 * C::kKVBytes);
+          for (int s = 0; s < ti.nseg; ++s) {
+            tma_load_3d(sK + (st * NSEG + s) * C::kKVBytes, &tm_k, gb.kv_full(st), 0, j * BC,
+                        ti.problem + s);
+            tma_load_3d(sV + (st * NSEG + s) * C::kKVBytes, &tm_v, gb.kv_full(st), 0, j * BC,
+                        ti.problem + s);
+          }
+          if (!checked) ++nkv;
+        }
+      }
+      if (ok) status_ok();  // a short launch that never waited still drains on error
+    }
+  }
 
   // Integer constants (host-derived by value, or device-derived).
   IntParams prm = args.prm;
-  if (args.dev_prm != nullptr) prm = *args.dev_prm;
+  if (dprm != nullptr) prm = *dprm;
   const bool run = (prm.status == 0);
 
   if (run) {
     if (warp < 2) {
-      // ========================================================= TMA producer of group `warp`
-      const int g = warp;
-      if (g < QT && lane == 0) {
-        const Bars gb{bars + g * C::kBarsPerGroup};
-        uint8_t* sQ = smem + g * C::kGroupSmem + C::kQ;
-        uint8_t* sK = smem + g * C::kGroupSmem + C::kK;
-        uint8_t* sV = smem + g * C::kGroupSmem + C::kV;
-        TileIter<NSEG> ti;
-        ti.init(args, blockIdx.x + g * gridDim.x);
-        int it = 0;
-        for (; ti.valid(args); ti.next(args)) {
-          const int qb = ti.i & 1;
-          if (ti.i >= 2) mbar_wait(gb.q_empty(qb), ((ti.i >> 1) - 1) & 1);
-          mbar_arrive_expect_tx(gb.q_full(qb), ti.nseg * C::kQBytes);
-          // segment s: rows of problem + s land at their tile rows, every other
-          // tile row is out of range (row < 0 or >= N) and zero-filled
-          for (int s = 0; s < ti.nseg; ++s)
-            tma_load_3d(sQ + (qb * NSEG + s) * C::kQBytes, &tm_q, gb.q_full(qb), 0,
-                        ti.off - s * args.N, ti.problem + s);
-          for (int j = 0; j < Tc; ++j, ++it) {
-            const int st = it % kStages;
-            if (it >= kStages) mbar_wait(gb.kv_empty(st), ((it / kStages) - 1) & 1);
-            mbar_arrive_expect_tx(gb.kv_full(st), ti.nseg * 2 * C::kKVBytes);
-            for (int s = 0; s < ti.nseg; ++s) {
-              tma_load_3d(sK + (st * NSEG + s) * C::kKVBytes, &tm_k, gb.kv_full(st), 0, j * BC,
-                          ti.problem + s);
-              tma_load_3d(sV + (st * NSEG + s) * C::kKVBytes, &tm_v, gb.kv_full(st), 0, j * BC,
-                          ti.problem + s);
-            }
-          }
-        }
-      }
+      // (producer role above)
     } else if (warp < 4) {
       if (warp == 3) {
         // reciprocal table for step (11) -> shared memory, off the critical path:
         // the softmax warps sync on named barrier 15 before their first normalization.
-        for (int i = lane; i < 1024; i += 32) recip[i] = g_recip.v[i];
+        {
+          uint4 t[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) t[k] = reinterpret_cast<const uint4*>(g_recip.v)[lane + 32 * k];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) reinterpret_cast<uint4*>(recip)[lane + 32 * k] = t[k];
+          if (!FQ && args.out_f32 != nullptr) {  // fused dequantization table (256 fp32 bit patterns)
+            const uint4* src = reinterpret_cast<const uint4*>(args.dq_table);
+            const uint4 a = src[lane], b = src[lane + 32];
+            reinterpret_cast<uint4*>(recip + 1024)[lane] = a;
+            reinterpret_cast<uint4*>(recip + 1024)[lane + 32] = b;
+          }
+        }
         __threadfence_block();
         named_bar_arrive(15, C::kNWG * 128 + 32);
       }
@@ -873,6 +1124,10 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (threadIdx.x == 0 && blockIdx.x == 0) QF_TS(102);
+  if constexpr (FQ) QF_FQ_TS(args, 9);
+  if constexpr (DBG) {
+    if (threadIdx.x == 0 && args.dbg_t != nullptr) args.dbg_t[129 + 2 * blockIdx.x] = globaltimer_ns();
+  }
   if (warp == 2) tmem_dealloc(tmem_base, kTmemCols);
 }
 
@@ -880,12 +1135,12 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
 // Host-side launch (called by the instantiation units).  `tiles` = number of
 // work tiles; the persistent grid is G = min(ceil(tiles / QT), SMs) CTAs whose
 // group g visits tiles b + g G, b + g G + QT G, ...
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FQ = false>
 cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                           AttnArgs args, int64_t tiles, int sms, cudaStream_t stream) {
   using C = Cfg<D, BC, NSEG, CS, QT>;
   static_assert(C::kAlloc <= 227 * 1024, "shared memory budget");
-  auto kern = qflash_attn_kernel<D, BC, NSEG, CS, QT, DBG>;
+  auto kern = qflash_attn_kernel<D, BC, NSEG, CS, QT, DBG, FQ>;
   static int configured[16] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -915,10 +1170,18 @@ cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CU
   cfg.dynamicSmemBytes = C::kAlloc;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddep_wait)
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = (pdl_mask() & 1) ? 1 : 0;
+  if constexpr (FQ) {
+    // fused step: grid barriers in the quantize prologue need every CTA resident
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  } else {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddep_wait)
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (pdl_mask() & 1) ? 1 : 0;
+  }
   return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, args);
 }
 

@@ -40,12 +40,23 @@ struct AttnArgs {
   uint64_t n_magic;  // ceil(2^64 / N) (row-packed tiling)
   IntParams prm;    // used when dev_prm == nullptr
   const IntParams* dev_prm;  // device-derived constants (dscale path) or nullptr
-  int8_t* out;
+  int8_t* out;          // int8 output (may be nullptr when out_f32 is set)
+  float* out_f32;       // fused dequantized fp32 output, or nullptr
+  const uint32_t* dq_table;  // [256] fp32 bits of s_V * (i - 128) (device), with out_f32
+  // fused step (FQ instantiations): the kernel's prologue quantizes fp32 inputs
+  const float* xin[3];  // Q, K, V fp32 [P, N, d] (device)
+  int8_t* xq[3];        // their int8 codes (the TMA maps point here)
+  float* scales_out;    // device float[3]: s_q, s_k, s_v
+  float* partial;       // device float[3 * gridDim.x]: per-CTA amax partials
+  IntParams* prm_out;   // device copy of the derived constants (workspace)
+  uint32_t* table_out;  // device copy of the dequant table (workspace + 4096)
+  int64_t numel;        // elements per tensor (a multiple of 4: d in {32, 64, 128})
   // bring-up dumps for CTA 0's first tile only; nullptr in production:
   int32_t* dbg_s;  // [128][BC] raw S of KV tile 0
   int32_t* dbg_p;  // [128][BC/4] packed P words of KV tile 0
   int32_t* dbg_o;  // [128][D+1] final O and l before normalization
-  long long* dbg_t;  // [128] clock64 timeline of CTA 0 (see QF_TS slots)
+  long long* dbg_t;  // [128] clock64 timeline of CTA 0 (see QF_TS slots), then
+                     // globaltimer (entry, exit) of every CTA b at [128 + 2b]
 };
 
 // Up to three tensors quantized by one launch pair (Q/K/V fusion).

@@ -28,6 +28,15 @@ QF_DECL_D(32)
 QF_DECL_D(64)
 QF_DECL_D(128)
 #undef QF_DECL_D
+cudaError_t launch_fused_d32(int BC, int nseg, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
+                             cudaStream_t stream);
+cudaError_t launch_fused_d64(int BC, int nseg, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
+                             cudaStream_t stream);
+cudaError_t launch_fused_d128(int BC, int nseg, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
+                              const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
+                              cudaStream_t stream);
 cudaError_t launch_attention_dbg(int D, int BC, int nseg, int cfg, const CUtensorMap& tq,
                                  const CUtensorMap& tk, const CUtensorMap& tv,
                                  const AttnArgs& args, int64_t tiles, int sms,
@@ -40,7 +49,13 @@ inline bool attention_supported(int D, int BC, int nseg, int cfg) {
 inline cudaError_t launch_attention(int D, int BC, int nseg, int cfg, const CUtensorMap& tq,
                                     const CUtensorMap& tk, const CUtensorMap& tv,
                                     const AttnArgs& args, int64_t tiles, int sms, bool dbg,
-                                    cudaStream_t stream) {
+                                    bool fused, cudaStream_t stream) {
+  if (fused) {
+    if (D == 32) return launch_fused_d32(BC, nseg, cfg, tq, tk, tv, args, tiles, sms, stream);
+    if (D == 64) return launch_fused_d64(BC, nseg, cfg, tq, tk, tv, args, tiles, sms, stream);
+    if (D == 128) return launch_fused_d128(BC, nseg, cfg, tq, tk, tv, args, tiles, sms, stream);
+    return cudaErrorNotSupported;
+  }
   if (dbg) return launch_attention_dbg(D, BC, nseg, cfg, tq, tk, tv, args, tiles, sms, stream);
   if (D == 32) return launch_attention_d32(BC, nseg, cfg, tq, tk, tv, args, tiles, sms, stream);
   if (D == 64) return launch_attention_d64(BC, nseg, cfg, tq, tk, tv, args, tiles, sms, stream);
@@ -180,10 +195,18 @@ qflash_status validate_qkvo(const int8_t* q, const int8_t* k, const int8_t* v, c
   return QFLASH_OK;
 }
 
+struct FusedIn {
+  const float* x[3];
+  int8_t* xq[3];
+  float* scales;
+  void* workspace;
+};
+
 qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
                             const qflash_attn_shape* shape, int bc, qflash_variant variant,
                             int8_t* o, const qf::IntParams* host_prm,
-                            const qf::IntParams* dev_prm, cudaStream_t stream,
+                            const qf::IntParams* dev_prm, cudaStream_t stream, float* y,
+                            const FusedIn* fin,
                             int32_t* dbg_s = nullptr, int32_t* dbg_p = nullptr,
                             int32_t* dbg_o = nullptr, long long* dbg_t = nullptr) {
   const int P = shape->num_problems, N = shape->seq_len, d = shape->head_dim;
@@ -257,6 +280,23 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   if (host_prm) args.prm = *host_prm;
   args.dev_prm = dev_prm;
   args.out = o;
+  if (y != nullptr && fin == nullptr) {
+    args.out_f32 = y;
+    args.dq_table = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(dev_prm) + 4096);
+  }
+  if (fin != nullptr) {  // fused step: the kernel quantizes fin->x into q/k/v itself
+    args.out_f32 = y;
+    args.dev_prm = nullptr;
+    for (int t = 0; t < 3; ++t) {
+      args.xin[t] = fin->x[t];
+      args.xq[t] = fin->xq[t];
+    }
+    args.scales_out = fin->scales;
+    args.prm_out = reinterpret_cast<qf::IntParams*>(fin->workspace);
+    args.partial = reinterpret_cast<float*>(static_cast<char*>(fin->workspace) + 256);
+    args.table_out = reinterpret_cast<uint32_t*>(static_cast<char*>(fin->workspace) + 4096);
+    args.numel = static_cast<int64_t>(P) * N * d;
+  }
   args.dbg_s = dbg_s;
   args.dbg_p = dbg_p;
   args.dbg_o = dbg_o;
@@ -264,7 +304,8 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   // Persistent grid: one CTA per SM, its groups walking tiles b + g G, + QT G, ...
   args.Tr = static_cast<int32_t>(Tr);
   const bool dbg = dbg_s != nullptr || dbg_p != nullptr || dbg_o != nullptr || dbg_t != nullptr;
-  cudaError_t e = qf::launch_attention(d, bc_eff, nseg, cfg, tq, tk, tv, args, tiles, sms, dbg, stream);
+  cudaError_t e = qf::launch_attention(d, bc_eff, nseg, cfg, tq, tk, tv, args, tiles, sms, dbg,
+                                       fin != nullptr, stream);
   if (e != cudaSuccess) return cuda_fail(e, "attention launch");
   return QFLASH_OK;
 }
@@ -288,7 +329,7 @@ qflash_status attention_host_scales(const int8_t* q, const int8_t* k, const int8
                 static_cast<double>(s_q), static_cast<double>(s_k), shape->head_dim);
   int dev = 0;
   if ((st = check_device(&dev)) != QFLASH_OK) return st;
-  if ((st = launch_common(q, k, v, shape, bc, variant, o, &prm, nullptr, stream)) != QFLASH_OK)
+  if ((st = launch_common(q, k, v, shape, bc, variant, o, &prm, nullptr, stream, nullptr, nullptr)) != QFLASH_OK)
     return st;
   if (s_o) *s_o = s_v;  // s_O = s_V
   return QFLASH_OK;
@@ -371,7 +412,7 @@ qflash_status qflash_attention_int8_dscale(const int8_t* q, const int8_t* k, con
   derive_params_kernel<<<1, 1, 0, s>>>(scales_dev, shape->head_dim, prm);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "derive_params_kernel launch");
-  return launch_common(q, k, v, shape, bc, variant, o, nullptr, prm, s);
+  return launch_common(q, k, v, shape, bc, variant, o, nullptr, prm, s, nullptr, nullptr);
 }
 
 static qflash_status quantize_impl(const void* const* xs, int8_t* const* xqs, float* const* scales,
@@ -476,7 +517,83 @@ qflash_status qflash_attention_int8_prepared(const int8_t* q, const int8_t* k, c
   if ((st = check_device(&dev)) != QFLASH_OK) return st;
   return launch_common(q, k, v, shape, bc, variant, o, nullptr,
                        reinterpret_cast<const qf::IntParams*>(workspace_dev),
-                       reinterpret_cast<cudaStream_t>(stream));
+                       reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr);
+}
+
+qflash_status qflash_attention_dequant_prepared(const int8_t* q, const int8_t* k, const int8_t* v,
+                                                const qflash_attn_shape* shape,
+                                                qflash_variant variant, int8_t* o, float* y,
+                                                const void* workspace_dev, qflash_stream_t stream) {
+  int bc = 0;
+  qflash_status st = validate_shape(shape, &bc);
+  if (st != QFLASH_OK) return st;
+  const int64_t n = static_cast<int64_t>(shape->num_problems) * shape->seq_len * shape->head_dim;
+  if (!y || !aligned16(y)) return fail(QFLASH_ERR_INVALID_ARGUMENT, "y NULL or not 16-byte aligned");
+  if (o != nullptr) {
+    if ((st = validate_qkvo(q, k, v, o, n)) != QFLASH_OK) return st;
+    if (overlaps(reinterpret_cast<const int8_t*>(y), 4 * n, o, n))
+      return fail(QFLASH_ERR_INVALID_ARGUMENT, "y aliases o");
+  } else {
+    if (!q || !k || !v) return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL tensor pointer");
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v))
+      return fail(QFLASH_ERR_INVALID_ARGUMENT, "tensor pointers must be 16-byte aligned");
+  }
+  const int8_t* yb = reinterpret_cast<const int8_t*>(y);
+  if (overlaps(yb, 4 * n, q, n) || overlaps(yb, 4 * n, k, n) || overlaps(yb, 4 * n, v, n))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "y aliases q/k/v");
+  if (!workspace_dev || !aligned16(workspace_dev))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "workspace_dev NULL or misaligned");
+  int dev = 0;
+  if ((st = check_device(&dev)) != QFLASH_OK) return st;
+  return launch_common(q, k, v, shape, bc, variant, o, nullptr,
+                       reinterpret_cast<const qf::IntParams*>(workspace_dev),
+                       reinterpret_cast<cudaStream_t>(stream), y, nullptr);
+}
+
+qflash_status qflash_forward_fused(const float* q, const float* k, const float* v,
+                                   const qflash_attn_shape* shape, qflash_variant variant,
+                                   int8_t* q_q, int8_t* k_q, int8_t* v_q, int8_t* o, float* y,
+                                   float* scales_dev, void* workspace_dev,
+                                   qflash_stream_t stream) {
+  int bc = 0;
+  qflash_status st = validate_shape(shape, &bc);
+  if (st != QFLASH_OK) return st;
+  const int64_t n = static_cast<int64_t>(shape->num_problems) * shape->seq_len * shape->head_dim;
+  if (!q || !k || !v || !y || !scales_dev || !workspace_dev)
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(y) || !aligned16(workspace_dev))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "q, k, v, y and workspace_dev must be 16-byte aligned");
+  const int8_t* outs[2] = {o, reinterpret_cast<const int8_t*>(y)};
+  const int64_t out_n[2] = {n, 4 * n};
+  if (o != nullptr) {
+    if ((st = validate_qkvo(q_q, k_q, v_q, o, n)) != QFLASH_OK) return st;
+  } else {
+    if (!q_q || !k_q || !v_q) return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL int8 buffer");
+    if (!aligned16(q_q) || !aligned16(k_q) || !aligned16(v_q))
+      return fail(QFLASH_ERR_INVALID_ARGUMENT, "int8 buffers must be 16-byte aligned");
+  }
+  const void* ins[3] = {q, k, v};
+  const int8_t* codes[3] = {q_q, k_q, v_q};
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 2; ++j)
+      if (outs[j] && overlaps(outs[j], out_n[j], ins[i], 4 * n))
+        return fail(QFLASH_ERR_INVALID_ARGUMENT, "outputs alias the inputs");
+    if (overlaps(codes[i], n, ins[i], 4 * n) || overlaps(reinterpret_cast<const int8_t*>(y), 4 * n, codes[i], n))
+      return fail(QFLASH_ERR_INVALID_ARGUMENT, "int8 buffers alias inputs or y");
+  }
+  int dev = 0;
+  if ((st = check_device(&dev)) != QFLASH_OK) return st;
+  FusedIn fin;
+  fin.x[0] = q;
+  fin.x[1] = k;
+  fin.x[2] = v;
+  fin.xq[0] = q_q;
+  fin.xq[1] = k_q;
+  fin.xq[2] = v_q;
+  fin.scales = scales_dev;
+  fin.workspace = workspace_dev;
+  return launch_common(q_q, k_q, v_q, shape, bc, variant, o, nullptr, nullptr,
+                       reinterpret_cast<cudaStream_t>(stream), y, &fin);
 }
 
 static qflash_status dequant_impl(const int8_t* x_q, float scale, const float* scale_dev,
@@ -523,7 +640,7 @@ qflash_status qflash_debug_attention(const int8_t* q, const int8_t* k, const int
   int dev = 0;
   if ((st = check_device(&dev)) != QFLASH_OK) return st;
   return launch_common(q, k, v, shape, bc, variant, o, &prm, nullptr,
-                       reinterpret_cast<cudaStream_t>(stream), dbg_s, dbg_p, dbg_o, dbg_t);
+                       reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr, dbg_s, dbg_p, dbg_o, dbg_t);
 }
 
 }  // extern "C"

@@ -40,10 +40,13 @@
 #include "ptx.cuh"
 #include "qflash_common.cuh"
 #include "qflash_params.cuh"
+#include "qflash_quant_elem.cuh"
 
 namespace qf {
 
 constexpr int kQThreads = 256;
+constexpr int kDqTableOffset = 4096;  // workspace bytes of the 256-entry dequant table
+static_assert(kQThreads == 256, "one thread per dequant-table entry");
 constexpr int kQElems = 16;  // elements per thread per iteration
 
 template <typename T>
@@ -147,46 +150,6 @@ __global__ void __launch_bounds__(kQThreads) amax_kernel(QuantTensors t, int64_t
   }
 }
 
-// roundf(fl32(x / s)) exactly (see the header comment).  Fast path: q = RN(x r),
-// rint(q) by the 1.5*2^23 magic-number add (exact for |q| < 2^22, no FRND/F2I),
-// flag `bad` when q is within 2^-14 of a half-integer.
-__device__ __forceinline__ int32_t quant_fast(float x, float r, bool& bad) {
-  const float q = __fmul_rn(x, r);
-  const float t = __fadd_rn(q, 12582912.0f);                    // 1.5 * 2^23
-  const float fi = __fadd_rn(t, -12582912.0f);                  // rint(q), exact
-  bad |= fabsf(__fadd_rn(q, -fi)) >= 0.49993896484375f;         // 0.5 - 2^-14
-  return static_cast<int32_t>(__float_as_uint(t) - 0x4B400000u);  // int(rint(q))
-}
-// the exact definition: IEEE division then round half away from zero (R1, R2)
-__device__ __forceinline__ int32_t quant_exact(float x, float s) {
-  return static_cast<int32_t>(roundf(__fdiv_rn(x, s)));
-}
-__device__ __forceinline__ int32_t quant_one(float x, float s, float r) {
-  bool bad = false;
-  const int32_t v = quant_fast(x, r, bad);
-  return bad ? quant_exact(x, s) : v;
-}
-// 16 elements -> 16 int8 (uint4), one warp-voted exact pass if any lane needs it.
-__device__ __forceinline__ uint4 quant16(const float* f, float s, float r) {
-  int32_t v[16];
-  bool bad = false;
-#pragma unroll
-  for (int k = 0; k < 16; ++k) v[k] = quant_fast(f[k], r, bad);
-  if (__any_sync(__activemask(), bad)) {
-#pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = quant_exact(f[k], s);
-  }
-  uint32_t w[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    uint32_t hi, lo;
-    asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(v[4 * k + 3]), "r"(v[4 * k + 2]));
-    asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(lo) : "r"(v[4 * k + 1]), "r"(v[4 * k]), "r"(hi));
-    w[k] = lo;
-  }
-  return make_uint4(w[0], w[1], w[2], w[3]);
-}
-
 template <typename T>
 __global__ void __launch_bounds__(kQThreads)
     quantize_kernel(QuantTensors t, int64_t numel, IntParams* prm_out, int32_t head_dim) {
@@ -214,6 +177,12 @@ __global__ void __launch_bounds__(kQThreads)
       *prm_out = p;
     }
   }
+  if (blockIdx.x == 0 && ti == 2 && prm_out != nullptr) {
+    // dequantization table of the fused attention epilogue: fl32(s_V * i), i = -128..127
+    // (the same IEEE multiply as dequantize_kernel)
+    reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(prm_out) + kDqTableOffset)[threadIdx.x] =
+        __float_as_uint(__fmul_rn(s, static_cast<float>(static_cast<int>(threadIdx.x) - 128)));
+  }
   const float r = __frcp_rn(s);
   const int64_t nv = numel / kQElems;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -235,6 +204,7 @@ __global__ void __launch_bounds__(kQThreads)
 // (coalesced), keeps them in registers across one grid barrier, and quantizes
 // them with the global scale: one launch, HBM read once, no memset, no atomics.
 constexpr int kFThreads = 256;
+static_assert(kFThreads == 256, "one thread per dequant-table entry");
 constexpr int kFBlocksPerSM = 2;
 
 template <typename T>
@@ -332,6 +302,11 @@ __global__ void __launch_bounds__(kFThreads, kFBlocksPerSM)
     }
   }
   __syncthreads();
+  if (blockIdx.x == 0 && prm_out != nullptr) {
+    // dequantization table of the fused attention epilogue: fl32(s_V * i), i = -128..127
+    reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(prm_out) + kDqTableOffset)[threadIdx.x] =
+        __float_as_uint(__fmul_rn(sc[2], static_cast<float>(static_cast<int>(threadIdx.x) - 128)));
+  }
   if (g == 0) {
     for (int i = 0; i < 3; ++i) *pick_s(t, i) = sc[i];
     if (prm_out != nullptr) {

@@ -1,0 +1,49 @@
+// qflash_quant_elem.cuh -- the per-element exact quantizer of Eq. 2 (readings R1,
+// R2): x^ = sat8(roundf(fl32(x / s))), shared by the quantize kernels
+// (qflash_quant.cu) and the fused-step prologue of the attention kernel.
+#pragma once
+#include <cstdint>
+
+namespace qf {
+
+// roundf(fl32(x / s)) exactly (see the header comment).  Fast path: q = RN(x r),
+// rint(q) by the 1.5*2^23 magic-number add (exact for |q| < 2^22, no FRND/F2I),
+// flag `bad` when q is within 2^-14 of a half-integer.
+__device__ __forceinline__ int32_t quant_fast(float x, float r, bool& bad) {
+  const float q = __fmul_rn(x, r);
+  const float t = __fadd_rn(q, 12582912.0f);                    // 1.5 * 2^23
+  const float fi = __fadd_rn(t, -12582912.0f);                  // rint(q), exact
+  bad |= fabsf(__fadd_rn(q, -fi)) >= 0.49993896484375f;         // 0.5 - 2^-14
+  return static_cast<int32_t>(__float_as_uint(t) - 0x4B400000u);  // int(rint(q))
+}
+// the exact definition: IEEE division then round half away from zero (R1, R2)
+__device__ __forceinline__ int32_t quant_exact(float x, float s) {
+  return static_cast<int32_t>(roundf(__fdiv_rn(x, s)));
+}
+__device__ __forceinline__ int32_t quant_one(float x, float s, float r) {
+  bool bad = false;
+  const int32_t v = quant_fast(x, r, bad);
+  return bad ? quant_exact(x, s) : v;
+}
+// 16 elements -> 16 int8 (uint4), one warp-voted exact pass if any lane needs it.
+__device__ __forceinline__ uint4 quant16(const float* f, float s, float r) {
+  int32_t v[16];
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = quant_fast(f[k], r, bad);
+  if (__any_sync(__activemask(), bad)) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = quant_exact(f[k], s);
+  }
+  uint32_t w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t hi, lo;
+    asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(v[4 * k + 3]), "r"(v[4 * k + 2]));
+    asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(lo) : "r"(v[4 * k + 1]), "r"(v[4 * k]), "r"(hi));
+    w[k] = lo;
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+}  // namespace qf

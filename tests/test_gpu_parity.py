@@ -309,6 +309,40 @@ def test_pipeline_end_to_end_bit_exact(orc):
     assert np.array_equal(out.numpy().view(np.uint32), ref.view(np.uint32))
 
 
+@pytest.mark.parametrize("name,batch", [("A1", 1), ("A3", 8), ("A4", 8), ("A7", 1), ("SwinB-s3", 8)])
+def test_fused_step_and_dequant_epilogue_bit_exact(orc, name, batch):
+    # quantize_prepare -> attention with the DQ step fused into the epilogue (fp32 bits from
+    # the quantizer's table) == oracle dequantize(attention(quantize)) == the 3-stage path
+    q, k, v = gen_workload(name, batch, seed=5)
+    P, N, d = q.shape
+    dq, dk, dv = _dev(q, k, v)
+    fused = qf.QFlashPipeline(P, N, d, mode="two")
+    staged = qf.QFlashPipeline(P, N, d, mode="three")
+    one = qf.QFlashPipeline(P, N, d, mode="fused")
+    y_f = fused(dq, dk, dv).clone()
+    y_s = staged(dq, dk, dv).clone()
+    y_1 = one(dq, dk, dv).clone()
+    o8_1 = torch.empty((P, N, d), dtype=torch.int8, device="cuda")
+    y_1b = qf.qflash_forward_fused(dq, dk, dv, out_int8=o8_1)
+    o8 = torch.empty((P, N, d), dtype=torch.int8, device="cuda")
+    y_b = qf.qflash_attention_dequant_prepared(fused.qkv_q[0], fused.qkv_q[1], fused.qkv_q[2],
+                                               fused.workspace, out_int8=o8)
+    torch.cuda.synchronize()
+    qq, sq = orc.quantize(q)
+    kq, sk = orc.quantize(k)
+    vq, sv = orc.quantize(v)
+    o_ref = orc.attention(qq, kq, vq, sq, sk, block_kv=128)
+    ref = orc.dequantize(o_ref, sv)
+    for y in (y_f, y_s, y_b, y_1, y_1b):
+        assert np.array_equal(y.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    assert np.array_equal(o8.cpu().numpy(), o_ref)
+    assert np.array_equal(o8_1.cpu().numpy(), o_ref)
+    for t, (xq, sx) in enumerate(((qq, sq), (kq, sk), (vq, sv))):  # the prologue's codes and scales
+        assert np.array_equal(one.qkv_q[t].cpu().numpy(), xq)
+        assert one.scales[t].item() == np.float32(sx)
+    assert int(one.workspace[0].item()) == 0
+
+
 def test_sqnr_floor_on_gpu_output(orc):
     from oracle.fp_reference import attention_fp64, sqnr_db
     for name, batch in [("A2", 8), ("A7", 8)]:

@@ -41,7 +41,12 @@ def _functions():
 
 def test_attention_kernels_integer_only_and_tensor_core():
     funcs = _functions()
-    prod = {n: ops for n, ops in funcs.items() if "qflash_attn_kernel" in n and "ELb0E" in n}
+    # template <D, B_c, NSEG, CS, QT, DBG, FQ>: DBG = false, FQ = false are the
+    # integer-only attention kernels; FQ = true adds the Eq. 2 quantizer prologue
+    # (fp32 by definition) in front of the same integer code
+    prod = {n: ops for n, ops in funcs.items() if "qflash_attn_kernel" in n and "ELb0ELb0E" in n}
+    fused = [n for n in funcs if "qflash_attn_kernel" in n and "ELb0ELb1E" in n]
+    assert len(fused) >= 20
     assert len(prod) >= 20, sorted(funcs)[:10]
     for name, ops in prod.items():
         fp = sorted({o for o in ops if o.split(".")[0] in FP_OPCODES})

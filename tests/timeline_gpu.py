@@ -29,7 +29,7 @@ for (P, N, d, variant, label) in [(96, 197, 64, 0, "A3 b8"), (1536, 49, 32, 0, "
     q, k, v = gen_int8_qkv(P, N, d, seed=1)
     dq, dk, dv = (torch.from_numpy(t).cuda() for t in (q, k, v))
     o = torch.empty_like(dq)
-    ts = torch.zeros(128, dtype=torch.int64, device="cuda")
+    ts = torch.zeros(512, dtype=torch.int64, device="cuda")
     sh = _lib.AttnShape(P, N, d, 128)
     for it in range(3):  # warm, then keep the last
         ts.zero_()
@@ -43,3 +43,11 @@ for (P, N, d, variant, label) in [(96, 197, 64, 0, "A3 b8"), (1536, 49, 32, 0, "
     for slot in sorted(NAMES):
         if t[slot]:
             print(f"  {slot:4d} {t[slot] - t0:8d} cyc  {NAMES[slot]}")
+    g = t[128:].reshape(-1, 2)
+    g = g[g[:, 0] > 0]
+    if len(g):
+        g0 = g[:, 0].min()
+        st, en = (g[:, 0] - g0) / 1e3, (g[:, 1] - g0) / 1e3
+        print(f"  CTAs {len(g)}: start spread {st.max():.2f} us, end min/median/max "
+              f"{en.min():.2f}/{np.median(en):.2f}/{en.max():.2f} us, lifetime median "
+              f"{np.median(en - st):.2f} us")
