@@ -233,6 +233,43 @@ class QFlashPipeline:
         return self.out
 
 
+class QFlashHostPipeline:
+    """Serving loop over host (pinned) fp32 batches: each call copies one batch in,
+    runs the whole hot path (QFlashPipeline) and copies the fp32 result back, all
+    asynchronously.  Consecutive batches alternate between `depth` device buffer
+    sets on their own streams, so batch t+1's host->device copy runs while batch t
+    computes and copies out (PCIe is full duplex: H2D and D2H on separate copy
+    engines).  Every batch is complete -- quantized with its own per-tensor
+    scales, attended, dequantized -- once synchronize() returns."""
+
+    def __init__(self, P: int, N: int, d: int, block_kv: int = 128, device="cuda",
+                 mode: str = "fused", depth: int = 2):
+        dev = torch.device(device)
+        self.depth = depth
+        self.pipes = [QFlashPipeline(P, N, d, block_kv=block_kv, device=dev, mode=mode)
+                      for _ in range(depth)]
+        self.dev_in = [[torch.empty((P, N, d), dtype=torch.float32, device=dev) for _ in range(3)]
+                       for _ in range(depth)]
+        self.streams = [torch.cuda.Stream(device=dev) for _ in range(depth)]
+        self.t = 0
+
+    def __call__(self, hq: torch.Tensor, hk: torch.Tensor, hv: torch.Tensor, hout: torch.Tensor):
+        """Enqueue one batch (host tensors; pinned for asynchronous copies)."""
+        i = self.t % self.depth
+        self.t += 1
+        s = self.streams[i]
+        with torch.cuda.stream(s):
+            for dst, src in zip(self.dev_in[i], (hq, hk, hv)):
+                dst.copy_(src, non_blocking=True)
+            out = self.pipes[i](*self.dev_in[i], stream=s)
+            hout.copy_(out, non_blocking=True)
+        return hout
+
+    def synchronize(self):
+        for s in self.streams:
+            s.synchronize()
+
+
 def qflash_forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, block_kv: int = 128):
     """End-to-end QFlash attention on real inputs [P, N, d] (fp32/bf16/f16).
     Host tensors are copied to the current device and the fp32 result copied back."""

@@ -47,6 +47,25 @@ QF_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(a, parity)) {
   }
 }
+// Non-blocking probe of a phase.
+QF_DEV bool mbar_test_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Wait with a sleep between probes: for warps whose wait is usually long and not
+// on the critical path (producers, correction warps), so that their polling does
+// not take issue slots from the computing warps of the same SM sub-partition.
+QF_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_test_wait(a, parity)) __nanosleep(ns);
+}
 
 // ------------------------------------------- programmatic dependent launch
 // A kernel launched with the programmatic-stream-serialization attribute may

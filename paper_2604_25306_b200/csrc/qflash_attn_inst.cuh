@@ -20,14 +20,19 @@ cudaError_t try_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUten
 
 // cfg 0: CS = 4 column splits x QT = 1 (one query tile in flight, 16 softmax warps)
 // cfg 1: CS = 2 x QT = 2 (two ping-ponging query tiles, 8 softmax warps each)
+// cfg 2: CS = 1 x QT = 2 (two ping-ponging query tiles, each a row-owner softmax
+//        warpgroup + a correction warpgroup)
+// cfg 3: CS = 1 x QT = 1
 template <int D, bool DBG, bool FQ = false>
 cudaError_t launch_attention_d(int BC, int nseg, int cfg, const CUtensorMap& tq,
                                const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& args,
                                int64_t tiles, int sms, cudaStream_t stream) {
 #define QF_BC_SEG(bc, ns)                                                                      \
   if (BC == bc && nseg == ns)                                                                  \
-    return cfg == 1 ? try_launch<D, bc, ns, 2, 2, DBG, FQ>(tq, tk, tv, args, tiles, sms, stream) \
-                    : try_launch<D, bc, ns, 4, 1, DBG, FQ>(tq, tk, tv, args, tiles, sms, stream);
+    return cfg == 1   ? try_launch<D, bc, ns, 2, 2, DBG, FQ>(tq, tk, tv, args, tiles, sms, stream) \
+           : cfg == 2 ? try_launch<D, bc, ns, 1, 2, DBG, FQ>(tq, tk, tv, args, tiles, sms, stream) \
+           : cfg == 3 ? try_launch<D, bc, ns, 1, 1, DBG, FQ>(tq, tk, tv, args, tiles, sms, stream) \
+                      : try_launch<D, bc, ns, 4, 1, DBG, FQ>(tq, tk, tv, args, tiles, sms, stream);
   QF_BC_SEG(64, 1) QF_BC_SEG(128, 1) QF_BC_SEG(256, 1)
   QF_BC_SEG(64, 2) QF_BC_SEG(128, 2) QF_BC_SEG(256, 2)
   QF_BC_SEG(64, 4) QF_BC_SEG(128, 4)
@@ -39,7 +44,10 @@ template <int D>
 constexpr bool supported_d(int BC, int nseg, int cfg) {
 #define QF_FITS(bc, ns)                                                                 \
   if (BC == bc && nseg == ns)                                                           \
-    return cfg == 1 ? config_fits<D, bc, ns, 2, 2>() : config_fits<D, bc, ns, 4, 1>();
+    return cfg == 1   ? config_fits<D, bc, ns, 2, 2>()                  \
+           : cfg == 2 ? config_fits<D, bc, ns, 1, 2>()                  \
+           : cfg == 3 ? config_fits<D, bc, ns, 1, 1>()                  \
+                      : config_fits<D, bc, ns, 4, 1>();
   QF_FITS(64, 1) QF_FITS(128, 1) QF_FITS(256, 1)
   QF_FITS(64, 2) QF_FITS(128, 2) QF_FITS(256, 2)
   QF_FITS(64, 4) QF_FITS(128, 4)

@@ -73,6 +73,18 @@ static __device__ const RecipTable g_recip = make_recip_table();
 constexpr int kStages = 2;
 constexpr int kBlockR = 128;
 
+// Sleep (ns) between barrier probes of the waits off the critical path
+// (experiment builds override with -D).
+#ifndef QF_SLEEP_CORR
+#define QF_SLEEP_CORR 128
+#endif
+#ifndef QF_SLEEP_PROD
+#define QF_SLEEP_PROD 256
+#endif
+#ifndef QF_SLEEP_SOFT
+#define QF_SLEEP_SOFT 0
+#endif
+
 __host__ __device__ constexpr uint32_t tmem_cols_pow2(int cols) {
   return cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
 }
@@ -84,7 +96,10 @@ __host__ __device__ constexpr uint32_t swizzle_layout() {
 // ---------------------------------------------------------------- configuration
 template <int D, int BC, int NSEG, int CS, int QT>
 struct Cfg {
-  static constexpr int kNWG = CS * QT;            // softmax warpgroups
+  // CS = 1 ("row owner"): per group one softmax warpgroup (thread = row, all B_c
+  // columns) plus one correction warpgroup (ScaleRelease of O and l, step 11).
+  static constexpr bool kRC = CS == 1;
+  static constexpr int kNWG = kRC ? 2 * QT : CS * QT;  // softmax (+ correction) warpgroups
   static constexpr int kCtl = 4;                  // control warps
   static constexpr int kThreads = 32 * kCtl + 128 * kNWG;
   static constexpr int kGroupThreads = 128 * CS;  // softmax threads of one group
@@ -104,7 +119,7 @@ struct Cfg {
   static constexpr int kK = 2 * NSEG * kQBytes;              // [kStages][NSEG]
   static constexpr int kV = kK + kStages * NSEG * kKVBytes;  // [kStages][NSEG]
   static constexpr int kOnes = QT * kGroupSmem;              // second MN atom of [V | 1]
-  static constexpr int kBarsPerGroup = 2 * kStages + 4 + kNumS + 2;
+  static constexpr int kBarsPerGroup = 2 * kStages + 4 + kNumS + 6;
   static constexpr int kBar = kOnes + BC * D;
   static constexpr int kTmemSlot = kBar + QT * kBarsPerGroup * 8;
   static constexpr int kRed = (kTmemSlot + 16 + 15) / 16 * 16;  // [QT][2][CS][128] int32
@@ -115,16 +130,17 @@ struct Cfg {
   static constexpr int kAlloc = kTotal + 1024;                  // slack for 1024-B alignment
   static_assert(QT * kGroupCols <= 512, "TMEM budget");
   static_assert(NSEG * (BC / 4) <= BC, "P segments must fit in one S buffer");
-  static_assert(kCW == 16 || kCW == 32 || kCW == 64, "columns per thread");
+  static_assert(kCW == 16 || kCW == 32 || kCW == 64 || (kRC && kCW == 128), "columns per thread");
   static_assert(kOW % 8 == 0, "O columns per thread");
 };
 
 template <int D, int BC, int NSEG, int CS, int QT>
 constexpr bool config_fits() {
   return (QT * (((QT == 1 && 2 * BC + D + 16 <= 512) ? 2 : 1) * BC + D + 16) <= 512) &&
-         (BC / CS == 16 || BC / CS == 32 || BC / CS == 64) && ((D / CS) % 8 == 0) &&
+         (BC / CS == 16 || BC / CS == 32 || BC / CS == 64 || (CS == 1 && BC == 128)) &&
+         ((D / CS) % 8 == 0) &&
          (NSEG * (BC / 4) <= BC) &&
-         (QT * (2 * NSEG * kBlockR * D + 2 * kStages * NSEG * BC * D) + BC * D + 64 * 8 +
+         (QT * (2 * NSEG * kBlockR * D + 2 * kStages * NSEG * BC * D) + BC * D + 64 * 10 +
               QT * 2 * CS * 512 + 5120 + 640 + 2048 <=
           227 * 1024);
 }
@@ -139,8 +155,13 @@ struct GroupBars {
   QF_DEV uint64_t* q_full(int b) const { return base + 2 * kStages + b; }
   QF_DEV uint64_t* q_empty(int b) const { return base + 2 * kStages + 2 + b; }
   QF_DEV uint64_t* s_full(int b) const { return base + 2 * kStages + 4 + b; }
-  QF_DEV uint64_t* p_full() const { return base + 2 * kStages + 4 + NUMS; }
-  QF_DEV uint64_t* o_full() const { return base + 2 * kStages + 5 + NUMS; }
+  // p_full(1), alpha_full(b) and rel_full are used by the row-owner roles (CS = 1),
+  // where the softmax warpgroup may run one KV tile ahead of its consumers: the
+  // double-buffered barriers (index it & 1, parity (it >> 1) & 1) never overrun.
+  QF_DEV uint64_t* p_full(int b = 0) const { return base + 2 * kStages + 4 + NUMS + b; }
+  QF_DEV uint64_t* o_full() const { return base + 2 * kStages + 6 + NUMS; }
+  QF_DEV uint64_t* alpha_full(int b) const { return base + 2 * kStages + 7 + NUMS + b; }
+  QF_DEV uint64_t* rel_full() const { return base + 2 * kStages + 9 + NUMS; }
 };
 
 
@@ -418,7 +439,10 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
       const int it = it0 + j;
       const int sb = (C::kNumS == 2) ? (it & 1) : 0;
       const uint32_t tS = tS0 + sb * BC;
-      mbar_wait(gb.s_full(sb), (C::kNumS == 2 ? (it >> 1) : it) & 1);
+      if (QF_SLEEP_SOFT > 0)
+        mbar_wait_sleep(gb.s_full(sb), (C::kNumS == 2 ? (it >> 1) : it) & 1, QF_SLEEP_SOFT);
+      else
+        mbar_wait(gb.s_full(sb), (C::kNumS == 2 ? (it >> 1) : it) & 1);
       tc_fence_after();
       if (dbg && ts_warp && j < 7) QF_TS(40 + 8 * j);
       // columns of this thread that exist in KV tile j (ragged last tile, R16)
@@ -694,6 +718,306 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
   if (!tables_ready) named_bar_arrive(15, C::kNWG * 128 + 32);  // a group without tiles
 }
 
+// ---------------------------------------------------------------- row-owner roles (CS = 1)
+// Softmax warpgroup: thread = query row, all B_c key columns of every KV tile.
+// No cross-warpgroup max exchange; alpha goes to the correction warpgroup
+// through shared memory (alpha_full barrier), P (packed, contiguous per segment)
+// over the S buffer once every S chunk of the row has been read.
+template <int D, int BC, int NSEG, int QT, bool FASTQ>
+__device__ __forceinline__ void softmax_rc_role(const AttnArgs& args, const IntParams& prm,
+                                                uint32_t tmem_group,
+                                                GroupBars<Cfg<D, BC, NSEG, 1, QT>::kNumS> gb,
+                                                uint32_t alpha_buf, int g, int quarter, int lane) {
+  using C = Cfg<D, BC, NSEG, 1, QT>;
+  constexpr int NH = BC / 32;  // 32-column chunks
+  const int N = args.N;
+  const int Tc = args.Tc;
+  const int row = quarter * 32 + lane;
+  const uint32_t tS0 = tmem_group + (static_cast<uint32_t>(quarter * 32) << 16);
+  const uint32_t s_inv = static_cast<uint32_t>(prm.s_inv);
+  const uint32_t one = static_cast<uint32_t>(prm.one);
+  TileIter<NSEG> ti;
+  ti.init(args, blockIdx.x + g * gridDim.x);
+  int it0 = 0;
+  for (; ti.valid(args); ti.next(args)) {
+    const bool live = row < ti.rows;
+    const bool warp_live = quarter * 32 < ti.rows;
+    int seg = 0;
+    if constexpr (NSEG > 1) {
+      const int x = ti.off + row;
+      seg = (x >= N ? 1 : 0);
+      if constexpr (NSEG > 2) seg += (x >= 2 * N ? 1 : 0) + (x >= 3 * N ? 1 : 0);
+    }
+    const int nseg = ti.nseg;
+    int32_t m = -(1 << 21);  // m^(0) = -2^21
+    for (int j = 0; j < Tc; ++j) {
+      const int it = it0 + j;
+      const int sb = (C::kNumS == 2) ? (it & 1) : 0;
+      const uint32_t tS = tS0 + sb * BC;
+      if (QF_SLEEP_SOFT > 0)
+        mbar_wait_sleep(gb.s_full(sb), (C::kNumS == 2 ? (it >> 1) : it) & 1, QF_SLEEP_SOFT);
+      else
+        mbar_wait(gb.s_full(sb), (C::kNumS == 2 ? (it >> 1) : it) & 1);
+      tc_fence_after();
+      const int valid = min(BC, N - j * BC);  // ragged last KV tile (R16), warp-uniform
+      // (2)(3) row max over the valid columns, two 32-column chunks per TMEM wait
+      int32_t tmax = INT32_MIN;
+      if (warp_live) {
+#pragma unroll
+        for (int h2 = 0; h2 < NH; h2 += 2) {
+          uint32_t sc[64];
+          tmem_ld32(tS + 32 * h2, *reinterpret_cast<uint32_t(*)[32]>(sc));
+          if (h2 + 1 < NH) tmem_ld32(tS + 32 * h2 + 32, *reinterpret_cast<uint32_t(*)[32]>(sc + 32));
+          tmem_wait_ld();
+          const int hv = valid - 32 * h2;
+          constexpr int W = NH >= 2 ? 64 : 32;
+          if (hv >= W) {
+#pragma unroll
+            for (int e = 0; e < W; ++e) tmax = max(tmax, static_cast<int32_t>(sc[e]));
+          } else {
+#pragma unroll
+            for (int k = 0; k < W / 8; ++k) {
+              if (8 * k + 8 <= hv) {
+#pragma unroll
+                for (int e = 8 * k; e < 8 * k + 8; ++e) tmax = max(tmax, static_cast<int32_t>(sc[e]));
+              } else if (8 * k < hv) {
+#pragma unroll
+                for (int e = 8 * k; e < 8 * k + 8; ++e)
+                  if (e < hv) tmax = max(tmax, static_cast<int32_t>(sc[e]));
+              }
+            }
+          }
+        }
+      }
+      const int32_t m_new = max(m, tmax);
+      // (4) alpha = ShiftExp2(m_old - m_new), handed to the correction warpgroup
+      const int32_t alpha = shift_exp2<FASTQ>(m - m_new, prm);
+      sts32(alpha_buf + static_cast<uint32_t>(((it & 1) * 128 + row) * 4), alpha);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(gb.alpha_full(it & 1));
+      // (5)(6) P = Requant(ShiftExp2(S - m_new)), chunk by chunk (S reloaded)
+      const uint32_t mu = static_cast<uint32_t>(m_new);
+      const uint32_t nmu = static_cast<uint32_t>(-m_new);
+      const uint32_t c3 = s_inv - mu;
+      uint32_t pk[BC / 4];
+#pragma unroll
+      for (int e = 0; e < BC / 4; ++e) pk[e] = 0u;
+      if (warp_live) {
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const int hv = valid - 32 * h;
+          if (hv > 0) {
+            uint32_t sc[32];
+            tmem_ld32(tS + 32 * h, sc);
+            tmem_wait_ld();
+            uint32_t* pw = pk + 8 * h;
+            if (hv >= 32) {
+#pragma unroll
+              for (int e = 0; e < 32; e += 4)
+                pw[e / 4] = pack4_sat_s8(
+                    shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e]), mu, nmu, c3, one, prm),
+                    shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 1]), mu, nmu, c3, one, prm),
+                    shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e + 2]), mu, nmu, c3, one, prm),
+                    shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 3]), mu, nmu, c3, one, prm));
+            } else {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                if (8 * k + 8 <= hv) {
+#pragma unroll
+                  for (int e = 8 * k; e < 8 * k + 8; e += 4)
+                    pw[e / 4] = pack4_sat_s8(
+                        shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e]), mu, nmu, c3, one, prm),
+                        shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 1]), mu, nmu, c3, one, prm),
+                        shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e + 2]), mu, nmu, c3, one, prm),
+                        shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 3]), mu, nmu, c3, one, prm));
+                } else if (8 * k < hv) {
+#pragma unroll
+                  for (int e = 8 * k; e < 8 * k + 8; e += 4) {
+                    int32_t pv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                      const int32_t x = shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e + u]), mu, nmu, c3, one, prm);
+                      pv[u] = (e + u < hv) ? x : 0;
+                    }
+                    pw[e / 4] = pack4_sat_s8(pv[0], pv[1], pv[2], pv[3]);
+                  }
+                }
+              }
+            }
+          }
+        }
+      }
+      // every S chunk of this row is read: P of segment s -> columns [s B_c/4, +B_c/4)
+      if (nseg == 1) {
+        tmem_st<BC / 4>(tS, pk);
+      } else {
+#pragma unroll
+        for (int sg = 0; sg < NSEG; ++sg) {
+          if (sg < nseg) {
+            uint32_t z[BC / 4];
+#pragma unroll
+            for (int e = 0; e < BC / 4; ++e) z[e] = (seg == sg && live) ? pk[e] : 0u;
+            tmem_st<BC / 4>(tS + sg * (BC / 4), z);
+          }
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(gb.p_full(it & 1));
+      m = m_new;
+    }
+    it0 += Tc;
+  }
+}
+
+// Correction warpgroup: thread = query row.  Per KV tile j >= 1 it releases the
+// row's O (all d columns) and l with the alpha of tile j once P V_{j-1} has
+// landed (Eq. 14, R10) -- concurrently with the softmax warpgroup's P work --
+// then arrives on rel_full, which the MMA warp needs (with p_full) before
+// P V_j.  After the last KV tile: step (11) and the stores (int8 and/or the
+// fused dequantization), before the next tile's first rel_full arrival.
+template <int D, int BC, int NSEG, int QT, bool FQ>
+__device__ __forceinline__ void correction_role(const AttnArgs& args, const IntParams& prm,
+                                                uint32_t tmem_group,
+                                                GroupBars<Cfg<D, BC, NSEG, 1, QT>::kNumS> gb,
+                                                uint32_t alpha_buf, const uint32_t* recip, int g,
+                                                int quarter, int lane) {
+  using C = Cfg<D, BC, NSEG, 1, QT>;
+  constexpr int OH = D < 32 ? D : 32;  // O columns per TMEM round trip
+  const int N = args.N;
+  const int Tc = args.Tc;
+  const int row = quarter * 32 + lane;
+  const uint32_t tO = tmem_group + (static_cast<uint32_t>(quarter * 32) << 16) + C::kNumS * BC;
+  const int sinv_log2 = 31 - __clz(prm.s_inv);
+  int32_t rel_lthr;
+  {
+    const uint64_t mg = (static_cast<uint64_t>(prm.rel_magic_hi) << 32) | prm.rel_magic_lo;
+    const uint64_t A = __umul64hi(0xFFFFFFFFull, mg) >> prm.rel_shift;
+    const int64_t t = (static_cast<int64_t>(A) - static_cast<int64_t>(prm.s_inv)) / 384 - 2 * Tc;
+    rel_lthr = t < 0 ? -1 : (t > 0x7FFFFFFF ? 0x7FFFFFFF : static_cast<int32_t>(t));
+  }
+  bool tables_ready = false;
+  TileIter<NSEG> ti;
+  ti.init(args, blockIdx.x + g * gridDim.x);
+  int it0 = 0;
+  for (; ti.valid(args); ti.next(args)) {
+    const bool live = row < ti.rows;
+    const bool warp_live = quarter * 32 < ti.rows;
+    for (int j = 0; j < Tc; ++j) {
+      const int it = it0 + j;
+      mbar_wait_sleep(gb.alpha_full(it & 1), (it >> 1) & 1, QF_SLEEP_CORR);
+      const int32_t alpha = lds32(alpha_buf + static_cast<uint32_t>(((it & 1) * 128 + row) * 4));
+      if (j > 0) {
+        mbar_wait_sleep(gb.o_full(), (it - 1) & 1, QF_SLEEP_CORR);
+        tc_fence_after();
+        if (warp_live && __any_sync(0xffffffffu, alpha != prm.s_inv)) {
+          uint32_t lcol;
+          uint32_t o[OH];
+          tmem_ld1(tO + D, lcol);
+          if constexpr (OH == 32) tmem_ld32(tO, *reinterpret_cast<uint32_t(*)[32]>(o));
+          else tmem_ld<OH>(tO, o);
+          tmem_wait_ld();
+          if (__all_sync(0xffffffffu, static_cast<int32_t>(lcol) <= rel_lthr)) {
+            const uint32_t bound = 128u * (lcol + 2u * static_cast<uint32_t>(Tc));
+            const BiasedRelease br = make_biased_release(alpha, bound, prm, sinv_log2);
+#pragma unroll
+            for (int h = 0; h < D / OH; ++h) {
+              if (h > 0) {
+                if constexpr (OH == 32) tmem_ld32(tO + OH * h, *reinterpret_cast<uint32_t(*)[32]>(o));
+                else tmem_ld<OH>(tO + OH * h, o);
+                tmem_wait_ld();
+              }
+#pragma unroll
+              for (int e = 0; e < OH; ++e) o[e] = br.apply(o[e]);
+              tmem_st<OH>(tO + OH * h, o);
+            }
+            tmem_st1(tO + D, br.apply(lcol));
+          } else {
+            const int32_t A = release_factor(alpha, prm);
+#pragma unroll
+            for (int h = 0; h < D / OH; ++h) {
+              if (h > 0) {
+                if constexpr (OH == 32) tmem_ld32(tO + OH * h, *reinterpret_cast<uint32_t(*)[32]>(o));
+                else tmem_ld<OH>(tO + OH * h, o);
+                tmem_wait_ld();
+              }
+#pragma unroll
+              for (int e = 0; e < OH; ++e)
+                o[e] = static_cast<uint32_t>(scale_release(static_cast<int32_t>(o[e]), alpha, A, prm.s_inv));
+              tmem_st<OH>(tO + OH * h, o);
+            }
+            tmem_st1(tO + D, static_cast<uint32_t>(scale_release(static_cast<int32_t>(lcol), alpha, A, prm.s_inv)));
+          }
+          tmem_wait_st();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(gb.rel_full());
+    }
+    // (11) O_i = floor(O / l), saturated (R14), stores
+    mbar_wait(gb.o_full(), (it0 + Tc - 1) & 1);
+    tc_fence_after();
+    if (!tables_ready) {
+      named_bar_sync(15, C::kNWG * 128 + 32);
+      tables_ready = true;
+    }
+    if (warp_live) {
+      uint32_t lraw;
+      tmem_ld1(tO + D, lraw);
+      tmem_wait_ld();
+      const Recip rc = make_recip(static_cast<int32_t>(lraw), recip);
+      const int64_t orow = static_cast<int64_t>(ti.problem) * N + ti.off + row;
+#pragma unroll
+      for (int h = 0; h < D / OH; ++h) {
+        uint32_t o[OH];
+        if constexpr (OH == 32) tmem_ld32(tO + OH * h, *reinterpret_cast<uint32_t(*)[32]>(o));
+        else tmem_ld<OH>(tO + OH * h, o);
+        tmem_wait_ld();
+        if (live) {
+          bool bad = false;
+          uint32_t w[OH / 4];
+#pragma unroll
+          for (int e = 0; e < OH; e += 4)
+            w[e / 4] = pack4_sat_s8(floor_div(static_cast<int32_t>(o[e]), rc, bad),
+                                    floor_div(static_cast<int32_t>(o[e + 1]), rc, bad),
+                                    floor_div(static_cast<int32_t>(o[e + 2]), rc, bad),
+                                    floor_div(static_cast<int32_t>(o[e + 3]), rc, bad));
+          if (bad) {
+#pragma unroll
+            for (int e = 0; e < OH; e += 4)
+              w[e / 4] = pack4_sat_s8(floor_div_exact(static_cast<int32_t>(o[e]), rc.l),
+                                      floor_div_exact(static_cast<int32_t>(o[e + 1]), rc.l),
+                                      floor_div_exact(static_cast<int32_t>(o[e + 2]), rc.l),
+                                      floor_div_exact(static_cast<int32_t>(o[e + 3]), rc.l));
+          }
+          if (args.out != nullptr) {
+            int8_t* dst = args.out + orow * D + OH * h;
+#pragma unroll
+            for (int e = 0; e < OH / 16; ++e)
+              reinterpret_cast<uint4*>(dst)[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+          }
+          if (args.out_f32 != nullptr) {
+            const uint32_t dqt = smem_u32(recip + 1024);
+            uint32_t* ydst = reinterpret_cast<uint32_t*>(args.out_f32 + orow * D + OH * h);
+#pragma unroll
+            for (int e = 0; e < OH / 4; ++e) {
+              uint32_t y4[4];
+#pragma unroll
+              for (int b = 0; b < 4; ++b)
+                y4[b] = static_cast<uint32_t>(lds32(dqt + ((((w[e] >> (8 * b)) & 0xFFu) ^ 0x80u) << 2)));
+              reinterpret_cast<uint4*>(ydst)[e] = make_uint4(y4[0], y4[1], y4[2], y4[3]);
+            }
+          }
+        }
+      }
+    }
+    it0 += Tc;
+  }
+  if (!tables_ready) named_bar_arrive(15, C::kNWG * 128 + 32);
+}
+
 // ---------------------------------------------------------------- fused-step prologue
 // Q0 for the fused step (FQ): every thread of the cooperative grid takes part.
 //  1. per-tensor amax over a grid-stride share of Q, K, V (fp32, one FMNMX per
@@ -798,7 +1122,15 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   // 2. global scales (every CTA, identical): s = fl32(amax / 127), R3 for zeros
   if (warp < 3) {
     float b = 0.f;
-    for (int j = lane; j < static_cast<int>(gridDim.x); j += 32) b = fmaxf(b, __ldcg(&a.partial[warp * gridDim.x + j]));
+    float pv[5];  // gridDim.x <= 160: every partial load in flight at once
+#pragma unroll
+    for (int u = 0; u < 5; ++u) {
+      const int j = lane + 32 * u;
+      pv[u] = j < static_cast<int>(gridDim.x) ? __ldcg(&a.partial[warp * gridDim.x + j]) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 5; ++u) b = fmaxf(b, pv[u]);
+    for (int j = lane + 160; j < static_cast<int>(gridDim.x); j += 32) b = fmaxf(b, __ldcg(&a.partial[warp * gridDim.x + j]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
     if (lane == 0) {
@@ -909,8 +1241,12 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
         mbar_init(gb.q_empty(b), 1);
       }
       for (int b = 0; b < C::kNumS; ++b) mbar_init(gb.s_full(b), 1);
-      mbar_init(gb.p_full(), C::kGroupThreads / 32);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(gb.p_full(b), C::kGroupThreads / 32);
+        mbar_init(gb.alpha_full(b), 4);
+      }
       mbar_init(gb.o_full(), 1);
+      mbar_init(gb.rel_full(), 4);
     }
     fence_barrier_init();
   }
@@ -969,7 +1305,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
         const int qb = ti.i & 1;
         if (ti.i >= 2) {
           if (!(ok = status_ok())) break;
-          mbar_wait(gb.q_empty(qb), ((ti.i >> 1) - 1) & 1);
+          mbar_wait_sleep(gb.q_empty(qb), ((ti.i >> 1) - 1) & 1, QF_SLEEP_PROD);
         }
         mbar_arrive_expect_tx(gb.q_full(qb), ti.nseg * C::kQBytes);
         // segment s: rows of problem + s land at their tile rows, every other
@@ -982,7 +1318,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
           const int st = it % kStages;
           if (it >= kStages) {
             if (!(ok = status_ok())) break;
-            mbar_wait(gb.kv_empty(st), ((it / kStages) - 1) & 1);
+            mbar_wait_sleep(gb.kv_empty(st), ((it / kStages) - 1) & 1, QF_SLEEP_PROD);
           }
           mbar_arrive_expect_tx(gb.kv_full(st), ti.nseg * 2 * C::kKVBytes);
           for (int s = 0; s < ti.nseg; ++s) {
@@ -1077,7 +1413,12 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
             const int st = it % kStages;
             const int sb = (C::kNumS == 2) ? (it & 1) : 0;
             // (8) O (+)= sum_s P_s [V_{s,j} | 1] : M=128, N=D+16, K=BC in steps of 32 keys.
-            mbar_wait(gb.p_full(), it & 1);
+            if constexpr (C::kRC) {
+              mbar_wait(gb.p_full(it & 1), (it >> 1) & 1);
+              mbar_wait(gb.rel_full(), it & 1);  // O released / consumed
+            } else {
+              mbar_wait(gb.p_full(), it & 1);
+            }
             tc_fence_after();
             if (ti.i == 0 && blockIdx.x == 0 && g == 0 && j < 7) QF_TS(4 + 4 * j);
             for (int s = 0; s < nseg; ++s) {
@@ -1107,6 +1448,21 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
     } else {
       const int sw = warp - C::kCtl;
       const int wg = sw >> 2;
+      if constexpr (C::kRC) {
+        const int g = wg >> 1;
+        const Bars gb{bars + g * C::kBarsPerGroup};
+        const uint32_t abuf = smem_u32(smem + C::kRed) + static_cast<uint32_t>(g * 2 * 128 * 4);
+        const uint32_t tG = tmem_base + g * C::kGroupCols;
+        const bool fastq = prm.q_shift == 0 &&
+                           static_cast<uint64_t>(prm.s_inv) * static_cast<uint64_t>(prm.m_p) < (1ull << 32);
+        if ((wg & 1) == 0) {
+          named_bar_arrive(15, C::kNWG * 128 + 32);  // softmax threads never read the tables
+          if (fastq) softmax_rc_role<D, BC, NSEG, QT, true>(args, prm, tG, gb, abuf, g, warp & 3, lane);
+          else softmax_rc_role<D, BC, NSEG, QT, false>(args, prm, tG, gb, abuf, g, warp & 3, lane);
+        } else {
+          correction_role<D, BC, NSEG, QT, FQ>(args, prm, tG, gb, abuf, recip, g, warp & 3, lane);
+        }
+      } else {
       const int g = wg / CS;
       const int c = wg - g * CS;
       const Bars gb{bars + g * C::kBarsPerGroup};
@@ -1116,6 +1472,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
         softmax_role<D, BC, NSEG, CS, QT, DBG, true>(args, prm, tG, gb, red_group, recip, g, c, warp & 3, lane);
       else
         softmax_role<D, BC, NSEG, CS, QT, DBG, false>(args, prm, tG, gb, red_group, recip, g, c, warp & 3, lane);
+      }
     }
   }
 

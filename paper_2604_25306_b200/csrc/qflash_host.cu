@@ -254,16 +254,25 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   }
   const int nseg = packed ? nseg_tpl : 1;
   const int64_t tiles = packed ? tiles_packed : tiles_generic;
-  // Kernel configuration (qflash_attn_kernel.cuh): cfg 1 (two ping-ponging
-  // query tiles per CTA, 2 column splits) when there is more than one wave of
-  // tiles and it fits TMEM / shared memory; else cfg 0 (one tile, 4 column
-  // splits: lowest latency per tile).  QFLASH_ATTN_CFG=0/1 overrides.
+  // Kernel configuration (qflash_attn_inst.cuh): with more than one wave of
+  // tiles, cfg 2 (two ping-ponging query tiles, row-owner softmax + correction
+  // warpgroups) or cfg 1 (two tiles, 2 column splits) where it fits TMEM /
+  // shared memory; else cfg 0 (one tile, 4 column splits: lowest latency per
+  // tile).  QFLASH_ATTN_CFG=0..3 overrides.
   static int cfg_env = -2;
   if (cfg_env == -2) {
     const char* env = getenv("QFLASH_ATTN_CFG");
-    cfg_env = (env != nullptr && (env[0] == '0' || env[0] == '1')) ? env[0] - '0' : -1;
+    cfg_env = (env != nullptr && env[0] >= '0' && env[0] <= '3') ? env[0] - '0' : -1;
   }
-  int cfg = (tiles > sms && qf::attention_supported(d, bc_eff, nseg, 1)) ? 1 : 0;
+  // Measured (profiles/r1_cfg_ab.txt): multi-wave with several KV tiles -> cfg 1
+  // (L14 b64: 848 vs 938 us for cfg 2); one KV tile (Swin windows) -> cfg 2.
+  const int Tc_host = (N + bc_eff - 1) / bc_eff;
+  int cfg = 0;
+  if (tiles > sms) {
+    const int pref[2] = {Tc_host == 1 ? 2 : 1, Tc_host == 1 ? 1 : 2};
+    for (int c : pref)
+      if (cfg == 0 && qf::attention_supported(d, bc_eff, nseg, c)) cfg = c;
+  }
   if (cfg_env >= 0 && qf::attention_supported(d, bc_eff, nseg, cfg_env)) cfg = cfg_env;
   if (!qf::attention_supported(d, bc_eff, nseg, cfg))
     return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "no kernel configuration for d=%d block=%d", d, bc_eff);

@@ -80,9 +80,8 @@ __host__ __device__ inline int derive_core(float s_q, float s_k, int32_t d, qf::
       q_shift = 0;
     } else {
       const int L = ceil_log2(D);
-      const int sh = L > 7 ? L - 7 : 0;
-      const u128 num = (u128(1) << (32 + sh));
-      const u128 mm = (num + D - 1) / D;
+      const int sh = L > 7 ? L - 7 : 0;           // L <= 25: 2^(32 + sh) < 2^51
+      const uint64_t mm = ((uint64_t(1) << (32 + sh)) + D - 1) / D;
       q_magic = static_cast<uint32_t>(mm);
       q_shift = sh;
     }
@@ -95,10 +94,16 @@ __host__ __device__ inline int derive_core(float s_q, float s_k, int32_t d, qf::
   uint64_t rel_magic;
   int32_t rel_shift;
   {
+    // ceil(2^(64 + sh) / D) by two 64-bit long-division steps (exact):
+    // 2^(32 + sh) = q1 D + r1, then r1 2^32 = q2 D + r2 (r1 < D < 2^25).
     const int L = ceil_log2(D);
     const int sh = L > 8 ? L - 8 : 0;
-    const u128 num = (u128(1) << (64 + sh));
-    rel_magic = static_cast<uint64_t>((num + D - 1) / D);
+    const uint64_t A = uint64_t(1) << (32 + sh);
+    const uint64_t q1 = A / D;
+    const uint64_t r1 = A - q1 * D;
+    const uint64_t q2 = (r1 << 32) / D;
+    const uint64_t r2 = (r1 << 32) - q2 * D;
+    rel_magic = (q1 << 32) + q2 + (r2 != 0 ? 1 : 0);
     rel_shift = sh;
   }
   if (o) {

@@ -43,9 +43,10 @@ def _config_fits(D, BC, NSEG, CS, QT):
     """Mirror of config_fits<> in qflash_attn_kernel.cuh (TMEM columns, columns per
     thread, shared memory)."""
     nums = 2 if (QT == 1 and 2 * BC + D + 16 <= 512) else 1
-    smem = (QT * (2 * NSEG * 128 * D + 2 * 2 * NSEG * BC * D) + BC * D + 64 * 8
-            + QT * 2 * CS * 512 + 4096 + 2048)
-    return (QT * (nums * BC + D + 16) <= 512 and BC // CS in (16, 32, 64) and (D // CS) % 8 == 0
+    smem = (QT * (2 * NSEG * 128 * D + 2 * 2 * NSEG * BC * D) + BC * D + 64 * 10
+            + QT * 2 * CS * 512 + 5120 + 640 + 2048)
+    cw_ok = BC // CS in (16, 32, 64) or (CS == 1 and BC == 128)
+    return (QT * (nums * BC + D + 16) <= 512 and cw_ok and (D // CS) % 8 == 0
             and NSEG * (BC // 4) <= BC and smem <= 227 * 1024)
 
 
@@ -59,7 +60,7 @@ def _packable(N, d, bkv):
     if seg > 4:
         return False
     nseg = 2 if seg <= 2 else 4
-    return _config_fits(d, bc, nseg, 4, 1) or _config_fits(d, bc, nseg, 2, 2)
+    return any(_config_fits(d, bc, nseg, cs, qt) for cs, qt in ((4, 1), (2, 2), (1, 2), (1, 1)))
 
 
 @pytest.mark.parametrize("N", N_GRID)
@@ -380,3 +381,21 @@ def test_validation_errors():
     q1 = torch.zeros((4, 20, 64), dtype=torch.int8, device="cuda")
     with pytest.raises(_lib.QFlashError):
         qf.qflash_attention_int8(q1, q1, q1, 0.05, 0.05, 0.05, variant="packed")  # N < 43
+
+
+def test_host_pipeline_overlapped_batches(orc):
+    # the serving loop: pinned host batches, two buffer sets / streams overlapping
+    # copies and compute; every batch's output equals the oracle's
+    batches = [gen_workload("A2", 1, seed=s) for s in (21, 22, 23)]
+    P, N, d = batches[0][0].shape
+    hp = qf.QFlashHostPipeline(P, N, d)
+    outs = [torch.empty((P, N, d), dtype=torch.float32).pin_memory() for _ in batches]
+    for (q, k, v), o in zip(batches, outs):
+        hp(*(torch.from_numpy(x).pin_memory() for x in (q, k, v)), o)
+    hp.synchronize()
+    for (q, k, v), o in zip(batches, outs):
+        qq, sq = orc.quantize(q)
+        kq, sk = orc.quantize(k)
+        vq, sv = orc.quantize(v)
+        ref = orc.dequantize(orc.attention(qq, kq, vq, sq, sk), sv)
+        assert np.array_equal(o.numpy().view(np.uint32), ref.view(np.uint32))
