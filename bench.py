@@ -131,6 +131,8 @@ def algorithmic(P, N, d):
         "int8_ops": 4.0 * N * N * d * P,       # QK^T + PV, 2 ops per MAC
         "score_elems": float(N) * N * P,       # units of the integer softmax
         "attn_bytes": 4.0 * N * d * P,         # read Q, K, V once, write O once (int8)
+        "attn_dq_bytes": 7.0 * N * d * P,      # int8 Q, K, V in, fp32 O out (fused dequantize)
+        "fused_step_bytes": 16.0 * N * d * P,  # fp32 Q, K, V in, fp32 O out (codes stay in L2)
         "step_bytes": 3 * 4.0 * N * d * P + 3 * N * d * P + 2 * N * d * P + 4.0 * N * d * P,
     }
 
@@ -381,6 +383,7 @@ def main():
     attn_share = attn_ms / ms_per_step
     launches_per_step = pipes[0].launches()
 
+    kbytes = alg["fused_step_bytes"] if one_launch else alg["attn_dq_bytes"]
     pk = peaks()
     sm_clk_ghz = (pk.get("sm_max_mhz") or 1965.0) / 1e3
     alu_peak = SMS * INT32_LANES * sm_clk_ghz * 1e9 / 1e12      # T int32 ops/s
@@ -400,14 +403,17 @@ def main():
                    "peak_tops": int8_peak_tops,
                    "frac": alg["int8_ops"] / (attn_ms * 1e-3) / 1e12 / int8_peak_tops,
                    "peak_source": "measured bf16 burst x 2 (int8/bf16 nominal ratio)"},
-        "hbm": {"achieved_gbs": alg["attn_bytes"] / (attn_ms * 1e-3) / 1e9,
+        "hbm": {"achieved_gbs": kbytes / (attn_ms * 1e-3) / 1e9,
                 "peak_gbs": pk.get("hbm_gbs"),
-                "frac": alg["attn_bytes"] / (attn_ms * 1e-3) / 1e9 / pk.get("hbm_gbs", 6452.5)},
+                "frac": kbytes / (attn_ms * 1e-3) / 1e9 / pk.get("hbm_gbs", 6452.5),
+                "bytes_per_launch": kbytes,
+                "per_unit": "16 N d B per problem (fp32 Q, K, V in + fp32 O out)" if one_launch
+                            else "7 N d B per problem (int8 Q, K, V in + fp32 O out)"},
     }
     traffic_file = os.path.join(ROOT, "profiles", "attn_traffic.json")
     if os.path.exists(traffic_file):
         try:
-            tj = json.load(open(traffic_file)).get(f"{name}_b{batch}")
+            tj = json.load(open(traffic_file)).get(f"{name}_b{batch}" + ("_fused" if one_launch else ""))
             if tj:
                 roofline["traffic"] = tj
         except Exception:
