@@ -1067,9 +1067,14 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   namespace cg = cooperative_groups;
   constexpr int kVR = 4;  // register-resident 16-B vectors per tensor and thread
   QF_FQ_TS(a, 0);
+  // Warp 0 moves no data: its lane 0 derives the integer constants (~1-2 us of
+  // fp64 / 64-bit integer work) while warps 1.. quantize, off the critical path.
   const int nthr_blk = blockDim.x;
-  const int64_t nthr = static_cast<int64_t>(gridDim.x) * nthr_blk;
-  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * nthr_blk + threadIdx.x;
+  const int ndata_blk = nthr_blk - 32;
+  const bool data_thread = threadIdx.x >= 32;
+  const int64_t nthr = static_cast<int64_t>(gridDim.x) * ndata_blk;
+  const int64_t gtid = data_thread ? static_cast<int64_t>(blockIdx.x) * ndata_blk + threadIdx.x - 32
+                                   : INT64_MAX / 2;
   const int64_t nvec = a.numel >> 2;
   const bool resident = nvec <= kVR * nthr;  // the whole share stays in registers
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1528,11 +1533,23 @@ cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CU
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   if constexpr (FQ) {
-    // fused step: grid barriers in the quantize prologue need every CTA resident
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    // fused step: grid barriers in the quantize prologue need every CTA resident;
+    // programmatic serialization lets the next step's grid be launched (and run its
+    // setup) while this one drains -- griddep_wait() precedes every global access
+    cudaLaunchAttribute a2[2];
+    a2[0].id = cudaLaunchAttributeCooperative;
+    a2[0].val.cooperative = 1;
+    a2[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a2[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = a2;
+    cfg.numAttrs = (pdl_mask() & 8) ? 2 : 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, args);
+    if (e != cudaSuccess && cfg.numAttrs == 2) {
+      (void)cudaGetLastError();
+      cfg.numAttrs = 1;
+      e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, args);
+    }
+    return e;
   } else {
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddep_wait)
     attr[0].val.programmaticStreamSerializationAllowed = 1;

@@ -26,7 +26,7 @@ struct IntParams {
 };
 static_assert(sizeof(IntParams) == 72, "IntParams layout");
 
-constexpr int kPdlDefault = 7;
+constexpr int kPdlDefault = 15;
 
 struct AttnArgs {
   int32_t N;        // sequence length
@@ -67,12 +67,13 @@ struct QuantTensors {
 };
 
 // Programmatic dependent launch per kernel (bit 0 attention, bit 1 dequantize,
-// bit 2 second quantize pass); QFLASH_PDL=<mask> overrides the default (A/B).
+// bit 2 second quantize pass, bit 3 fused step); QFLASH_PDL=<mask> overrides the
+// default (A/B).
 inline int pdl_mask() {
   static int m = -1;
   if (m < 0) {
     const char* e = getenv("QFLASH_PDL");
-    m = (e != nullptr && e[0] >= '0' && e[0] <= '7') ? e[0] - '0' : kPdlDefault;
+    m = (e != nullptr) ? static_cast<int>(strtol(e, nullptr, 10)) : kPdlDefault;
   }
   return m;
 }
