@@ -58,7 +58,8 @@ typedef enum { QFLASH_F32 = 0, QFLASH_BF16 = 1, QFLASH_F16 = 2 } qflash_dtype;
  * x: device, numel elements of `dtype`, contiguous.  x_q: device int8[numel].
  * scale_dev: device float* receiving s (may be NULL).  scale_host: host float*
  * receiving s (may be NULL; if set the call synchronizes `stream`).  At least
- * one scale pointer is required.  numel == 0 gives s = 1/127.  A non-finite
+ * one scale pointer is required.  numel == 0 gives s = 1/127 (x and x_q may then
+ * be NULL).  A non-finite
  * input yields a non-finite s (rejected later by qflash_attention_int8).
  * ------------------------------------------------------------------------ */
 QFLASH_API qflash_status qflash_quantize_per_tensor(const void* x, qflash_dtype dtype, int64_t numel,

@@ -432,7 +432,10 @@ static qflash_status quantize_impl(const void* const* xs, int8_t* const* xqs, fl
   if (dtype != QFLASH_F32 && dtype != QFLASH_BF16 && dtype != QFLASH_F16)
     return fail(QFLASH_ERR_INVALID_ARGUMENT, "unknown dtype %d", static_cast<int>(dtype));
   for (int i = 0; i < nt; ++i) {
-    if (!xs[i] || !xqs[i] || !scales[i]) return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL pointer");
+    // an empty tensor (numel == 0) may pass NULL data pointers: no codes are
+    // written and its scale is 1/127 (amax of the empty set is 0, reading R3)
+    if ((numel > 0 && (!xs[i] || !xqs[i])) || !scales[i])
+      return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL pointer");
     if (!aligned16(xs[i]) || !aligned16(xqs[i]))
       return fail(QFLASH_ERR_INVALID_ARGUMENT, "x and x_q must be 16-byte aligned");
   }
@@ -457,7 +460,7 @@ qflash_status qflash_quantize_per_tensor(const void* x, qflash_dtype dtype, int6
                                          qflash_stream_t stream) {
   if (!scale_dev && !scale_host)
     return fail(QFLASH_ERR_INVALID_ARGUMENT, "need scale_dev or scale_host");
-  if (!x || !x_q) return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (numel > 0 && (!x || !x_q)) return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL pointer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   float* sd = scale_dev;
   bool temp = false;

@@ -185,6 +185,34 @@ def test_full_size_l14_b64_sampled(orc):
             assert np.array_equal(got[p, a:b], ref), (p, a)
 
 
+@pytest.mark.parametrize("d,kind", [(64, "uniform"), (64, "all_min"), (128, "uniform")])
+def test_maximum_sequence_length_sampled(orc, d, kind):
+    # N = 65536, the ABI maximum: |O| <= 128 * 127 * N stays below 2^31 and the
+    # release / normaliser paths see their largest l; rows sampled at tile edges
+    N = 65536
+    q, k, v = gen_int8_qkv(1, N, d, seed=5, kind=kind)
+    for (sq, sk) in [(0.05, 0.05), (0.004, 0.003)]:
+        got = _gpu_attention(q, k, v, sq, sk, block_kv=128)
+        for (a, b) in [(0, 2), (127, 129), (32767, 32769), (N - 2, N)]:
+            ref = orc.attention_rows(q, k, v, sq, sk, 0, a, b)
+            assert np.array_equal(got[0, a:b], ref), (d, kind, sq, a)
+
+
+def test_empty_inputs():
+    # zero elements: the quantizer is a no-op; an attention call with no problems or
+    # no tokens is rejected before any launch (QFLASH_ERR_UNSUPPORTED_SHAPE)
+    x = torch.zeros(0, dtype=torch.float32, device="cuda")
+    xq = torch.zeros(0, dtype=torch.int8, device="cuda")
+    _, sc = qf.qflash_quantize_per_tensor(x, out=xq)
+    torch.cuda.synchronize()
+    assert sc.item() == np.float32(1.0 / 127.0)  # amax of the empty set is 0 (R3)
+    for shape in [(0, 197, 64), (3, 0, 64)]:
+        q = torch.zeros(shape, dtype=torch.int8, device="cuda")
+        with pytest.raises(_lib.QFlashError) as e:
+            qf.qflash_attention_int8(q, q, q, 0.05, 0.05, 0.05)
+        assert e.value.status == _lib.QFLASH_ERR_UNSUPPORTED_SHAPE
+
+
 # ------------------------------------------------------------------ quantizer
 @pytest.mark.parametrize("n", [1, 3, 16, 1000, 4099, 1 << 20, 1_210_368])
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
