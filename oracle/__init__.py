@@ -233,3 +233,46 @@ def attention_rows_state(q, k, v, s_q, s_k, p: int, row_begin: int, row_end: int
     if rc != QO_OK:
         raise ValueError(rc)
     return out, l_state, o_state
+
+
+# --------------------------------------------------------------- per-head granularity
+# one scale per (tensor, head) instead of per
+# tensor.  Problems are the flattened (batch, window, head) with the head fastest
+# (p = (b W + w) H + h), so head h owns the problems p = h, h + H, h + 2H, ...  Each
+# head is quantized, attended and dequantized exactly as a per-tensor problem set of
+# its own: the definitions below are that composition, nothing more.
+def head_problems(P: int, H: int, h: int) -> np.ndarray:
+    return np.arange(h, P, H)
+
+
+def quantize_per_head(x: np.ndarray, H: int):
+    """Eq. 2 with the amax taken over each head's problems (x: [P, N, d])."""
+    P = x.shape[0]
+    assert P % H == 0
+    out = np.empty(x.shape, dtype=np.int8)
+    scales = np.empty(H, dtype=np.float32)
+    for h in range(H):
+        idx = head_problems(P, H, h)
+        out[idx], s = quantize(np.ascontiguousarray(x[idx]))
+        scales[h] = s
+    return out, scales
+
+
+def attention_per_head(q, k, v, s_q, s_k, H: int, block_kv: int = 128, nthreads: int = 1):
+    """Algorithm 1 with head h's constants derived from (s_q[h], s_k[h])."""
+    P = q.shape[0]
+    out = np.empty_like(np.asarray(q, dtype=np.int8))
+    for h in range(H):
+        idx = head_problems(P, H, h)
+        out[idx] = attention(q[idx], k[idx], v[idx], float(s_q[h]), float(s_k[h]),
+                             block_kv=block_kv, nthreads=nthreads)
+    return out
+
+
+def dequantize_per_head(xq: np.ndarray, s: np.ndarray, H: int) -> np.ndarray:
+    P = xq.shape[0]
+    y = np.empty(xq.shape, dtype=np.float32)
+    for h in range(H):
+        idx = head_problems(P, H, h)
+        y[idx] = dequantize(np.ascontiguousarray(xq[idx]), float(s[h]))
+    return y

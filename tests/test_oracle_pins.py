@@ -382,3 +382,65 @@ def test_scale_release_vs_accumulation(orc):
     a1 = orc.attention(qq, kq, vq, sq, sk, block_kv=1024, mode=0)
     b1 = orc.attention(qq, kq, vq, sq, sk, block_kv=1024, mode=1)
     assert np.abs(a1.astype(int) - b1.astype(int)).max() <= 1
+
+
+# ------------------------------------------------------------- per-head granularity (N1)
+def _head_data(P, N, d, H, seed, spread):
+    rng = np.random.default_rng(seed)
+    gains = np.exp(np.linspace(-spread, spread, H)).astype(np.float32)
+    x = [rng.standard_normal((P, N, d)).astype(np.float32) for _ in range(3)]
+    for t in x:
+        t *= np.tile(gains, P // H)[:, None, None]
+    return x
+
+
+def test_per_head_with_one_head_is_per_tensor(orc):
+    q, k, v = _head_data(4, 49, 32, 1, 0, 0.0)
+    qh, sh = orc.quantize_per_head(q, 1)
+    qt, st = orc.quantize(q)
+    assert np.array_equal(qh, qt) and sh[0] == np.float32(st)
+    kq, sk = orc.quantize(k)
+    vq, _ = orc.quantize(v)
+    a = orc.attention_per_head(qt, kq, vq, sh, [sk], 1)
+    assert np.array_equal(a, orc.attention(qt, kq, vq, st, sk))
+
+
+def test_per_head_equal_heads_match_per_tensor(orc):
+    # every head carries the same data: per-head scales all equal the per-tensor one
+    base = _head_data(1, 49, 32, 1, 3, 0.0)
+    q, k, v = (np.repeat(t, 4, axis=0) for t in base)
+    qh, sh = orc.quantize_per_head(q, 4)
+    qt, st = orc.quantize(q)
+    assert np.all(sh == np.float32(st)) and np.array_equal(qh, qt)
+
+
+def test_per_head_codes_and_error_bound(orc):
+    H = 3
+    q, _, _ = _head_data(6, 49, 32, H, 1, 2.0)
+    qh, sh = orc.quantize_per_head(q, H)
+    for h in range(H):
+        idx = orc.head_problems(6, H, h)
+        amax = np.abs(q[idx]).max()
+        assert sh[h] == np.float32(amax) / np.float32(127.0)
+        err = np.abs(q[idx] - sh[h] * qh[idx].astype(np.float32))
+        assert err.max() <= sh[h] / 2 * (1 + 1e-6)
+
+
+def test_per_head_improves_sqnr_with_head_spread(orc):
+    # heads of very different magnitude (x e^-2 .. e^2): per-tensor scales crush the
+    # small heads, per-head scales do not (the paper's motivation)
+    from oracle.fp_reference import attention_fp64, sqnr_db
+    H, P, N, d = 4, 8, 64, 32
+    q, k, v = _head_data(P, N, d, H, 7, 2.0)
+    ref = attention_fp64(q, k, v)
+    qq, sq = orc.quantize(q)
+    kq, sk = orc.quantize(k)
+    vq, sv = orc.quantize(v)
+    y_t = orc.dequantize(orc.attention(qq, kq, vq, sq, sk), sv)
+    qh, sqh = orc.quantize_per_head(q, H)
+    kh, skh = orc.quantize_per_head(k, H)
+    vh, svh = orc.quantize_per_head(v, H)
+    y_h = orc.dequantize_per_head(orc.attention_per_head(qh, kh, vh, sqh, skh, H), svh, H)
+    small = orc.head_problems(P, H, 0)  # the smallest-gain head
+    assert sqnr_db(ref[small], y_h[small]) > sqnr_db(ref[small], y_t[small]) + 6.0
+    assert sqnr_db(ref, y_h) >= sqnr_db(ref, y_t) - 0.5
