@@ -194,6 +194,38 @@ QFLASH_API qflash_status qflash_forward_fused(const float* q, const float* k, co
                                               float* scales_dev, void* workspace_dev,
                                               qflash_stream_t stream);
 
+/* --------------------------------------------------------------------------
+ * Per-head granularity (the paper's per-tensor scales are the
+ * H = 1 case).  Problems are the flattened (batch,
+ * window, head) with the head fastest, so head = problem mod H; every head gets
+ * its own (s_q, s_k, s_v) and hence its own integer constants.  Bit-identical to
+ * running the per-tensor path on each head's problems separately.
+ *   H in [1, 96], num_problems a multiple of H, num_problems * H^2 < 2^32.
+ * qflash_quantize_per_head: fp32 q, k, v [P, N, d] -> int8 codes; scales_dev =
+ *   device float[3 H] written as (s_q[0..H), s_k[0..H), s_v[0..H)).
+ * qflash_attention_int8_per_head: Algorithm 1 with head h's constants derived on
+ *   the device from scales_dev (same layout) into workspace_dev
+ *   (QFLASH_DSCALE_WORKSPACE_BYTES; int32 status at offset 0, nothing written to o
+ *   if a head's scales are out of range); s_O[h] = s_V[h].
+ * qflash_dequantize_per_head: y = fl32(s[head] * x^), scales_dev = device float[H]
+ *   (e.g. scales_dev + 2 H of the calls above). */
+QFLASH_API qflash_status qflash_quantize_per_head(const float* q, const float* k, const float* v,
+                                                  int32_t num_problems, int32_t seq_len,
+                                                  int32_t head_dim, int32_t heads, int8_t* q_q,
+                                                  int8_t* k_q, int8_t* v_q, float* scales_dev,
+                                                  qflash_stream_t stream);
+QFLASH_API qflash_status qflash_attention_int8_per_head(const int8_t* q, const int8_t* k,
+                                                        const int8_t* v, const float* scales_dev,
+                                                        int32_t heads,
+                                                        const qflash_attn_shape* shape,
+                                                        qflash_variant variant, int8_t* o,
+                                                        void* workspace_dev,
+                                                        qflash_stream_t stream);
+QFLASH_API qflash_status qflash_dequantize_per_head(const int8_t* x_q, const float* scales_dev,
+                                                    int32_t num_problems, int32_t seq_len,
+                                                    int32_t head_dim, int32_t heads, float* y,
+                                                    qflash_stream_t stream);
+
 /* Inverse of Eq. 2: y = fl32(scale * (float)x^).  x_q device int8[numel],
  * y device float[numel]. */
 QFLASH_API qflash_status qflash_dequantize(const int8_t* x_q, float scale, int64_t numel, float* y,

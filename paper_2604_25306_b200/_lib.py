@@ -33,6 +33,7 @@ EXPORTED = [
     "qflash_status_string", "qflash_last_error", "qflash_version",
     "qflash_quantize_qkv_prepare", "qflash_attention_int8_prepared",
     "qflash_attention_dequant_prepared", "qflash_forward_fused",
+    "qflash_quantize_per_head", "qflash_attention_int8_per_head", "qflash_dequantize_per_head",
 ]
 
 
@@ -91,6 +92,13 @@ def lib():
     L.qflash_forward_fused.restype = st
     L.qflash_forward_fused.argtypes = [vp, vp, vp, ctypes.POINTER(AttnShape), st, vp, vp, vp, vp,
                                        vp, vp, vp, vp]
+    L.qflash_quantize_per_head.restype = st
+    L.qflash_quantize_per_head.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp]
+    L.qflash_attention_int8_per_head.restype = st
+    L.qflash_attention_int8_per_head.argtypes = [vp, vp, vp, vp, i32, ctypes.POINTER(AttnShape), st,
+                                                 vp, vp, vp]
+    L.qflash_dequantize_per_head.restype = st
+    L.qflash_dequantize_per_head.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp]
     L.qflash_dequantize.restype = st
     L.qflash_dequantize.argtypes = [vp, f32, i64, vp, vp]
     L.qflash_dequantize_dscale.restype = st

@@ -233,6 +233,34 @@ class QFlashPipeline:
         return self.out
 
 
+# ------------------------------------------------ per-head granularity
+def qflash_forward_per_head(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, heads: int,
+                            block_kv: int = 128, variant: str = "auto", stream=None):
+    """Per-head scales: fp32 Q, K, V [P, N, d] (head = problem mod heads) ->
+    per-head quantization -> integer attention with per-head constants ->
+    per-head dequantization.  Returns (y fp32, o int8, scales float32[3 heads],
+    workspace) -- the int32 status of the constant derivation is workspace[0]."""
+    assert q.shape == k.shape == v.shape and q.dim() == 3 and q.dtype == torch.float32
+    P, N, d = q.shape
+    dev = q.device
+    codes = [torch.empty(q.shape, dtype=torch.int8, device=dev) for _ in range(3)]
+    scales = torch.empty(3 * heads, dtype=torch.float32, device=dev)
+    check(lib().qflash_quantize_per_head(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v), P, N, d, heads,
+                                         _dev_ptr(codes[0]), _dev_ptr(codes[1]), _dev_ptr(codes[2]),
+                                         _dev_ptr(scales), _stream(stream)))
+    o = torch.empty(q.shape, dtype=torch.int8, device=dev)
+    ws = torch.empty(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=dev)
+    shape = _shape(q, block_kv)
+    check(lib().qflash_attention_int8_per_head(_dev_ptr(codes[0]), _dev_ptr(codes[1]),
+                                               _dev_ptr(codes[2]), _dev_ptr(scales), heads,
+                                               ctypes.byref(shape), _lib.VARIANTS[variant],
+                                               _dev_ptr(o), _dev_ptr(ws), _stream(stream)))
+    y = torch.empty(q.shape, dtype=torch.float32, device=dev)
+    check(lib().qflash_dequantize_per_head(_dev_ptr(o), _dev_ptr(scales[2 * heads:]), P, N, d,
+                                           heads, _dev_ptr(y), _stream(stream)))
+    return y, o, scales, ws
+
+
 class QFlashHostPipeline:
     """Serving loop over host (pinned) fp32 batches: each call copies one batch in,
     runs the whole hot path (QFlashPipeline) and copies the fp32 result back, all

@@ -8,11 +8,11 @@
 
 namespace qf {
 
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FQ>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FQ, bool PH = false>
 cudaError_t try_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const AttnArgs& args, int64_t tiles, int sms, cudaStream_t stream) {
   if constexpr (config_fits<D, BC, NSEG, CS, QT>()) {
-    return launch_attn_t<D, BC, NSEG, CS, QT, DBG, FQ>(tq, tk, tv, args, tiles, sms, stream);
+    return launch_attn_t<D, BC, NSEG, CS, QT, DBG, FQ, PH>(tq, tk, tv, args, tiles, sms, stream);
   } else {
     return cudaErrorNotSupported;
   }
@@ -37,6 +37,21 @@ cudaError_t launch_attention_d(int BC, int nseg, int cfg, const CUtensorMap& tq,
   QF_BC_SEG(64, 2) QF_BC_SEG(128, 2) QF_BC_SEG(256, 2)
   QF_BC_SEG(64, 4) QF_BC_SEG(128, 4)
 #undef QF_BC_SEG
+  return cudaErrorNotSupported;
+}
+
+// Per-head constants (cfg 0 only): one instantiation per (B_c, NSEG).
+template <int D>
+cudaError_t launch_attention_ph_d(int BC, int nseg, const CUtensorMap& tq, const CUtensorMap& tk,
+                                  const CUtensorMap& tv, const AttnArgs& args, int64_t tiles,
+                                  int sms, cudaStream_t stream) {
+#define QF_PH(bc, ns)           \
+  if (BC == bc && nseg == ns)   \
+    return try_launch<D, bc, ns, 4, 1, false, false, true>(tq, tk, tv, args, tiles, sms, stream);
+  QF_PH(64, 1) QF_PH(128, 1) QF_PH(256, 1)
+  QF_PH(64, 2) QF_PH(128, 2) QF_PH(256, 2)
+  QF_PH(64, 4) QF_PH(128, 4)
+#undef QF_PH
   return cudaErrorNotSupported;
 }
 

@@ -389,8 +389,34 @@ struct TileIter {
 // ---------------------------------------------------------------- softmax role
 // Masked 8-column groups: column group k of a thread is fully valid, partial
 // (the ragged edge), or absent; `valid` is warp-uniform so the branches are too.
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FASTQ>
-__device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntParams& prm,
+// Per-head granularity: the constants of head h = problem mod H
+// (problems are (batch, window, head) with the head fastest), read per tile.
+struct RowConsts {
+  uint32_t s_inv;
+  int sinv_log2;
+  int32_t rel_lthr;
+};
+QF_DEV RowConsts row_consts(const IntParams& prm, int Tc) {
+  RowConsts r;
+  r.s_inv = static_cast<uint32_t>(prm.s_inv);
+  r.sinv_log2 = 31 - __clz(prm.s_inv);
+  // fast-release threshold on l: (3 * 128 (l + 2 T_c) + s_inv) s_inv < 2^32, i.e.
+  // 384 (l + 2 T_c) + s_inv <= floor((2^32 - 1) / s_inv) (64-bit magic, n < 2^56)
+  const uint64_t mg = (static_cast<uint64_t>(prm.rel_magic_hi) << 32) | prm.rel_magic_lo;
+  const uint64_t A = __umul64hi(0xFFFFFFFFull, mg) >> prm.rel_shift;
+  const int64_t t = (static_cast<int64_t>(A) - static_cast<int64_t>(r.s_inv)) / 384 - 2 * Tc;
+  r.rel_lthr = t < 0 ? -1 : (t > 0x7FFFFFFF ? 0x7FFFFFFF : static_cast<int32_t>(t));
+  return r;
+}
+QF_DEV IntParams head_params(const AttnArgs& a, int problem) {
+  // problem / H (H = 1: the 32-bit magic ceil(2^32 / 1) does not exist)
+  const int q = a.H == 1 ? problem : static_cast<int>(__umulhi(static_cast<uint32_t>(problem), a.h_magic));
+  const int h = problem - q * a.H;
+  return *reinterpret_cast<const IntParams*>(reinterpret_cast<const char*>(a.head_prm) + kHeadPrmStride * h);
+}
+
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FASTQ, bool PH = false>
+__device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntParams& prm_k,
                                              uint32_t tmem_group, GroupBars<Cfg<D, BC, NSEG, CS, QT>::kNumS> gb,
                                              uint32_t red_group, const uint32_t* recip, int g,
                                              int c, int quarter, int lane) {
@@ -406,17 +432,7 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
   const int c0 = c * CW;  // first key column of this thread
   const bool dbg_on = DBG && blockIdx.x == 0 && g == 0;
   const bool ts_warp = dbg_on && c == 0 && quarter == 0 && lane == 0;
-  const uint32_t s_inv = static_cast<uint32_t>(prm.s_inv);
-  const int sinv_log2 = 31 - __clz(prm.s_inv);
-  // fast-release threshold on l: (3 * 128 (l + 2 T_c) + s_inv) s_inv < 2^32, i.e.
-  // 384 (l + 2 T_c) + s_inv <= floor((2^32 - 1) / s_inv) (64-bit magic, n < 2^56)
-  int32_t rel_lthr;
-  {
-    const uint64_t mg = (static_cast<uint64_t>(prm.rel_magic_hi) << 32) | prm.rel_magic_lo;
-    const uint64_t A = __umul64hi(0xFFFFFFFFull, mg) >> prm.rel_shift;
-    const int64_t t = (static_cast<int64_t>(A) - static_cast<int64_t>(s_inv)) / 384 - 2 * Tc;
-    rel_lthr = t < 0 ? -1 : (t > 0x7FFFFFFF ? 0x7FFFFFFF : static_cast<int32_t>(t));
-  }
+  const RowConsts rck = row_consts(prm_k, Tc);  // per-tensor constants (PH: per tile below)
   bool tables_ready = false;  // named barrier 15: step (11) / dequant tables in smem
 
   TileIter<NSEG> ti;
@@ -434,6 +450,16 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
     }
     const int nseg = ti.nseg;
     int32_t m = -(1 << 21);  // m^(0) = -2^21
+    IntParams prm_t;
+    RowConsts rct;
+    if constexpr (PH) {
+      prm_t = head_params(args, ti.problem + seg);
+      rct = row_consts(prm_t, Tc);
+    }
+    const IntParams& prm = PH ? prm_t : prm_k;
+    const uint32_t s_inv = PH ? rct.s_inv : rck.s_inv;
+    const int sinv_log2 = PH ? rct.sinv_log2 : rck.sinv_log2;
+    const int32_t rel_lthr = PH ? rct.rel_lthr : rck.rel_lthr;
 
     for (int j = 0; j < Tc; ++j) {
       const int it = it0 + j;
@@ -1201,7 +1227,7 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FQ = false>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FQ = false, bool PH = false>
 __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
     qflash_attn_kernel(const __grid_constant__ CUtensorMap tm_q,
                        const __grid_constant__ CUtensorMap tm_k,
@@ -1473,10 +1499,11 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
       const Bars gb{bars + g * C::kBarsPerGroup};
       const uint32_t red_group = smem_u32(smem + C::kRed) + static_cast<uint32_t>(g * 2 * CS * 128 * 4);
       const uint32_t tG = tmem_base + g * C::kGroupCols;
+      // (PH: the header's q_shift / s_inv / m_p encode "every head takes the fast path")
       if (prm.q_shift == 0 && static_cast<uint64_t>(prm.s_inv) * static_cast<uint64_t>(prm.m_p) < (1ull << 32))
-        softmax_role<D, BC, NSEG, CS, QT, DBG, true>(args, prm, tG, gb, red_group, recip, g, c, warp & 3, lane);
+        softmax_role<D, BC, NSEG, CS, QT, DBG, true, PH>(args, prm, tG, gb, red_group, recip, g, c, warp & 3, lane);
       else
-        softmax_role<D, BC, NSEG, CS, QT, DBG, false>(args, prm, tG, gb, red_group, recip, g, c, warp & 3, lane);
+        softmax_role<D, BC, NSEG, CS, QT, DBG, false, PH>(args, prm, tG, gb, red_group, recip, g, c, warp & 3, lane);
       }
     }
   }
@@ -1497,12 +1524,13 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
 // Host-side launch (called by the instantiation units).  `tiles` = number of
 // work tiles; the persistent grid is G = min(ceil(tiles / QT), SMs) CTAs whose
 // group g visits tiles b + g G, b + g G + QT G, ...
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FQ = false>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FQ = false, bool PH = false>
 cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                           AttnArgs args, int64_t tiles, int sms, cudaStream_t stream) {
   using C = Cfg<D, BC, NSEG, CS, QT>;
   static_assert(C::kAlloc <= 227 * 1024, "shared memory budget");
-  auto kern = qflash_attn_kernel<D, BC, NSEG, CS, QT, DBG, FQ>;
+  static_assert(!PH || CS > 1, "per-head constants: column-split configurations only");
+  auto kern = qflash_attn_kernel<D, BC, NSEG, CS, QT, DBG, FQ, PH>;
   static int configured[16] = {0};
   int dev = 0;
   cudaGetDevice(&dev);

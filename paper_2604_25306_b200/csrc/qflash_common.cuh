@@ -27,6 +27,9 @@ struct IntParams {
 static_assert(sizeof(IntParams) == 72, "IntParams layout");
 
 constexpr int kPdlDefault = 15;
+constexpr int kHeadPrmStride = 80;   // bytes per head in the per-head constant table
+constexpr int kHeadPrmOffset = 128;  // table offset in the per-head workspace
+constexpr int kMaxHeads = 96;        // 128 + 96 * 80 <= QFLASH_DSCALE_WORKSPACE_BYTES
 
 struct AttnArgs {
   int32_t N;        // sequence length
@@ -51,6 +54,10 @@ struct AttnArgs {
   IntParams* prm_out;   // device copy of the derived constants (workspace)
   uint32_t* table_out;  // device copy of the dequant table (workspace + 4096)
   int64_t numel;        // elements per tensor (a multiple of 4: d in {32, 64, 128})
+  // per-head granularity (PH instantiations): head h = problem mod H
+  const IntParams* head_prm;  // device table, kHeadPrmStride bytes per head
+  int32_t H;
+  uint32_t h_magic;           // ceil(2^32 / H): problem / H = umulhi(problem, h_magic)
   // bring-up dumps for CTA 0's first tile only; nullptr in production:
   int32_t* dbg_s;  // [128][BC] raw S of KV tile 0
   int32_t* dbg_p;  // [128][BC/4] packed P words of KV tile 0

@@ -37,6 +37,15 @@ cudaError_t launch_fused_d64(int BC, int nseg, int cfg, const CUtensorMap& tq, c
 cudaError_t launch_fused_d128(int BC, int nseg, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
                               const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
                               cudaStream_t stream);
+cudaError_t launch_attention_ph(int D, int BC, int nseg, const CUtensorMap& tq,
+                                const CUtensorMap& tk, const CUtensorMap& tv,
+                                const AttnArgs& args, int64_t tiles, int sms,
+                                cudaStream_t stream);
+cudaError_t launch_quantize_per_head(const QuantTensors& t, int ntensors, int64_t P,
+                                     int64_t vec_per_problem, int H, cudaStream_t stream);
+cudaError_t launch_derive_per_head(const float* scales, int H, int32_t d, void* ws, cudaStream_t stream);
+cudaError_t launch_dequantize_per_head(const int8_t* xq, const float* scales, int64_t P,
+                                       int64_t vec_per_problem, int H, float* y, cudaStream_t stream);
 cudaError_t launch_attention_dbg(int D, int BC, int nseg, int cfg, const CUtensorMap& tq,
                                  const CUtensorMap& tk, const CUtensorMap& tv,
                                  const AttnArgs& args, int64_t tiles, int sms,
@@ -206,7 +215,7 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
                             const qflash_attn_shape* shape, int bc, qflash_variant variant,
                             int8_t* o, const qf::IntParams* host_prm,
                             const qf::IntParams* dev_prm, cudaStream_t stream, float* y,
-                            const FusedIn* fin,
+                            const FusedIn* fin, int heads,
                             int32_t* dbg_s = nullptr, int32_t* dbg_p = nullptr,
                             int32_t* dbg_o = nullptr, long long* dbg_t = nullptr) {
   const int P = shape->num_problems, N = shape->seq_len, d = shape->head_dim;
@@ -268,12 +277,12 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   // (L14 b64: 848 vs 938 us for cfg 2); one KV tile (Swin windows) -> cfg 2.
   const int Tc_host = (N + bc_eff - 1) / bc_eff;
   int cfg = 0;
-  if (tiles > sms) {
+  if (tiles > sms && heads == 0) {
     const int pref[2] = {Tc_host == 1 ? 2 : 1, Tc_host == 1 ? 1 : 2};
     for (int c : pref)
       if (cfg == 0 && qf::attention_supported(d, bc_eff, nseg, c)) cfg = c;
   }
-  if (cfg_env >= 0 && qf::attention_supported(d, bc_eff, nseg, cfg_env)) cfg = cfg_env;
+  if (cfg_env >= 0 && heads == 0 && qf::attention_supported(d, bc_eff, nseg, cfg_env)) cfg = cfg_env;
   if (!qf::attention_supported(d, bc_eff, nseg, cfg))
     return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "no kernel configuration for d=%d block=%d", d, bc_eff);
   CUtensorMap tq, tk, tv;
@@ -313,8 +322,17 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   // Persistent grid: one CTA per SM, its groups walking tiles b + g G, + QT G, ...
   args.Tr = static_cast<int32_t>(Tr);
   const bool dbg = dbg_s != nullptr || dbg_p != nullptr || dbg_o != nullptr || dbg_t != nullptr;
-  cudaError_t e = qf::launch_attention(d, bc_eff, nseg, cfg, tq, tk, tv, args, tiles, sms, dbg,
-                                       fin != nullptr, stream);
+  cudaError_t e;
+  if (heads > 0) {  // per-head constants (configuration 0)
+    args.head_prm = reinterpret_cast<const qf::IntParams*>(reinterpret_cast<const char*>(dev_prm) +
+                                                          qf::kHeadPrmOffset);
+    args.H = heads;
+    args.h_magic = static_cast<uint32_t>(((1ull << 32) + heads - 1) / heads);
+    e = qf::launch_attention_ph(d, bc_eff, nseg, tq, tk, tv, args, tiles, sms, stream);
+  } else {
+    e = qf::launch_attention(d, bc_eff, nseg, cfg, tq, tk, tv, args, tiles, sms, dbg,
+                             fin != nullptr, stream);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "attention launch");
   return QFLASH_OK;
 }
@@ -338,7 +356,7 @@ qflash_status attention_host_scales(const int8_t* q, const int8_t* k, const int8
                 static_cast<double>(s_q), static_cast<double>(s_k), shape->head_dim);
   int dev = 0;
   if ((st = check_device(&dev)) != QFLASH_OK) return st;
-  if ((st = launch_common(q, k, v, shape, bc, variant, o, &prm, nullptr, stream, nullptr, nullptr)) != QFLASH_OK)
+  if ((st = launch_common(q, k, v, shape, bc, variant, o, &prm, nullptr, stream, nullptr, nullptr, 0)) != QFLASH_OK)
     return st;
   if (s_o) *s_o = s_v;  // s_O = s_V
   return QFLASH_OK;
@@ -421,7 +439,7 @@ qflash_status qflash_attention_int8_dscale(const int8_t* q, const int8_t* k, con
   derive_params_kernel<<<1, 1, 0, s>>>(scales_dev, shape->head_dim, prm);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "derive_params_kernel launch");
-  return launch_common(q, k, v, shape, bc, variant, o, nullptr, prm, s, nullptr, nullptr);
+  return launch_common(q, k, v, shape, bc, variant, o, nullptr, prm, s, nullptr, nullptr, 0);
 }
 
 static qflash_status quantize_impl(const void* const* xs, int8_t* const* xqs, float* const* scales,
@@ -529,7 +547,7 @@ qflash_status qflash_attention_int8_prepared(const int8_t* q, const int8_t* k, c
   if ((st = check_device(&dev)) != QFLASH_OK) return st;
   return launch_common(q, k, v, shape, bc, variant, o, nullptr,
                        reinterpret_cast<const qf::IntParams*>(workspace_dev),
-                       reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr);
+                       reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr, 0);
 }
 
 qflash_status qflash_attention_dequant_prepared(const int8_t* q, const int8_t* k, const int8_t* v,
@@ -559,7 +577,7 @@ qflash_status qflash_attention_dequant_prepared(const int8_t* q, const int8_t* k
   if ((st = check_device(&dev)) != QFLASH_OK) return st;
   return launch_common(q, k, v, shape, bc, variant, o, nullptr,
                        reinterpret_cast<const qf::IntParams*>(workspace_dev),
-                       reinterpret_cast<cudaStream_t>(stream), y, nullptr);
+                       reinterpret_cast<cudaStream_t>(stream), y, nullptr, 0);
 }
 
 qflash_status qflash_forward_fused(const float* q, const float* k, const float* v,
@@ -605,7 +623,7 @@ qflash_status qflash_forward_fused(const float* q, const float* k, const float* 
   fin.scales = scales_dev;
   fin.workspace = workspace_dev;
   return launch_common(q_q, k_q, v_q, shape, bc, variant, o, nullptr, nullptr,
-                       reinterpret_cast<cudaStream_t>(stream), y, &fin);
+                       reinterpret_cast<cudaStream_t>(stream), y, &fin, 0);
 }
 
 static qflash_status dequant_impl(const int8_t* x_q, float scale, const float* scale_dev,
@@ -636,6 +654,86 @@ qflash_status qflash_dequantize_dscale(const int8_t* x_q, const float* scale_dev
   return dequant_impl(x_q, 0.0f, scale_dev, numel, y, reinterpret_cast<cudaStream_t>(stream));
 }
 
+// ------------------------------------------------ per-head granularity
+static qflash_status check_heads(int32_t P, int32_t H) {
+  if (H < 1 || H > qf::kMaxHeads)
+    return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "heads %d not in [1, %d]", H, qf::kMaxHeads);
+  if (P % H != 0) return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "num_problems %d not a multiple of heads %d", P, H);
+  // problem / H by umulhi(problem, ceil(2^32 / H)) is exact for problem < 2^32 / H^2
+  if (static_cast<uint64_t>(P) * H * H >= (1ull << 32))
+    return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "num_problems * heads^2 must be < 2^32");
+  return QFLASH_OK;
+}
+
+qflash_status qflash_quantize_per_head(const float* q, const float* k, const float* v,
+                                       int32_t num_problems, int32_t seq_len, int32_t head_dim,
+                                       int32_t heads, int8_t* q_q, int8_t* k_q, int8_t* v_q,
+                                       float* scales_dev, qflash_stream_t stream) {
+  if (!q || !k || !v || !q_q || !k_q || !v_q || !scales_dev)
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (num_problems < 1 || seq_len < 1 || (head_dim != 32 && head_dim != 64 && head_dim != 128))
+    return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "shape (%d, %d, %d)", num_problems, seq_len, head_dim);
+  qflash_status st = check_heads(num_problems, heads);
+  if (st != QFLASH_OK) return st;
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(q_q) || !aligned16(k_q) || !aligned16(v_q))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
+  int dev = 0;
+  if ((st = check_device(&dev)) != QFLASH_OK) return st;
+  qf::QuantTensors t;
+  memset(&t, 0, sizeof(t));
+  const void* xs[3] = {q, k, v};
+  int8_t* xqs[3] = {q_q, k_q, v_q};
+  for (int i = 0; i < 3; ++i) {
+    t.x[i] = xs[i];
+    t.xq[i] = xqs[i];
+    t.scale[i] = scales_dev + i * heads;
+  }
+  const int64_t vpp = static_cast<int64_t>(seq_len) * head_dim / 4;
+  cudaError_t e = qf::launch_quantize_per_head(t, 3, num_problems, vpp, heads,
+                                               reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "per-head quantize launch");
+  return QFLASH_OK;
+}
+
+qflash_status qflash_attention_int8_per_head(const int8_t* q, const int8_t* k, const int8_t* v,
+                                             const float* scales_dev, int32_t heads,
+                                             const qflash_attn_shape* shape, qflash_variant variant,
+                                             int8_t* o, void* workspace_dev, qflash_stream_t stream) {
+  int bc = 0;
+  qflash_status st = validate_shape(shape, &bc);
+  if (st != QFLASH_OK) return st;
+  if ((st = check_heads(shape->num_problems, heads)) != QFLASH_OK) return st;
+  const int64_t bytes = static_cast<int64_t>(shape->num_problems) * shape->seq_len * shape->head_dim;
+  if ((st = validate_qkvo(q, k, v, o, bytes)) != QFLASH_OK) return st;
+  if (!scales_dev || !workspace_dev || !aligned16(workspace_dev))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "scales_dev / workspace_dev NULL or misaligned");
+  int dev = 0;
+  if ((st = check_device(&dev)) != QFLASH_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = qf::launch_derive_per_head(scales_dev, heads, shape->head_dim, workspace_dev, s);
+  if (e != cudaSuccess) return cuda_fail(e, "derive_per_head launch");
+  return launch_common(q, k, v, shape, bc, variant, o, nullptr,
+                       reinterpret_cast<const qf::IntParams*>(workspace_dev), s, nullptr, nullptr, heads);
+}
+
+qflash_status qflash_dequantize_per_head(const int8_t* x_q, const float* scales_dev,
+                                         int32_t num_problems, int32_t seq_len, int32_t head_dim,
+                                         int32_t heads, float* y, qflash_stream_t stream) {
+  if (!x_q || !scales_dev || !y) return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (num_problems < 1 || seq_len < 1 || (head_dim != 32 && head_dim != 64 && head_dim != 128))
+    return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "shape (%d, %d, %d)", num_problems, seq_len, head_dim);
+  qflash_status st = check_heads(num_problems, heads);
+  if (st != QFLASH_OK) return st;
+  if (!aligned16(x_q) || !aligned16(y)) return fail(QFLASH_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
+  int dev = 0;
+  if ((st = check_device(&dev)) != QFLASH_OK) return st;
+  cudaError_t e = qf::launch_dequantize_per_head(x_q, scales_dev, num_problems,
+                                                 static_cast<int64_t>(seq_len) * head_dim / 4, heads, y,
+                                                 reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "per-head dequantize launch");
+  return QFLASH_OK;
+}
+
 // Bring-up entry (include/qflash_debug.h): qflash_attention_int8_ex plus raw
 // dumps of S, P and the final (O, l) of CTA (problem 0, query tile 0).
 qflash_status qflash_debug_attention(const int8_t* q, const int8_t* k, const int8_t* v, float s_q,
@@ -652,7 +750,7 @@ qflash_status qflash_debug_attention(const int8_t* q, const int8_t* k, const int
   int dev = 0;
   if ((st = check_device(&dev)) != QFLASH_OK) return st;
   return launch_common(q, k, v, shape, bc, variant, o, &prm, nullptr,
-                       reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr, dbg_s, dbg_p, dbg_o, dbg_t);
+                       reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr, 0, dbg_s, dbg_p, dbg_o, dbg_t);
 }
 
 }  // extern "C"

@@ -399,6 +399,174 @@ __global__ void __launch_bounds__(kQThreads)
     y[i] = __fmul_rn(s, static_cast<float>(xq[i]));
 }
 
+// ------------------------------------------------------- per-head granularity (N1)
+// Problems are (batch, window, head) with the head fastest: head = problem mod H.
+// Grid: x = problem, y = chunk of 1024 16-byte vectors of that problem, so every
+// block sees one head.  Pass 1: block amax -> atomicMax of s = fl32(amax / 127)
+// into scales[t * H + head] (pre-zeroed; fl32 division is monotone).  Pass 2:
+// quantize with the head's final scale (0 -> 1/127, R3).
+constexpr int kPHVec = 4;  // vectors per thread per block
+
+__device__ __forceinline__ int head_of(int p, int H, uint32_t h_magic) {
+  if (H == 1) return 0;  // ceil(2^32 / 1) does not fit the 32-bit magic
+  const int q = static_cast<int>(__umulhi(static_cast<uint32_t>(p), h_magic));
+  return p - q * H;
+}
+
+__global__ void __launch_bounds__(kQThreads)
+    amax_per_head_kernel(QuantTensors t, int64_t vec_per_problem, int H, uint32_t h_magic) {
+  const int ti = blockIdx.z;
+  const int p = blockIdx.x;
+  const float4* x = reinterpret_cast<const float4*>(pick(t, ti)) + static_cast<int64_t>(p) * vec_per_problem;
+  float m = 0.f;
+  const int64_t v0 = static_cast<int64_t>(blockIdx.y) * kQThreads * kPHVec + threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < kPHVec; ++u) {
+    const int64_t i = v0 + u * kQThreads;
+    if (i < vec_per_problem) {
+      const float4 v = __ldg(x + i);
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ float red[kQThreads / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b = red[0];
+#pragma unroll
+    for (int w = 1; w < kQThreads / 32; ++w) b = fmaxf(b, red[w]);
+    const float sb = __fdiv_rn(b, 127.0f);
+    atomicMax(reinterpret_cast<unsigned int*>(pick_s(t, ti)) + head_of(p, H, h_magic), __float_as_uint(sb));
+  }
+}
+
+__global__ void __launch_bounds__(kQThreads)
+    quantize_per_head_kernel(QuantTensors t, int64_t vec_per_problem, int H, uint32_t h_magic) {
+  const int ti = blockIdx.z;
+  const int p = blockIdx.x;
+  const int h = head_of(p, H, h_magic);
+  float s = *reinterpret_cast<volatile float*>(pick_s(t, ti) + h);
+  if (s == 0.0f) s = 1.0f / 127.0f;  // all-zero head (R3)
+  if (p == h && blockIdx.y == 0 && threadIdx.x == 0) pick_s(t, ti)[h] = s;
+  const float r = __frcp_rn(s);
+  const float4* x = reinterpret_cast<const float4*>(pick(t, ti)) + static_cast<int64_t>(p) * vec_per_problem;
+  uint32_t* xq = reinterpret_cast<uint32_t*>(pick_q(t, ti)) + static_cast<int64_t>(p) * vec_per_problem;
+  const int64_t v0 = static_cast<int64_t>(blockIdx.y) * kQThreads * kPHVec + threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < kPHVec; ++u) {
+    const int64_t i = v0 + u * kQThreads;
+    if (i < vec_per_problem) {
+      const float4 v = __ldg(x + i);
+      int32_t q[4];
+      bool bad = false;
+      q[0] = quant_fast(v.x, r, bad);
+      q[1] = quant_fast(v.y, r, bad);
+      q[2] = quant_fast(v.z, r, bad);
+      q[3] = quant_fast(v.w, r, bad);
+      if (bad) {
+        q[0] = quant_exact(v.x, s);
+        q[1] = quant_exact(v.y, s);
+        q[2] = quant_exact(v.z, s);
+        q[3] = quant_exact(v.w, s);
+      }
+      uint32_t hi, lo;
+      asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(q[3]), "r"(q[2]));
+      asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(lo) : "r"(q[1]), "r"(q[0]), "r"(hi));
+      xq[i] = lo;
+    }
+  }
+}
+
+// Per-head integer constants: thread h derives head h's constants from
+// (s_q[h], s_k[h]) with derive_core (the fp64 expression of qflash_derive_params)
+// into table + kHeadPrmStride h; thread 0 then writes the header: status (first
+// failing head's), and q_shift / s_inv / m_p chosen so that the kernel's fast-path
+// test is true iff every head takes the fast quotient / requant path.
+__global__ void derive_per_head_kernel(const float* __restrict__ scales, int H, int32_t d,
+                                       char* __restrict__ ws) {
+  __shared__ int fast_all, status;
+  if (threadIdx.x == 0) {
+    fast_all = 1;
+    status = 0;
+  }
+  __syncthreads();
+  for (int h = threadIdx.x; h < H; h += blockDim.x) {
+    IntParams p;
+    const int st = derive_core(scales[h], scales[H + h], d, &p, nullptr);
+    if (st != QFLASH_OK) {
+      memset(&p, 0, sizeof(p));
+      p.status = st;
+      atomicCAS(&status, 0, st);
+    } else if (!(p.q_shift == 0 && static_cast<uint64_t>(p.s_inv) * static_cast<uint64_t>(p.m_p) < (1ull << 32))) {
+      atomicAnd(&fast_all, 0);
+    }
+    *reinterpret_cast<IntParams*>(ws + kHeadPrmOffset + kHeadPrmStride * h) = p;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    IntParams hdr;
+    memset(&hdr, 0, sizeof(hdr));
+    hdr.status = status;
+    hdr.q_shift = fast_all ? 0 : 1;
+    hdr.s_inv = 1;
+    hdr.m_p = 1;
+    hdr.one = 1;
+    *reinterpret_cast<IntParams*>(ws) = hdr;
+  }
+}
+
+__global__ void __launch_bounds__(kQThreads)
+    dequantize_per_head_kernel(const int8_t* __restrict__ xq, const float* __restrict__ scales,
+                               int64_t vec_per_problem, int H, uint32_t h_magic, float* __restrict__ y) {
+  const int p = blockIdx.x;
+  const float s = scales[head_of(p, H, h_magic)];
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(xq) + static_cast<int64_t>(p) * vec_per_problem;
+  float4* dst = reinterpret_cast<float4*>(y) + static_cast<int64_t>(p) * vec_per_problem;
+  const int64_t v0 = static_cast<int64_t>(blockIdx.y) * kQThreads * kPHVec + threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < kPHVec; ++u) {
+    const int64_t i = v0 + u * kQThreads;
+    if (i < vec_per_problem) {
+      const uint32_t w = __ldg(src + i);
+      dst[i] = make_float4(__fmul_rn(s, static_cast<float>(static_cast<int8_t>(w & 0xFF))),
+                           __fmul_rn(s, static_cast<float>(static_cast<int8_t>((w >> 8) & 0xFF))),
+                           __fmul_rn(s, static_cast<float>(static_cast<int8_t>((w >> 16) & 0xFF))),
+                           __fmul_rn(s, static_cast<float>(static_cast<int8_t>(w >> 24))));
+    }
+  }
+}
+
+cudaError_t launch_quantize_per_head(const QuantTensors& t, int ntensors, int64_t P,
+                                     int64_t vec_per_problem, int H, cudaStream_t stream) {
+  const uint32_t hm = static_cast<uint32_t>(((1ull << 32) + H - 1) / H);
+  for (int i = 0; i < ntensors; ++i) {
+    cudaError_t e = cudaMemsetAsync(t.scale[i], 0, sizeof(float) * H, stream);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid(static_cast<unsigned>(P),
+            static_cast<unsigned>((vec_per_problem + kQThreads * kPHVec - 1) / (kQThreads * kPHVec)),
+            ntensors);
+  amax_per_head_kernel<<<grid, kQThreads, 0, stream>>>(t, vec_per_problem, H, hm);
+  quantize_per_head_kernel<<<grid, kQThreads, 0, stream>>>(t, vec_per_problem, H, hm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_derive_per_head(const float* scales, int H, int32_t d, void* ws, cudaStream_t stream) {
+  derive_per_head_kernel<<<1, 128, 0, stream>>>(scales, H, d, static_cast<char*>(ws));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dequantize_per_head(const int8_t* xq, const float* scales, int64_t P,
+                                       int64_t vec_per_problem, int H, float* y, cudaStream_t stream) {
+  const uint32_t hm = static_cast<uint32_t>(((1ull << 32) + H - 1) / H);
+  dim3 grid(static_cast<unsigned>(P),
+            static_cast<unsigned>((vec_per_problem + kQThreads * kPHVec - 1) / (kQThreads * kPHVec)));
+  dequantize_per_head_kernel<<<grid, kQThreads, 0, stream>>>(xq, scales, vec_per_problem, H, hm, y);
+  return cudaGetLastError();
+}
+
 static int num_sms() {
   static int sms = 0;
   if (sms == 0) {

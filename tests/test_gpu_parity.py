@@ -427,3 +427,37 @@ def test_host_pipeline_overlapped_batches(orc):
         vq, sv = orc.quantize(v)
         ref = orc.dequantize(orc.attention(qq, kq, vq, sq, sk), sv)
         assert np.array_equal(o.numpy().view(np.uint32), ref.view(np.uint32))
+
+
+# ------------------------------------------------------- per-head granularity (N1)
+def _head_spread(q, k, v, H, spread=1.5):
+    gains = np.exp(np.linspace(-spread, spread, H)).astype(np.float32)
+    g = np.tile(gains, q.shape[0] // H)[:, None, None]
+    return q * g, k * g, v * g
+
+
+@pytest.mark.parametrize("name,batch,H", [("A1", 1, 3), ("A3", 8, 12), ("A4", 8, 3),
+                                          ("SwinB-s3", 1, 16), ("L14", 1, 16)])
+def test_per_head_path_bit_exact(orc, name, batch, H):
+    q, k, v = _head_spread(*gen_workload(name, batch, seed=3), H)
+    dq, dk, dv = _dev(q, k, v)
+    y, o, scales, ws = qf.qflash_forward_per_head(dq, dk, dv, H)
+    torch.cuda.synchronize()
+    assert int(ws[0].item()) == 0
+    qh, sq = orc.quantize_per_head(q, H)
+    kh, sk = orc.quantize_per_head(k, H)
+    vh, sv = orc.quantize_per_head(v, H)
+    assert np.array_equal(scales.cpu().numpy(), np.concatenate([sq, sk, sv]))
+    o_ref = orc.attention_per_head(qh, kh, vh, sq, sk, H, nthreads=8)
+    assert np.array_equal(o.cpu().numpy(), o_ref)
+    ref = orc.dequantize_per_head(o_ref, sv, H)
+    assert np.array_equal(y.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+def test_per_head_one_head_equals_per_tensor(orc):
+    q, k, v = gen_workload("A2", 1, seed=4)
+    dq, dk, dv = _dev(q, k, v)
+    y, _, _, _ = qf.qflash_forward_per_head(dq, dk, dv, 1)
+    y_t = qf.qflash_forward(dq, dk, dv)
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(torch.int32), y_t.view(torch.int32))
