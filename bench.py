@@ -238,6 +238,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mode", default="fused", choices=["fused", "two", "three"],
                     help="step form: one cooperative launch (default), or 2 / 3 launches")
+    ap.add_argument("--scales", default="per-tensor", choices=["per-tensor", "per-head"],
+                    help="granularity (per-head = SURVEY 8(f) N1; 5 launches per step)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -276,8 +278,13 @@ def main():
         # distinct bytes per set (sign flips keep the distribution and the scales)
         sgn = -1.0 if (i % 2) else 1.0
         sets.append([(t * sgn).roll(shifts=i, dims=1).contiguous() for t in base])
-    pipes = [qfl.QFlashPipeline(P_local, N, d, block_kv=args.block_kv, device=dev, mode=args.mode)
-             for _ in range(n_sets)]
+    if args.scales == "per-head":
+        pipes = [qfl.QFlashPerHeadPipeline(P_local, N, d, w.heads, block_kv=args.block_kv, device=dev)
+                 for _ in range(n_sets)]
+        args.no_e2e = True
+    else:
+        pipes = [qfl.QFlashPipeline(P_local, N, d, block_kv=args.block_kv, device=dev, mode=args.mode)
+                 for _ in range(n_sets)]
 
     stream = torch.cuda.Stream(device=dev)
     graphs = []
@@ -335,6 +342,7 @@ def main():
     # step is one launch, else the attention kernel with the fused dequantize
     k_launch = min(args.steps, 2000)
     one_launch = pipes[0].launches() == 1
+    per_head = args.scales == "per-head"
     ka, kb = [], []
     with torch.cuda.stream(stream):
         # head start covering the host cost of every eager launch (<= 50 us each),
@@ -346,6 +354,8 @@ def main():
             a.record(stream)
             if one_launch:
                 p(*sets[i % n_sets], stream=stream)
+            elif per_head:
+                p.attention(stream=stream)
             else:
                 qfl.qflash_attention_dequant_prepared(p.qkv_q[0], p.qkv_q[1], p.qkv_q[2],
                                                       p.workspace, args.block_kv, out=p.out,
@@ -358,7 +368,7 @@ def main():
     attn_ms = statistics.mean(durs[: max(1, int(0.9 * len(durs)))])  # drop the slowest 10 %
 
     # ---- for context: the two-launch form of the step, stage by stage (eager)
-    k_bd = min(args.steps, 500)
+    k_bd = 0 if per_head else min(args.steps, 500)
     evs = []
     with torch.cuda.stream(stream):
         torch.cuda._sleep(int(k_bd * 120e-6 * 2.0e9))
@@ -376,14 +386,15 @@ def main():
             evs.append(e)
     torch.cuda.synchronize()
     def _med(a, b):
-        return statistics.median(x[a].elapsed_time(x[b]) for x in evs) * 1e3
+        return statistics.median(x[a].elapsed_time(x[b]) for x in evs) * 1e3 if evs else None
     breakdown = {"two_launch_quantize_qkv_us": _med(0, 1), "two_launch_attention_dequant_us": _med(1, 2),
                  "note": "eager launches, GPU kept busy; medians over %d steps" % k_bd}
     # share of the step (the ncu launch list must agree on this share)
     attn_share = attn_ms / ms_per_step
     launches_per_step = pipes[0].launches()
 
-    kbytes = alg["fused_step_bytes"] if one_launch else alg["attn_dq_bytes"]
+    kbytes = (alg["fused_step_bytes"] if one_launch else alg["attn_bytes"] if per_head
+              else alg["attn_dq_bytes"])
     pk = peaks()
     sm_clk_ghz = (pk.get("sm_max_mhz") or 1965.0) / 1e3
     alu_peak = SMS * INT32_LANES * sm_clk_ghz * 1e9 / 1e12      # T int32 ops/s
@@ -391,7 +402,8 @@ def main():
     int8_peak_tops = 2.0 * pk.get("bf16_tflops", 1674.9)          # measured bf16 x nominal 2x
     roofline = {
         "kernel": ("qflash_attn_kernel<FQ> (fused step: quantize prologue + attention + dequantize)"
-                   if one_launch else "qflash_attn_kernel (fused dequantize epilogue)"),
+                   if one_launch else "derive_per_head + qflash_attn_kernel<PH> (int8 out)" if per_head
+                   else "qflash_attn_kernel (fused dequantize epilogue)"),
         "bound": "alu", "achieved": alu_achieved,
         "peak": alu_peak, "unit": "T int32-op/s", "frac": alu_achieved / alu_peak,
         "traffic": None,
@@ -408,12 +420,13 @@ def main():
                 "frac": kbytes / (attn_ms * 1e-3) / 1e9 / pk.get("hbm_gbs", 6452.5),
                 "bytes_per_launch": kbytes,
                 "per_unit": "16 N d B per problem (fp32 Q, K, V in + fp32 O out)" if one_launch
+                            else "4 N d B per problem (int8 Q, K, V in + int8 O out)" if per_head
                             else "7 N d B per problem (int8 Q, K, V in + fp32 O out)"},
     }
     traffic_file = os.path.join(ROOT, "profiles", "attn_traffic.json")
     if os.path.exists(traffic_file):
         try:
-            tj = json.load(open(traffic_file)).get(f"{name}_b{batch}" + ("_fused" if one_launch else ""))
+            tj = json.load(open(traffic_file)).get(f"{name}_b{batch}" + ("_fused" if one_launch else "_ph" if per_head else ""))
             if tj:
                 roofline["traffic"] = tj
         except Exception:
@@ -482,7 +495,10 @@ def main():
                        "problems_per_rank": P_local, "seq_len": N, "head_dim": d,
                        "block_kv": args.block_kv, "parallelism": f"independent problems x{world}",
                        "step": ("qflash_forward_fused (CUDA graph, 1 cooperative launch)" if launches_per_step == 1
+                                else "per-head quantize + derive + attention + dequantize (CUDA graph)"
+                                if args.scales == "per-head"
                                 else "quantize_qkv_prepare + attention_dequant_prepared (CUDA graph)"),
+                       "scales": args.scales,
                        "l2": f"rotating {n_sets} input sets ({n_sets * set_bytes / 2**20:.0f} MiB > 2x L2)"},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

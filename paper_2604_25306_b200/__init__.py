@@ -3,14 +3,14 @@
 The product is libqflash.so (C ABI, include/qflash.h); this package is its thin
 Python binding (argument marshalling only) plus the seeded synthetic inputs.
 """
-from .api import (QFlashHostPipeline, QFlashPipeline, qflash_attention_int8, qflash_attention_int8_dscale,
+from .api import (QFlashHostPipeline, QFlashPerHeadPipeline, QFlashPipeline, qflash_attention_int8, qflash_attention_int8_dscale,
                   qflash_attention_int8_prepared, qflash_quantize_qkv_prepare,
                   qflash_attention_dequant_prepared, qflash_forward_fused,
                   qflash_forward_per_head,
                   qflash_dequantize, qflash_derive_params, qflash_forward, qflash_partition,
                   qflash_quantize_per_tensor, qflash_quantize_qkv)
 
-__all__ = ["QFlashHostPipeline", "QFlashPipeline", "qflash_attention_int8", "qflash_attention_int8_dscale",
+__all__ = ["QFlashHostPipeline", "QFlashPerHeadPipeline", "QFlashPipeline", "qflash_attention_int8", "qflash_attention_int8_dscale",
            "qflash_attention_int8_prepared", "qflash_quantize_qkv_prepare",
            "qflash_attention_dequant_prepared", "qflash_forward_fused", "qflash_forward_per_head",
            "qflash_dequantize", "qflash_derive_params", "qflash_forward", "qflash_partition",

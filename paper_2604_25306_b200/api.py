@@ -261,6 +261,51 @@ def qflash_forward_per_head(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, h
     return y, o, scales, ws
 
 
+class QFlashPerHeadPipeline:
+    """qflash_forward_per_head with preallocated buffers (graph-capturable): per-head
+    quantize (amax + quantize), constant derivation + attention, dequantize."""
+
+    def __init__(self, P: int, N: int, d: int, heads: int, block_kv: int = 128, device="cuda",
+                 variant: str = "auto"):
+        dev = torch.device(device)
+        self.shape, self.heads, self.block_kv, self.variant = (P, N, d), heads, block_kv, variant
+        self.codes = [torch.empty(self.shape, dtype=torch.int8, device=dev) for _ in range(3)]
+        self.scales = torch.empty(3 * heads, dtype=torch.float32, device=dev)
+        self.o_q = torch.empty(self.shape, dtype=torch.int8, device=dev)
+        self.workspace = torch.empty(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=dev)
+        self.out = torch.empty(self.shape, dtype=torch.float32, device=dev)
+
+    def launches(self, dtype=torch.float32) -> int:
+        return 5  # amax, quantize, derive, attention, dequantize
+
+    def __call__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, stream=None):
+        P, N, d = self.shape
+        H = self.heads
+        c = self.codes
+        check(lib().qflash_quantize_per_head(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v), P, N, d, H,
+                                             _dev_ptr(c[0]), _dev_ptr(c[1]), _dev_ptr(c[2]),
+                                             _dev_ptr(self.scales), _stream(stream)))
+        shape = AttnShape(P, N, d, self.block_kv)
+        check(lib().qflash_attention_int8_per_head(_dev_ptr(c[0]), _dev_ptr(c[1]), _dev_ptr(c[2]),
+                                                   _dev_ptr(self.scales), H, ctypes.byref(shape),
+                                                   _lib.VARIANTS[self.variant], _dev_ptr(self.o_q),
+                                                   _dev_ptr(self.workspace), _stream(stream)))
+        check(lib().qflash_dequantize_per_head(_dev_ptr(self.o_q), _dev_ptr(self.scales[2 * H:]),
+                                               P, N, d, H, _dev_ptr(self.out), _stream(stream)))
+        return self.out
+
+    def attention(self, stream=None):
+        """The attention stage alone (constant derivation + Algorithm 1) on the codes."""
+        P, N, d = self.shape
+        c = self.codes
+        shape = AttnShape(P, N, d, self.block_kv)
+        check(lib().qflash_attention_int8_per_head(_dev_ptr(c[0]), _dev_ptr(c[1]), _dev_ptr(c[2]),
+                                                   _dev_ptr(self.scales), self.heads, ctypes.byref(shape),
+                                                   _lib.VARIANTS[self.variant], _dev_ptr(self.o_q),
+                                                   _dev_ptr(self.workspace), _stream(stream)))
+        return self.o_q
+
+
 class QFlashHostPipeline:
     """Serving loop over host (pinned) fp32 batches: each call copies one batch in,
     runs the whole hot path (QFlashPipeline) and copies the fp32 result back, all
