@@ -238,6 +238,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mode", default="fused", choices=["fused", "two", "three"],
                     help="step form: one cooperative launch (default), or 2 / 3 launches")
+    ap.add_argument("--variant", default="auto", choices=["auto", "generic", "packed"],
+                    help="attention tiling (auto: row-packed when it saves a wave)")
     ap.add_argument("--scales", default="per-tensor", choices=["per-tensor", "per-head"],
                     help="granularity (per-head = SURVEY 8(f) N1; 5 launches per step)")
     args = ap.parse_args()
@@ -283,7 +285,8 @@ def main():
                  for _ in range(n_sets)]
         args.no_e2e = True
     else:
-        pipes = [qfl.QFlashPipeline(P_local, N, d, block_kv=args.block_kv, device=dev, mode=args.mode)
+        pipes = [qfl.QFlashPipeline(P_local, N, d, block_kv=args.block_kv, device=dev, mode=args.mode,
+                                    variant=args.variant)
                  for _ in range(n_sets)]
 
     stream = torch.cuda.Stream(device=dev)
@@ -358,8 +361,8 @@ def main():
                 p.attention(stream=stream)
             else:
                 qfl.qflash_attention_dequant_prepared(p.qkv_q[0], p.qkv_q[1], p.qkv_q[2],
-                                                      p.workspace, args.block_kv, out=p.out,
-                                                      stream=stream)
+                                                      p.workspace, args.block_kv, args.variant,
+                                                      out=p.out, stream=stream)
             b.record(stream)
             ka.append(a)
             kb.append(b)

@@ -75,6 +75,9 @@ constexpr int kBlockR = 128;
 
 // Sleep (ns) between barrier probes of the waits off the critical path
 // (experiment builds override with -D).
+#ifndef QF_KVR
+#define QF_KVR 4
+#endif
 #ifndef QF_SLEEP_CORR
 #define QF_SLEEP_CORR 128
 #endif
@@ -109,7 +112,15 @@ struct Cfg {
   // buffer j: segment s at columns [s BC/4, (s+1) BC/4)), then O (D columns),
   // l (column D) and 15 copies of l from the ones block.
   static constexpr int kNumS = (QT == 1 && 2 * BC + D + 16 <= 512) ? 2 : 1;
-  static constexpr int kGroupCols = kNumS * BC + D + 16;
+  // Separate P region (CS = 2, QT = 2, generic tiles, when TMEM allows): P lives
+  // in its own B_c/4 columns instead of aliasing S, so the next Q K^T may overwrite
+  // S as soon as the softmax warps have read it (s_empty), overlapping the round
+  // trip with the P arithmetic and the release instead of following P V.
+  static constexpr bool kSepP =
+      CS == 2 && QT == 2 && NSEG == 1 && QT * (BC + BC / 4 + D + 16) <= 512;
+  static constexpr int kPCol = kNumS * BC;                         // P region (kSepP)
+  static constexpr int kOCol = kNumS * BC + (kSepP ? BC / 4 : 0);  // O (+ l, ones copies)
+  static constexpr int kGroupCols = kOCol + D + 16;
   static constexpr uint32_t kTmemCols = tmem_cols_pow2(QT * kGroupCols);
   // shared memory (offsets from the 1024-aligned base)
   static constexpr int kQBytes = kBlockR * D;
@@ -119,7 +130,7 @@ struct Cfg {
   static constexpr int kK = 2 * NSEG * kQBytes;              // [kStages][NSEG]
   static constexpr int kV = kK + kStages * NSEG * kKVBytes;  // [kStages][NSEG]
   static constexpr int kOnes = QT * kGroupSmem;              // second MN atom of [V | 1]
-  static constexpr int kBarsPerGroup = 2 * kStages + 4 + kNumS + 6;
+  static constexpr int kBarsPerGroup = 2 * kStages + 4 + kNumS + 7;
   static constexpr int kBar = kOnes + BC * D;
   static constexpr int kTmemSlot = kBar + QT * kBarsPerGroup * 8;
   static constexpr int kRed = (kTmemSlot + 16 + 15) / 16 * 16;  // [QT][2][CS][128] int32
@@ -140,7 +151,7 @@ constexpr bool config_fits() {
          (BC / CS == 16 || BC / CS == 32 || BC / CS == 64 || (CS == 1 && BC == 128)) &&
          ((D / CS) % 8 == 0) &&
          (NSEG * (BC / 4) <= BC) &&
-         (QT * (2 * NSEG * kBlockR * D + 2 * kStages * NSEG * BC * D) + BC * D + 64 * 10 +
+         (QT * (2 * NSEG * kBlockR * D + 2 * kStages * NSEG * BC * D) + BC * D + 64 * 11 +
               QT * 2 * CS * 512 + 5120 + 640 + 2048 <=
           227 * 1024);
 }
@@ -162,6 +173,7 @@ struct GroupBars {
   QF_DEV uint64_t* o_full() const { return base + 2 * kStages + 6 + NUMS; }
   QF_DEV uint64_t* alpha_full(int b) const { return base + 2 * kStages + 7 + NUMS + b; }
   QF_DEV uint64_t* rel_full() const { return base + 2 * kStages + 9 + NUMS; }
+  QF_DEV uint64_t* s_empty() const { return base + 2 * kStages + 10 + NUMS; }  // kSepP
 };
 
 
@@ -428,7 +440,8 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
   const int row = quarter * 32 + lane;  // TMEM lane == tile row
   const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
   const uint32_t tS0 = tmem_group + lane_off;  // S buffer b at + b * BC
-  const uint32_t tO = tS0 + C::kNumS * BC;
+  const uint32_t tO = tS0 + C::kOCol;
+  const uint32_t tP = tS0 + C::kPCol;  // kSepP
   const int c0 = c * CW;  // first key column of this thread
   const bool dbg_on = DBG && blockIdx.x == 0 && g == 0;
   const bool ts_warp = dbg_on && c == 0 && quarter == 0 && lane == 0;
@@ -451,7 +464,7 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
     const int nseg = ti.nseg;
     int32_t m = -(1 << 21);  // m^(0) = -2^21
     IntParams prm_t;
-    RowConsts rct;
+    RowConsts rct = rck;
     if constexpr (PH) {
       prm_t = head_params(args, ti.problem + seg);
       rct = row_consts(prm_t, Tc);
@@ -584,7 +597,18 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
           }
         }
       }
-      if (nseg == 1) {
+      if constexpr (C::kSepP) {
+        // every S read of this warp is done: the next Q K^T may overwrite S; P goes
+        // to its own region once P V_{j-1} has read the previous P (o_full)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(gb.s_empty());
+        if (j > 0) {
+          mbar_wait(gb.o_full(), (it - 1) & 1);
+          tc_fence_after();
+        }
+        tmem_st<CW / 4>(tP + c * (CW / 4), pk);
+      } else if (nseg == 1) {
         tmem_st<CW / 4>(tS + p_col<BC, CW>(c, 0), pk);
       } else {
         // segment s gets this row's P if the row belongs to it, zeros otherwise
@@ -606,8 +630,10 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
       // all kept their maximum (alpha = s_inv is the identity, R10).  P V_j is
       // issued only after every warp's p_full arrival below, i.e. after the release.
       if (j > 0) {
-        mbar_wait(gb.o_full(), (it - 1) & 1);
-        tc_fence_after();
+        if constexpr (!C::kSepP) {
+          mbar_wait(gb.o_full(), (it - 1) & 1);
+          tc_fence_after();
+        }
         if (dbg && ts_warp && j < 7) QF_TS(45 + 8 * j);
         if (warp_live && __any_sync(0xffffffffu, alpha != prm.s_inv)) {
           uint32_t o[OW];
@@ -914,7 +940,7 @@ __device__ __forceinline__ void correction_role(const AttnArgs& args, const IntP
   const int N = args.N;
   const int Tc = args.Tc;
   const int row = quarter * 32 + lane;
-  const uint32_t tO = tmem_group + (static_cast<uint32_t>(quarter * 32) << 16) + C::kNumS * BC;
+  const uint32_t tO = tmem_group + (static_cast<uint32_t>(quarter * 32) << 16) + C::kOCol;
   const int sinv_log2 = 31 - __clz(prm.s_inv);
   int32_t rel_lthr;
   {
@@ -1091,7 +1117,7 @@ template <int D>
 __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float* scratch,
                                                        IntParams* sprm, uint32_t* dq_table) {
   namespace cg = cooperative_groups;
-  constexpr int kVR = 4;  // register-resident 16-B vectors per tensor and thread
+  constexpr int kVR = QF_KVR;  // register-resident 16-B vectors per tensor and thread
   QF_FQ_TS(a, 0);
   // Warp 0 moves no data: its lane 0 derives the integer constants (~1-2 us of
   // fp64 / 64-bit integer work) while warps 1.. quantize, off the critical path.
@@ -1278,6 +1304,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
       }
       mbar_init(gb.o_full(), 1);
       mbar_init(gb.rel_full(), 4);
+      mbar_init(gb.s_empty(), C::kGroupThreads / 32);
     }
     fence_barrier_init();
   }
@@ -1404,7 +1431,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
       if (g < QT && lane == 0) {
         const Bars gb{bars + g * C::kBarsPerGroup};
         const uint32_t tG = tmem_base + g * C::kGroupCols;
-        const uint32_t tO = tG + C::kNumS * BC;
+        const uint32_t tO = tG + C::kOCol;
         const uint32_t ones_addr = smem_u32(sOnes);
         uint8_t* sQ = smem + g * C::kGroupSmem + C::kQ;
         uint8_t* sK = smem + g * C::kGroupSmem + C::kK;
@@ -1423,6 +1450,9 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
             const int st = it % kStages;
             const int sb = (C::kNumS == 2) ? (it & 1) : 0;
             mbar_wait(gb.kv_full(st), (it / kStages) & 1);
+            if constexpr (C::kSepP) {
+              if (it > 0) mbar_wait(gb.s_empty(), (it - 1) & 1);  // S_{it-1} read by every softmax warp
+            }
             tc_fence_after();
             if (ti.i == 0 && blockIdx.x == 0 && g == 0 && j < 7) QF_TS(3 + 4 * j);
             // (1) S = sum_s Q_s K_{s,j}^T : M=128, N=BC, K=D in steps of 32 bytes.
@@ -1458,7 +1488,8 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
               for (int kk = 0; kk < BC / 32; ++kk) {
                 const uint32_t vk = v_addr + 32 * kk * D;
                 const uint64_t db = make_smem_desc(vk, ones_addr - v_addr, 8 * D, kSwz);
-                mma_i8_ts(tO, tG + sb * BC + p_col_k<BC, C::kCW>(kk, s), db, kIdescPV,
+                mma_i8_ts(tO, C::kSepP ? tG + C::kPCol + 8 * kk : tG + sb * BC + p_col_k<BC, C::kCW>(kk, s),
+                          db, kIdescPV,
                           (j > 0 || s > 0 || kk > 0) ? 1u : 0u);
               }
             }
@@ -1467,9 +1498,9 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
           };
           issue_qk(0);
           for (int j = 0; j < Tc; ++j) {
-            if (C::kNumS == 2 && j + 1 < Tc) issue_qk(j + 1);
+            if ((C::kNumS == 2 || C::kSepP) && j + 1 < Tc) issue_qk(j + 1);
             issue_pv(j);
-            if (C::kNumS == 1 && j + 1 < Tc) issue_qk(j + 1);
+            if (C::kNumS == 1 && !C::kSepP && j + 1 < Tc) issue_qk(j + 1);
           }
         }
         // every MMA of this group is issued: let the next grid (dequantize) be

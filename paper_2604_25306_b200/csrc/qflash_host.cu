@@ -250,7 +250,13 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   const int64_t waves_packed = (tiles_packed + sms - 1) / sms;
   bool packed;
   switch (variant) {
-    case QFLASH_VARIANT_AUTO: packed = packable && waves_packed < waves_generic; break;
+    case QFLASH_VARIANT_AUTO:
+      // one wave: pack when it saves a wave (A3 b8: 192 -> 148 tiles); several waves:
+      // generic tiles get configuration 1's separate P region (measured L14 b64: 802 us
+      // generic vs 844 us packed), so pack only for a large tile saving (Swin windows)
+      packed = packable && (tiles_generic > sms ? tiles_packed * 100 < tiles_generic * 85
+                                                : waves_packed < waves_generic);
+      break;
     case QFLASH_VARIANT_GENERIC: packed = false; break;
     case QFLASH_VARIANT_PACKED:
       if (!packable)
