@@ -76,6 +76,11 @@ QF_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
 QF_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 QF_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Whole-cluster barrier with release / acquire semantics (all threads of every CTA).
+QF_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 QF_DEV long long globaltimer_ns() {
   long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -1174,7 +1174,8 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   }
   QF_FQ_TS(a, 1);
   __threadfence();
-  cg::this_grid().sync();
+  if (a.cluster_grid) cluster_sync_all();
+  else cg::this_grid().sync();
   QF_FQ_TS(a, 2);
   // 2. global scales (every CTA, identical): s = fl32(amax / 127), R3 for zeros
   if (warp < 3) {
@@ -1247,7 +1248,8 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   QF_FQ_TS(a, 4);
   fence_proxy_async_global();
   __threadfence();
-  cg::this_grid().sync();
+  if (a.cluster_grid) cluster_sync_all();
+  else cg::this_grid().sync();
   fence_proxy_async_global();
   QF_FQ_TS(a, 5);
 }
@@ -1592,6 +1594,34 @@ cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CU
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   if constexpr (FQ) {
+    // small grids (<= 8 CTAs portable; up to 16 where the GPU schedules it): launch
+    // the grid as ONE thread-block cluster -- its
+    // CTAs are co-scheduled and barrier.cluster (hardware) replaces the two grid
+    // barriers of the quantize prologue; falls back to the cooperative launch
+    static int cluster_env = -2;
+    if (cluster_env == -2) {
+      const char* env = getenv("QFLASH_FUSED_CLUSTER");
+      cluster_env = (env != nullptr && env[0] == '0') ? 0 : 1;
+    }
+    if (cluster_env && G <= 16) {
+      static int nonportable[16] = {0};
+      if (G > 8 && dev >= 0 && dev < 16 && !nonportable[dev]) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)
+          nonportable[dev] = 1;
+      }
+      cudaLaunchAttribute ca[1];
+      ca[0].id = cudaLaunchAttributeClusterDimension;
+      ca[0].val.clusterDim.x = static_cast<unsigned>(G);
+      ca[0].val.clusterDim.y = 1;
+      ca[0].val.clusterDim.z = 1;
+      cudaLaunchConfig_t ccfg = cfg;
+      ccfg.attrs = ca;
+      ccfg.numAttrs = 1;
+      AttnArgs cargs = args;
+      cargs.cluster_grid = 1;
+      if (cudaLaunchKernelEx(&ccfg, kern, tq, tk, tv, cargs) == cudaSuccess) return cudaSuccess;
+      (void)cudaGetLastError();  // cluster shape not schedulable here: cooperative launch
+    }
     // fused step: grid barriers in the quantize prologue need every CTA resident;
     // programmatic serialization lets the next step's grid be launched (and run its
     // setup) while this one drains -- griddep_wait() precedes every global access

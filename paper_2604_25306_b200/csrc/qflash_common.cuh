@@ -58,6 +58,9 @@ struct AttnArgs {
   const IntParams* head_prm;  // device table, kHeadPrmStride bytes per head
   int32_t H;
   uint32_t h_magic;           // ceil(2^32 / H): problem / H = umulhi(problem, h_magic)
+  int32_t cluster_grid;       // fused step: 1 = the grid is one thread-block cluster
+                              // (barrier.cluster replaces the grid barriers)
+  int32_t pad2;
   // bring-up dumps for CTA 0's first tile only; nullptr in production:
   int32_t* dbg_s;  // [128][BC] raw S of KV tile 0
   int32_t* dbg_p;  // [128][BC/4] packed P words of KV tile 0

@@ -13,7 +13,7 @@ from paper_2604_25306_b200.inputs import CATALOG, gen_real_qkv  # noqa: E402
 
 names = {8: "entry", 0: "prologue", 1: "amax", 2: "sync1", 3: "constants", 4: "quantized",
          5: "sync2", 9: "teardown"}
-for wl, b in [("A3", 8), ("A1", 1)]:
+for wl, b in [("A3", 8), ("A4", 8), ("A1", 1)]:
     w = CATALOG[wl]
     P, N, d = w.problems(b), w.seq_len, w.head_dim
     base = [torch.from_numpy(x).cuda() for x in gen_real_qkv(P, N, d, seed=0, family=w.family)]
