@@ -44,9 +44,25 @@ using u128 = unsigned __int128;
 
 // smallest L with 2^L >= x (x >= 1)
 __host__ __device__ inline int ceil_log2(uint64_t x) {
+#ifdef __CUDA_ARCH__
+  return x <= 1 ? 0 : 64 - __clzll(x - 1);
+#else
   int L = 0;
   while ((uint64_t(1) << L) < x) ++L;
   return L;
+#endif
+}
+// sqrt(d) of Alg. 1's s = s_q s_k log2(e) / sqrt(d): the device uses the
+// correctly rounded fp64 constants for the supported d (identical to IEEE sqrt).
+__host__ __device__ inline double sqrt_head_dim(int32_t d) {
+#ifdef __CUDA_ARCH__
+  if (d == 32) return 5.65685424949238058190;   // RN(sqrt(32)) = 0x4016A09E667F3BCD
+  if (d == 64) return 8.0;
+  if (d == 128) return 11.3137084989847611638;  // RN(sqrt(128)) = 0x4026A09E667F3BCD
+  return dsqrt(static_cast<double>(d));
+#else
+  return std::sqrt(static_cast<double>(d));
+#endif
 }
 
 __host__ __device__ inline int derive_core(float s_q, float s_k, int32_t d, qf::IntParams* o,
@@ -55,7 +71,7 @@ __host__ __device__ inline int derive_core(float s_q, float s_k, int32_t d, qf::
     return QFLASH_ERR_SCALE_RANGE;
   const double log2e = 1.4426950408889634;
   const double s = ddiv(dmul(dmul(static_cast<double>(s_q), static_cast<double>(s_k)), log2e),
-                        dsqrt(static_cast<double>(d)));
+                        sqrt_head_dim(d));
   if (!(s >= ldexp(1.0, -24)) || !(s <= 0.5)) return QFLASH_ERR_SCALE_RANGE;
   const int64_t s_inv = llround(ddiv(1.0, s));  // round half away (R1)
   const double ratio = dmul(s, 127.0);          // s / s_P, s_P = 1/127 (R8)

@@ -461,3 +461,28 @@ def test_per_head_one_head_equals_per_tensor(orc):
     y_t = qf.qflash_forward(dq, dk, dv)
     torch.cuda.synchronize()
     assert torch.equal(y.view(torch.int32), y_t.view(torch.int32))
+
+
+@pytest.mark.parametrize("d", [32, 64, 128])
+def test_device_constants_equal_host_constants(d):
+    # the device derivation (derive_core on the GPU: fp64 with explicit rounding,
+    # 64-bit magics, sqrt(d) constants) equals the host's field by field
+    rng = np.random.default_rng(d)
+    q = torch.zeros((1, 2, d), dtype=torch.int8, device="cuda")
+    for _ in range(24):
+        sq, sk = (float(np.float32(10.0 ** rng.uniform(-3.6, -0.4))) for _ in range(2))
+        try:
+            hp = qf.qflash_derive_params(sq, sk, d)
+        except _lib.QFlashError:
+            continue
+        scales = torch.tensor([sq, sk, 0.05], dtype=torch.float32, device="cuda")
+        _, ws = qf.qflash_attention_int8_dscale(q, q, q, scales)
+        torch.cuda.synchronize()
+        w = ws.cpu().numpy()
+        s_dev = ws[16:18].cpu().numpy().view(np.float64)[0]
+        rel = (int(np.uint32(w[7])) << 32) | int(np.uint32(w[6]))
+        assert (w[0], w[1], np.uint32(w[2]), w[3], np.uint32(w[4]), w[5]) == (
+            0, hp["s_inv"], hp["q_magic"], hp["q_shift"], hp["p_mul"], hp["p_pre"])
+        assert (rel, w[8], w[9], w[10], w[11], w[12]) == (
+            hp["rel_magic"], hp["rel_shift"], hp["p_max"], hp["r_p"], hp["m_p"], hp["n"])
+        assert s_dev == hp["s"]
