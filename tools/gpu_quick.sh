@@ -1,3 +1,5 @@
-./tools/derive_bench | tee gpurun_out/derive.txt
-timeout 400 python -m pytest tests -m gpu -q -x --timeout 120 2>&1 | tail -2 | tee gpurun_out/pytest.log
-timeout 120 python bench.py --no-cpu-baseline --no-e2e 2>&1 | tail -1 > gpurun_out/bench_a3.log
+for wl in "A1 1" "A3 8" "A1 1" "A3 8"; do
+  set -- $wl
+  timeout 120 python bench.py --workload $1 --batch $2 --steps 2000 --no-cpu-baseline --no-e2e 2>&1 | tail -1 >> gpurun_out/bench_chk_$1.log
+done
+QFLASH_FUSED_CLUSTER=0 timeout 120 python bench.py --workload A1 --batch 1 --steps 2000 --no-cpu-baseline --no-e2e 2>&1 | tail -1 >> gpurun_out/bench_chk_A1nocl.log
