@@ -525,7 +525,10 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
       if constexpr (CS > 1) {
         const uint32_t rb = red_group + static_cast<uint32_t>((it & 1) * (CS * 128) * 4);
         sts32(rb + static_cast<uint32_t>((c * 128 + row) * 4), tmax);
-        named_bar_sync(1 + g, C::kGroupThreads);
+        // only the CS warps that share this warp's TMEM lane quarter (the same 32
+        // rows) exchange maxima, and only their S / P columns alias: one named
+        // barrier per (group, lane quarter) of CS x 32 threads
+        named_bar_sync(1 + g * 4 + quarter, CS * 32);
 #pragma unroll
         for (int h = 0; h < CS; ++h)
           if (h != c) tmax = max(tmax, lds32(rb + static_cast<uint32_t>((h * 128 + row) * 4)));
@@ -673,7 +676,7 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
       tmem_wait_st();
       if constexpr (DBG) {
         if (args.dbg_p != nullptr && dbg && j == 0) {
-          if constexpr (CS > 1) named_bar_sync(1 + g, C::kGroupThreads);
+          if constexpr (CS > 1) named_bar_sync(1 + g * 4 + quarter, CS * 32);
           if (c == 0) {
             for (int kk = 0; kk < BC / 32; ++kk) {
               uint32_t pw[8];
