@@ -213,6 +213,31 @@ def test_empty_inputs():
         assert e.value.status == _lib.QFLASH_ERR_UNSUPPORTED_SHAPE
 
 
+def test_full_size_l14_b64_fused_step_sampled(orc):
+    # configs[4] through the one-launch fused step (the bench's default step form):
+    # codes, scales and sampled rows of the fp32 output against the oracle
+    w = CATALOG["L14"]
+    P = w.problems(64)
+    q, k, v = gen_real_qkv(P, w.seq_len, w.head_dim, seed=1)
+    pipe = qf.QFlashPipeline(P, w.seq_len, w.head_dim, mode="fused")
+    y = pipe(*_dev(q, k, v))
+    torch.cuda.synchronize()
+    assert int(pipe.workspace[0].item()) == 0
+    qq, sq = orc.quantize(q)
+    kq, sk = orc.quantize(k)
+    vq, sv = orc.quantize(v)
+    assert [pipe.scales[i].item() for i in range(3)] == [np.float32(x) for x in (sq, sk, sv)]
+    for t, ref in enumerate((qq, kq, vq)):
+        assert np.array_equal(pipe.qkv_q[t].cpu().numpy(), ref)
+    got = y.cpu().numpy()
+    rng = np.random.default_rng(1)
+    for p in list(rng.integers(0, P, 5)) + [0, P - 1]:
+        for (a, b) in [(0, 2), (127, 129), (1023, 1025)]:
+            o = orc.attention_rows(qq, kq, vq, sq, sk, int(p), a, b)
+            ref = orc.dequantize(o, sv)
+            assert np.array_equal(got[p, a:b].view(np.uint32), ref.view(np.uint32)), (p, a)
+
+
 # ------------------------------------------------------------------ quantizer
 @pytest.mark.parametrize("n", [1, 3, 16, 1000, 4099, 1 << 20, 1_210_368])
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
