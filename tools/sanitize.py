@@ -21,3 +21,10 @@ for (N, d, P, var) in [(197, 64, 4, "packed"), (300, 64, 3, "generic"), (49, 32,
 q, k, v = gen_workload("A1", 1, seed=0)
 y = qf.qflash_forward(*(torch.from_numpy(x) for x in (q, k, v)))
 print("parity", ok)
+# per-head path and the two-launch pipeline
+q, k, v = gen_workload("A4", 1, seed=2)
+dq, dk, dv = (torch.from_numpy(x).cuda() for x in (q, k, v))
+y, o, sc, ws = qf.qflash_forward_per_head(dq, dk, dv, 3)
+y2 = qf.QFlashPipeline(*q.shape, mode="two")(dq, dk, dv)
+torch.cuda.synchronize()
+print("per-head status", int(ws[0].item()))
