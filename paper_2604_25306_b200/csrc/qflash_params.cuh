@@ -42,6 +42,30 @@ __host__ __device__ inline double dsqrt(double a) {
 
 using u128 = unsigned __int128;
 
+// floor(N / D) and N mod D for 1 <= D < 2^26, N < 2^58, quotient < 2^33: an fp64
+// estimate (relative error < 2^-51, so within 1 of the quotient) corrected by the
+// exact 64-bit remainder.  Replaces the ~100-instruction software u64 division
+// on the device's constant-derivation critical path; checked against '/' for
+// every D of the domain by tools/udiv_check.cpp.
+__host__ __device__ inline uint64_t udiv_small(uint64_t N, uint64_t D, uint64_t* rem) {
+#ifdef __CUDA_ARCH__
+  const double est = __dmul_rz(__ull2double_rn(N), __drcp_rn(__ull2double_rn(D)));
+#else
+  const double est = static_cast<double>(N) * (1.0 / static_cast<double>(D));
+#endif
+  uint64_t q = static_cast<uint64_t>(est);
+  int64_t r = static_cast<int64_t>(N - q * D);
+  if (r < 0) {
+    --q;
+    r += static_cast<int64_t>(D);
+  } else if (r >= static_cast<int64_t>(D)) {
+    ++q;
+    r -= static_cast<int64_t>(D);
+  }
+  *rem = static_cast<uint64_t>(r);
+  return q;
+}
+
 // smallest L with 2^L >= x (x >= 1)
 __host__ __device__ inline int ceil_log2(uint64_t x) {
 #ifdef __CUDA_ARCH__
@@ -70,10 +94,15 @@ __host__ __device__ inline int derive_core(float s_q, float s_k, int32_t d, qf::
   if (!(s_q > 0.0f) || !(s_k > 0.0f) || !isfinite(s_q) || !isfinite(s_k))
     return QFLASH_ERR_SCALE_RANGE;
   const double log2e = 1.4426950408889634;
-  const double s = ddiv(dmul(dmul(static_cast<double>(s_q), static_cast<double>(s_k)), log2e),
-                        sqrt_head_dim(d));
+  const double x = dmul(dmul(static_cast<double>(s_q), static_cast<double>(s_k)), log2e);
+  // x / 8 is the exact scaling x * 2^-3 (x is a normal fp64 number)
+  const double s = d == 64 ? dmul(x, 0.125) : ddiv(x, sqrt_head_dim(d));
   if (!(s >= ldexp(1.0, -24)) || !(s <= 0.5)) return QFLASH_ERR_SCALE_RANGE;
+#ifdef __CUDA_ARCH__
+  const int64_t s_inv = llround(__drcp_rn(s));   // RN(1/s), round half away (R1)
+#else
   const int64_t s_inv = llround(ddiv(1.0, s));  // round half away (R1)
+#endif
   const double ratio = dmul(s, 127.0);          // s / s_P, s_P = 1/127 (R8)
   int e = 0;
   (void)frexp(ratio, &e);
@@ -86,7 +115,9 @@ __host__ __device__ inline int derive_core(float s_q, float s_k, int32_t d, qf::
   uint32_t q_magic;
   int32_t q_shift;
   {
-    const uint64_t m = ((uint64_t(1) << 32) + D - 1) / D;
+    uint64_t r0;
+    const uint64_t m0 = udiv_small(uint64_t(1) << 32, D, &r0);
+    const uint64_t m = m0 + (r0 != 0 ? 1 : 0);  // ceil(2^32 / D)
     const uint64_t err = m * D - (uint64_t(1) << 32);
     // fast form: exact for t < 27 s_inv (q1 <= 26); beyond, the estimate is
     // >= the true quotient (>= 26) and the shifted value is < 2^26, so y = 0
@@ -97,7 +128,9 @@ __host__ __device__ inline int derive_core(float s_q, float s_k, int32_t d, qf::
     } else {
       const int L = ceil_log2(D);
       const int sh = L > 7 ? L - 7 : 0;           // L <= 25: 2^(32 + sh) < 2^51
-      const uint64_t mm = ((uint64_t(1) << (32 + sh)) + D - 1) / D;
+      uint64_t rr;
+      const uint64_t mm0 = udiv_small(uint64_t(1) << (32 + sh), D, &rr);
+      const uint64_t mm = mm0 + (rr != 0 ? 1 : 0);
       q_magic = static_cast<uint32_t>(mm);
       q_shift = sh;
     }
@@ -115,10 +148,9 @@ __host__ __device__ inline int derive_core(float s_q, float s_k, int32_t d, qf::
     const int L = ceil_log2(D);
     const int sh = L > 8 ? L - 8 : 0;
     const uint64_t A = uint64_t(1) << (32 + sh);
-    const uint64_t q1 = A / D;
-    const uint64_t r1 = A - q1 * D;
-    const uint64_t q2 = (r1 << 32) / D;
-    const uint64_t r2 = (r1 << 32) - q2 * D;
+    uint64_t r1, r2;
+    const uint64_t q1 = udiv_small(A, D, &r1);
+    const uint64_t q2 = udiv_small(r1 << 32, D, &r2);
     rel_magic = (q1 << 32) + q2 + (r2 != 0 ? 1 : 0);
     rel_shift = sh;
   }

@@ -55,6 +55,37 @@ def test_derive_params_matches_oracle(orc, sq, sk, d):
         assert got[key] == ref[key], key
 
 
+def test_derive_params_sweep_matches_oracle_and_magic_definitions(orc):
+    # 600 random scale pairs over the whole accepted range: the oracle's fields, and
+    # the division magics equal their definitions ceil(2^k / s_inv) in big integers
+    # (the library computes them with an fp64-estimated, remainder-corrected division)
+    rng = np.random.default_rng(2604)
+    checked = 0
+    for i in range(600):
+        d = (32, 64, 128)[i % 3]
+        sq, sk = (float(np.float32(10.0 ** rng.uniform(-4.5, 0.3))) for _ in range(2))
+        try:
+            ref = orc.derive_params(sq, sk, d)
+        except ValueError:
+            with pytest.raises(_lib.QFlashError):
+                qflash_derive_params(sq, sk, d)
+            continue
+        got = qflash_derive_params(sq, sk, d)
+        for key in ("s", "s_inv", "n", "r_p", "m_p"):
+            assert got[key] == ref[key], (key, sq, sk, d)
+        D = got["s_inv"]
+        L = (D - 1).bit_length()
+        if got["q_shift"] == 0:
+            assert got["q_magic"] == -(-(1 << 32) // D)
+        else:
+            assert got["q_shift"] == max(L - 7, 0)
+            assert got["q_magic"] == -(-(1 << (32 + got["q_shift"])) // D)
+        assert got["rel_shift"] == max(L - 8, 0)
+        assert got["rel_magic"] == -(-(1 << (64 + got["rel_shift"])) // D)
+        checked += 1
+    assert checked > 300
+
+
 def _s_invs():
     return [2, 3, 22, 127, 251, 1287, 1420, 2293, 8030, 11408, 11769, 12853, 65537, 250001,
             (1 << 22), (1 << 24) - 3]
