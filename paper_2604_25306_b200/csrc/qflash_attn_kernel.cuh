@@ -1086,16 +1086,17 @@ __device__ __forceinline__ void correction_role(const AttnArgs& args, const IntP
 //     proxy fence + grid barrier, after which the attention roles start.
 #ifdef QF_FQ_TIMING
 // experiment builds: globaltimer stamps of CTA 0 in the workspace (bytes 6144..)
-#define QF_FQ_TS(a, k)                                                                      \
+#define QF_FQ_TS_AT(a, k, b, t)                                                            \
   do {                                                                                     \
-    if (blockIdx.x == 0 && threadIdx.x == 0)                                               \
+    if (blockIdx.x == (b) && threadIdx.x == (t))                                           \
       reinterpret_cast<long long*>(reinterpret_cast<char*>((a).prm_out) + 6144)[k] = globaltimer_ns(); \
   } while (0)
 #else
-#define QF_FQ_TS(a, k) \
-  do {                 \
+#define QF_FQ_TS_AT(a, k, b, t) \
+  do {                          \
   } while (0)
 #endif
+#define QF_FQ_TS(a, k) QF_FQ_TS_AT(a, k, 0, 0)
 // Quantize one float4 (4 elements) -> 4 packed int8 codes (exact, see qflash_quant_elem.cuh).
 __device__ __forceinline__ uint32_t quant4(const float4& v, float s, float r) {
   int32_t q[4];
@@ -1176,7 +1177,10 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
     a.partial[threadIdx.x * gridDim.x + blockIdx.x] = b;
   }
   QF_FQ_TS(a, 1);
-  __threadfence();
+  // No per-thread __threadfence: both grid barriers order memory themselves
+  // (grid.sync(): bar.sync, then the arriving thread's gpu-scope fence + atomic;
+  // barrier.cluster arrive.release / wait.acquire).  Dropping the redundant
+  // fences saved ~1 us of the A3 step (profiles/r1_cfg_ab.txt).
   if (a.cluster_grid) cluster_sync_all();
   else cg::this_grid().sync();
   QF_FQ_TS(a, 2);
@@ -1202,6 +1206,7 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   }
   __syncthreads();
   const float s3[3] = {scratch[96], scratch[97], scratch[98]};
+  QF_FQ_TS_AT(a, 13, 0, 32);
   // the integer constants (one thread, ~1.3 us of fp64) overlap the quantization
   // of every other warp; the roles read *sprm only after the final __syncthreads
   if (threadIdx.x == 0) {
@@ -1224,37 +1229,49 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
     dq_table[i + 128] = bits;
     if (blockIdx.x == 0) a.table_out[i + 128] = bits;
   }
-  // 3. quantize this thread's share (registers, or an L2-resident re-read)
+  // 3. quantize this thread's share (registers, or an L2-resident re-read with
+  // all three tensors' loads in flight per step, as in the amax pass)
+  float r3[3];
 #pragma unroll
-  for (int t = 0; t < 3; ++t) {
-    const float s = s3[t];
-    const float r = __frcp_rn(s);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(a.xq[t]);
-    if (resident) {
+  for (int t = 0; t < 3; ++t) r3[t] = __frcp_rn(s3[t]);
+  if (resident) {
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      uint32_t* dst = reinterpret_cast<uint32_t*>(a.xq[t]);
 #pragma unroll
       for (int u = 0; u < kVR; ++u) {
         const int64_t i = gtid + u * nthr;
-        if (i < nvec) dst[i] = quant4(reg[t][u], s, r);
+        if (i < nvec) dst[i] = quant4(reg[t][u], s3[t], r3[t]);
       }
-    } else {
-      const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
-      for (int64_t i = gtid; i < nvec; i += 2 * nthr) {
-        const float4 v0 = __ldcg(src + i);
-        const bool two = i + nthr < nvec;
-        const float4 v1 = two ? __ldcg(src + i + nthr) : make_float4(0.f, 0.f, 0.f, 0.f);
-        dst[i] = quant4(v0, s, r);
-        if (two) dst[i + nthr] = quant4(v1, s, r);
+    }
+  } else {
+    for (int64_t i = gtid; i < nvec; i += 2 * nthr) {
+      const bool two = i + nthr < nvec;
+      float4 v[3][2];
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
+        v[t][0] = __ldcg(src + i);
+        v[t][1] = two ? __ldcg(src + i + nthr) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        uint32_t* dst = reinterpret_cast<uint32_t*>(a.xq[t]);
+        dst[i] = quant4(v[t][0], s3[t], r3[t]);
+        if (two) dst[i + nthr] = quant4(v[t][1], s3[t], r3[t]);
       }
     }
   }
   // int8 codes (generic-proxy stores) -> TMA loads of other CTAs after the barrier
   QF_FQ_TS(a, 4);
+  QF_FQ_TS_AT(a, 6, 0, 32);
   fence_proxy_async_global();
-  __threadfence();
+  QF_FQ_TS_AT(a, 7, 0, 32);
   if (a.cluster_grid) cluster_sync_all();
   else cg::this_grid().sync();
   fence_proxy_async_global();
   QF_FQ_TS(a, 5);
+  QF_FQ_TS_AT(a, 10, 0, 32);
 }
 
 // ---------------------------------------------------------------- the kernel
@@ -1550,6 +1567,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
   tc_fence_after();
   if (threadIdx.x == 0 && blockIdx.x == 0) QF_TS(102);
   if constexpr (FQ) QF_FQ_TS(args, 9);
+  if constexpr (FQ) QF_FQ_TS_AT(args, 12, gridDim.x - 1, 0);
   if constexpr (DBG) {
     if (threadIdx.x == 0 && args.dbg_t != nullptr) args.dbg_t[129 + 2 * blockIdx.x] = globaltimer_ns();
   }
