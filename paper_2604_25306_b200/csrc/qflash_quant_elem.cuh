@@ -6,15 +6,18 @@
 
 namespace qf {
 
-// roundf(fl32(x / s)) exactly (see the header comment).  Fast path: q = RN(x r),
-// rint(q) by the 1.5*2^23 magic-number add (exact for |q| < 2^22, no FRND/F2I),
-// flag `bad` when q is within 2^-14 of a half-integer.
+// roundf(fl32(x / s)) exactly (see the header comment).  Fast path on the exact
+// product x r (r = RN(1/s), so x r = (x / s)(1 + d), |d| <= 2^-24): t = RN(x r +
+// 1.5*2^23) is rint(x r) + 1.5*2^23 for |x r| < 2^22 (no FRND/F2I); the FFMA
+// x r - rint(x r) flags `bad` when x r is within 2^-14 of a half-integer, where
+// x / s and fl32(x / s) could round differently (|x r - x / s| < 2^-16 for
+// |x / s| < 2^8), or when |x r| >= 2^22 (then |x r - fi| >= 1/2).  NaN / inf
+// propagate as before (not flagged, NaN bits).  FFMA + FADD + FFMA + FSETP + IADD.
 __device__ __forceinline__ int32_t quant_fast(float x, float r, bool& bad) {
-  const float q = __fmul_rn(x, r);
-  const float t = __fadd_rn(q, 12582912.0f);                    // 1.5 * 2^23
-  const float fi = __fadd_rn(t, -12582912.0f);                  // rint(q), exact
-  bad |= fabsf(__fadd_rn(q, -fi)) >= 0.49993896484375f;         // 0.5 - 2^-14
-  return static_cast<int32_t>(__float_as_uint(t) - 0x4B400000u);  // int(rint(q))
+  const float t = __fmaf_rn(x, r, 12582912.0f);                 // 1.5 * 2^23
+  const float fi = __fadd_rn(t, -12582912.0f);                  // rint(x r), exact
+  bad |= fabsf(__fmaf_rn(x, r, -fi)) >= 0.49993896484375f;      // 0.5 - 2^-14
+  return static_cast<int32_t>(__float_as_uint(t) - 0x4B400000u);  // int(rint(x r))
 }
 // the exact definition: IEEE division then round half away from zero (R1, R2)
 __device__ __forceinline__ int32_t quant_exact(float x, float s) {
