@@ -11,8 +11,9 @@ namespace qf {
 // 1.5*2^23) is rint(x r) + 1.5*2^23 for |x r| < 2^22 (no FRND/F2I); the FFMA
 // x r - rint(x r) flags `bad` when x r is within 2^-14 of a half-integer, where
 // x / s and fl32(x / s) could round differently (|x r - x / s| < 2^-16 for
-// |x / s| < 2^8), or when |x r| >= 2^22 (then |x r - fi| >= 1/2).  NaN / inf
-// propagate as before (not flagged, NaN bits).  FFMA + FADD + FFMA + FSETP + IADD.
+// |x / s| < 2^8; beyond 2^8 every value saturates to +-127 / -128 anyway).  Domain:
+// |x / s| < 2^22, which every caller guarantees (s = fl32(amax / 127) of the same
+// values, so |x / s| <= 127 (1 + 2^-22)).  FFMA + FADD + FFMA + FSETP + IADD.
 __device__ __forceinline__ int32_t quant_fast(float x, float r, bool& bad) {
   const float t = __fmaf_rn(x, r, 12582912.0f);                 // 1.5 * 2^23
   const float fi = __fadd_rn(t, -12582912.0f);                  // rint(x r), exact
