@@ -28,3 +28,12 @@ y, o, sc, ws = qf.qflash_forward_per_head(dq, dk, dv, 3)
 y2 = qf.QFlashPipeline(*q.shape, mode="two")(dq, dk, dv)
 torch.cuda.synchronize()
 print("per-head status", int(ws[0].item()))
+# fused one-launch step on the cooperative (grid.sync) path: A3 b8 (148 CTAs) vs the
+# multi-launch pipeline's output, and the A4 b2 streamed-quantize case
+for wl, b in (("A3", 8), ("A4", 2)):
+    q, k, v = gen_workload(wl, b, seed=3)
+    dq, dk, dv = (torch.from_numpy(x).cuda() for x in (q, k, v))
+    yf = qf.QFlashPipeline(*q.shape, mode="fused")(dq, dk, dv).clone()
+    yt = qf.QFlashPipeline(*q.shape, mode="three")(dq, dk, dv)
+    torch.cuda.synchronize()
+    print("fused", wl, b, bool(torch.equal(yf.view(torch.int32), yt.view(torch.int32))))
