@@ -48,11 +48,14 @@ static double qo_round(double x) { return round(x); }
 /* ------------------------------------------------ Eq. 1-2: quantization */
 
 /* Eq. 2: s_X = ||X||_inf / (2^(b-1)-1), X^ = round(X / s_X), b=8.
- * R2: fp32 arithmetic, IEEE division, roundf (half away).  R3: all-zero tensor
- * -> s = 1/127.  R4: saturate to [-128, 127] (Eq. 1). */
+ * R2: fp32 arithmetic, IEEE division, roundf (half away).  R3: a tensor whose
+ * scale is zero -- all-zero, or so small (amax <= 127 * 2^-150) that fl32(amax/127)
+ * underflows -- gets s = 1/127 (Eq. 2 divides by s).  R4: saturate to
+ * [-128, 127] (Eq. 1). */
 static float qo_scale_from_amax(float amax) {
-  if (amax == 0.0f) return 1.0f / 127.0f;
-  return amax / 127.0f;
+  const float s = amax / 127.0f;
+  if (s == 0.0f) return 1.0f / 127.0f;
+  return s;
 }
 
 static int8_t qo_quantize_one(float x, float s) {

@@ -43,6 +43,19 @@ def test_quantize_zero_tensor(orc):
     assert not xq.any()
 
 
+def test_quantize_underflowing_scale(orc):
+    # R3: amax > 0 but fl32(amax / 127) == 0 (amax <= 127 * 2^-150: every element a
+    # tiny subnormal) has no usable Eq. 2 scale either -> s = 1/127, all codes 0;
+    # one ulp above the underflow the scale is the subnormal fl32(amax / 127).
+    tiny = np.float32(np.ldexp(1.0, -149))          # the smallest subnormal
+    xq, s = orc.quantize(np.array([tiny, -tiny, 0.0], np.float32))
+    assert s == np.float32(1.0) / np.float32(127.0) and not xq.any()
+    amax = np.float32(np.ldexp(1.0, -120))
+    xq, s = orc.quantize(np.array([amax, -amax / 2, 0.0], np.float32))
+    assert s == amax / np.float32(127.0) and s > 0
+    assert xq.tolist() == [127, -64, 0]                # -63.5 rounds away from zero (R1)
+
+
 def test_quantize_error_bound_and_idempotence(orc):
     rng = np.random.default_rng(1)
     x = (rng.standard_normal(100_000) * 3).astype(np.float32)
@@ -444,3 +457,40 @@ def test_per_head_improves_sqnr_with_head_spread(orc):
     small = orc.head_problems(P, H, 0)  # the smallest-gain head
     assert sqnr_db(ref[small], y_h[small]) > sqnr_db(ref[small], y_t[small]) + 6.0
     assert sqnr_db(ref, y_h) >= sqnr_db(ref, y_t) - 0.5
+
+
+# ------------------------------------------------- FP64 reference and error metrics
+def test_sqnr_mse_hand_values():
+    # SQNR = 10 log10(sum ref^2 / sum (ref - test)^2), MSE = mean (ref - test)^2.
+    from oracle.fp_reference import mse, sqnr_db
+    assert math.isclose(sqnr_db([1.0, 1.0], [1.0, 0.0]), 10 * math.log10(2.0), rel_tol=1e-12)
+    assert math.isclose(sqnr_db([1.0, 1.0], [1.0, 0.0]), 3.010299956639812, rel_tol=1e-12)
+    # noise 1 % of the signal amplitude -> 40 dB (10 log10, not 20 log10: a power ratio)
+    assert math.isclose(sqnr_db([3.0, 4.0], [3.03, 4.04]), 40.0, rel_tol=1e-9)
+    assert math.isclose(sqnr_db([2.0, 0.0], [0.0, 0.0]), 0.0, abs_tol=1e-12)
+    assert sqnr_db([1.0, -2.0], [1.0, -2.0]) == float("inf")
+    assert mse([1.0, 1.0], [1.0, 0.0]) == 0.5
+    assert mse([[1.0, 2.0], [3.0, 4.0]], [[1.0, 2.0], [3.0, 1.0]]) == 9.0 / 4.0
+    # SQNR in dB of the paper's own pair (Table[SQNR]): MSE 1.51e-3 at
+    # 32.50 dB implies a reference power MSE 10^(SQNR/10) = 2.68
+    ref = np.array([np.sqrt(2.68)] * 4)
+    test = ref + np.sqrt(1.51e-3)
+    assert math.isclose(sqnr_db(ref, test), 32.5, abs_tol=0.01)
+
+
+def test_attention_fp64_hand_example():
+    # softmax(q k^T / sqrt(d)) v worked by hand: d = 1, scores (0, ln 3) -> weights
+    # (1/4, 3/4) -> 1/4 * 1 + 3/4 * 5 = 4; the second query sees scores (0, 0) ->
+    # the mean of v.  Constant shifts of a score row cancel (max subtraction).
+    from oracle.fp_reference import attention_fp64
+    q = np.array([[[1.0], [0.0]]])
+    k = np.array([[[0.0], [math.log(3.0)]]])
+    v = np.array([[[1.0], [5.0]]])
+    out = attention_fp64(q, k, v)
+    assert np.allclose(out[0, :, 0], [4.0, 3.0], rtol=0, atol=1e-12)
+    # d = 4: the 1/sqrt(d) = 1/2 scaling -- scores q.k = 2 ln 3 -> ln 3 after scaling
+    q4 = np.array([[[math.log(3.0), math.log(3.0), 0.0, 0.0]]])
+    k4 = np.array([[[0.0, 0.0, 0.0, 0.0], [1.0, 1.0, 0.0, 0.0]]])
+    v4 = np.array([[[1.0, 0.0, 0.0, 0.0], [5.0, 1.0, 0.0, 0.0]]])
+    out4 = attention_fp64(q4, k4, v4)
+    assert np.allclose(out4[0, 0], [4.0, 0.75, 0.0, 0.0], rtol=0, atol=1e-12)
