@@ -25,6 +25,24 @@ QFLASH_API qflash_status qflash_debug_attention(const int8_t* q, const int8_t* k
                                                 int32_t* dbg_p, int32_t* dbg_o, long long* dbg_t,
                                                 qflash_stream_t stream);
 
+/* Force the attention kernel configuration of every later launch in this process
+ * (tests and A/B runs; the host heuristic picks one otherwise):
+ *   cfg -1  the heuristic (default; QFLASH_ATTN_CFG=<0..3> in the environment sets
+ *           the initial value)
+ *   cfg 0   CS = 4 column splits x QT = 1 query tile in flight
+ *   cfg 1   CS = 2 x QT = 2
+ *   cfg 2   row-owner softmax + correction warpgroups x QT = 2
+ *   cfg 3   row-owner softmax + correction warpgroups x QT = 1
+ * A forced configuration that has no instantiation for a shape (TMEM / shared
+ * memory budget) falls back to the heuristic's choice.  Returns
+ * QFLASH_ERR_INVALID_ARGUMENT for cfg outside [-1, 3].  Not thread-safe with
+ * respect to launches already being prepared on other threads. */
+QFLASH_API qflash_status qflash_debug_force_config(int32_t cfg);
+
+/* The configuration (bits 0-3) and row-packing segment count NSEG (bits 4-7) of
+ * the calling thread's last attention launch, or -1 if it made none. */
+QFLASH_API int32_t qflash_debug_last_config(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -116,6 +116,10 @@ def lib():
     L.qflash_debug_attention.restype = st
     L.qflash_debug_attention.argtypes = [vp, vp, vp, f32, f32, ctypes.POINTER(AttnShape), st, vp,
                                          vp, vp, vp, vp, vp]
+    L.qflash_debug_force_config.restype = st
+    L.qflash_debug_force_config.argtypes = [i32]
+    L.qflash_debug_last_config.restype = i32
+    L.qflash_debug_last_config.argtypes = []
     _lib = L
     return L
 
@@ -126,6 +130,17 @@ def status_string(status: int) -> str:
 
 def last_error() -> str:
     return lib().qflash_last_error().decode()
+
+
+def force_config(cfg: int) -> None:
+    """Force the attention kernel configuration (-1 = heuristic); include/qflash_debug.h."""
+    check(lib().qflash_debug_force_config(cfg))
+
+
+def last_config() -> tuple[int, int]:
+    """(configuration, row-packing segments) of this thread's last attention launch."""
+    c = lib().qflash_debug_last_config()
+    return (-1, 0) if c < 0 else (c & 15, c >> 4)
 
 
 def check(status: int) -> None:

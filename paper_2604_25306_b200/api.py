@@ -30,6 +30,41 @@ def _dev_ptr(t: torch.Tensor) -> ctypes.c_void_p:
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _check_like(ref: torch.Tensor, t: torch.Tensor, name: str, dtype=None) -> None:
+    """t must have ref's shape (the library sizes every buffer from q's shape), the
+    expected dtype and ref's device -- checked before any pointer reaches the C ABI."""
+    if tuple(t.shape) != tuple(ref.shape):
+        raise ValueError("%s: shape %s != %s" % (name, tuple(t.shape), tuple(ref.shape)))
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError("%s: dtype %s, expected %s" % (name, t.dtype, dtype))
+    if t.device != ref.device:
+        raise ValueError("%s: device %s != %s" % (name, t.device, ref.device))
+
+
+def _check_qkv(q, k, v, dtype=torch.int8) -> None:
+    if q.dim() != 3:
+        raise ValueError("expected [P, N, d] tensors, got %s" % (tuple(q.shape),))
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        _check_like(q, t, name, dtype)
+
+
+def _check_buffer(t: torch.Tensor, nbytes: int, name: str, device, dtype=None) -> None:
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError("%s: dtype %s, expected %s" % (name, t.dtype, dtype))
+    if t.numel() * t.element_size() < nbytes:
+        raise ValueError("%s: %d bytes < %d" % (name, t.numel() * t.element_size(), nbytes))
+    if t.device != device:
+        raise ValueError("%s: device %s != %s" % (name, t.device, device))
+
+
+def _check_workspace(ws: torch.Tensor, device) -> None:
+    _check_buffer(ws, _lib.DSCALE_WORKSPACE_BYTES, "workspace", device)
+
+
+def _check_scales(sc: torch.Tensor, n: int, device) -> None:
+    _check_buffer(sc, 4 * n, "scales", device, torch.float32)
+
+
 # ---------------------------------------------------------------- quantizer
 def qflash_quantize_per_tensor(x: torch.Tensor, out: torch.Tensor | None = None,
                                scale_out: torch.Tensor | None = None, stream=None):
@@ -38,6 +73,8 @@ def qflash_quantize_per_tensor(x: torch.Tensor, out: torch.Tensor | None = None,
         raise TypeError(x.dtype)
     out = torch.empty(x.shape, dtype=torch.int8, device=x.device) if out is None else out
     scale_out = torch.empty(1, dtype=torch.float32, device=x.device) if scale_out is None else scale_out
+    _check_like(x, out, "out", torch.int8)
+    _check_scales(scale_out, 1, x.device)
     check(lib().qflash_quantize_per_tensor(_dev_ptr(x), _DTYPES[x.dtype], x.numel(), _dev_ptr(out),
                                            _dev_ptr(scale_out), None, _stream(stream)))
     return out, scale_out
@@ -46,10 +83,16 @@ def qflash_quantize_per_tensor(x: torch.Tensor, out: torch.Tensor | None = None,
 def qflash_quantize_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, outs=None,
                         scales: torch.Tensor | None = None, stream=None):
     """Fused Q/K/V quantization.  Returns (q_q, k_q, v_q, scales float32[3] on device)."""
-    assert q.shape == k.shape == v.shape and q.dtype == k.dtype == v.dtype
+    if q.dtype not in _DTYPES:
+        raise TypeError(q.dtype)
+    for name, t in (("k", k), ("v", v)):
+        _check_like(q, t, name, q.dtype)
     if outs is None:
         outs = [torch.empty(q.shape, dtype=torch.int8, device=q.device) for _ in range(3)]
     scales = torch.empty(3, dtype=torch.float32, device=q.device) if scales is None else scales
+    for i, t in enumerate(outs):
+        _check_like(q, t, "outs[%d]" % i, torch.int8)
+    _check_scales(scales, 3, q.device)
     check(lib().qflash_quantize_qkv(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v), _DTYPES[q.dtype],
                                     q.numel(), _dev_ptr(outs[0]), _dev_ptr(outs[1]),
                                     _dev_ptr(outs[2]), _dev_ptr(scales), _stream(stream)))
@@ -68,10 +111,9 @@ def qflash_attention_int8(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, s_q
                           s_k: float, s_v: float, block_kv: int = 128, variant: str = "auto",
                           out: torch.Tensor | None = None, stream=None):
     """Algorithm 1 (integer-only fused attention).  int8 [P, N, d] in, (int8 out, s_O) back."""
-    for t in (q, k, v):
-        if t.dtype != torch.int8:
-            raise TypeError("q, k, v must be int8")
+    _check_qkv(q, k, v)
     out = torch.empty_like(q) if out is None else out
+    _check_like(q, out, "out", torch.int8)
     shape = _shape(q, block_kv)
     s_o = ctypes.c_float(0.0)
     check(lib().qflash_attention_int8_ex(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v), s_q, s_k, s_v,
@@ -86,9 +128,13 @@ def qflash_attention_int8_dscale(q: torch.Tensor, k: torch.Tensor, v: torch.Tens
                                  workspace: torch.Tensor | None = None, stream=None):
     """Device-scale attention: scales = device float32[3] (s_q, s_k, s_v); no host sync.
     Returns (out int8, workspace) -- workspace[0] (int32) holds the status."""
+    _check_qkv(q, k, v)
     out = torch.empty_like(q) if out is None else out
     if workspace is None:
         workspace = torch.empty(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=q.device)
+    _check_like(q, out, "out", torch.int8)
+    _check_scales(scales, 3, q.device)
+    _check_workspace(workspace, q.device)
     shape = _shape(q, block_kv)
     check(lib().qflash_attention_int8_dscale(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v),
                                              _dev_ptr(scales), ctypes.byref(shape),
@@ -100,8 +146,12 @@ def qflash_attention_int8_dscale(q: torch.Tensor, k: torch.Tensor, v: torch.Tens
 # ---------------------------------------------------------------- dequantizer
 def qflash_dequantize(x_q: torch.Tensor, scale, out: torch.Tensor | None = None, stream=None):
     """y = scale * x^ in fp32.  `scale` is a python float or a device float32 tensor."""
+    if x_q.dtype != torch.int8:
+        raise TypeError("x_q must be int8")
     out = torch.empty(x_q.shape, dtype=torch.float32, device=x_q.device) if out is None else out
+    _check_like(x_q, out, "out", torch.float32)
     if isinstance(scale, torch.Tensor):
+        _check_scales(scale, 1, x_q.device)
         check(lib().qflash_dequantize_dscale(_dev_ptr(x_q), _dev_ptr(scale), x_q.numel(),
                                              _dev_ptr(out), _stream(stream)))
     else:
@@ -116,12 +166,18 @@ def qflash_quantize_qkv_prepare(q: torch.Tensor, k: torch.Tensor, v: torch.Tenso
                                 workspace: torch.Tensor | None = None, stream=None):
     """Fused Q/K/V quantization that also derives the attention constants on the
     device.  Returns (q_q, k_q, v_q, scales float32[3], workspace int32[32])."""
-    assert q.shape == k.shape == v.shape and q.dtype == k.dtype == v.dtype and q.dim() == 3
+    if q.dtype not in _DTYPES:
+        raise TypeError(q.dtype)
+    _check_qkv(q, k, v, q.dtype)
     if outs is None:
         outs = [torch.empty(q.shape, dtype=torch.int8, device=q.device) for _ in range(3)]
     scales = torch.empty(3, dtype=torch.float32, device=q.device) if scales is None else scales
     if workspace is None:
         workspace = torch.empty(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=q.device)
+    for i, t in enumerate(outs):
+        _check_like(q, t, "outs[%d]" % i, torch.int8)
+    _check_scales(scales, 3, q.device)
+    _check_workspace(workspace, q.device)
     check(lib().qflash_quantize_qkv_prepare(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v),
                                             _DTYPES[q.dtype], q.numel(), _dev_ptr(outs[0]),
                                             _dev_ptr(outs[1]), _dev_ptr(outs[2]), _dev_ptr(scales),
@@ -134,7 +190,10 @@ def qflash_attention_int8_prepared(q: torch.Tensor, k: torch.Tensor, v: torch.Te
                                    variant: str = "auto", out: torch.Tensor | None = None,
                                    stream=None):
     """Algorithm 1 with the constants qflash_quantize_qkv_prepare left in `workspace`."""
+    _check_qkv(q, k, v)
     out = torch.empty_like(q) if out is None else out
+    _check_like(q, out, "out", torch.int8)
+    _check_workspace(workspace, q.device)
     shape = _shape(q, block_kv)
     check(lib().qflash_attention_int8_prepared(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v),
                                                ctypes.byref(shape), _lib.VARIANTS[variant],
@@ -149,7 +208,12 @@ def qflash_attention_dequant_prepared(q: torch.Tensor, k: torch.Tensor, v: torch
     """Algorithm 1 with the dequantization fused into its epilogue: fp32
     y = s_V * O^ (and optionally the int8 O^), constants and dequant table from
     `workspace` (qflash_quantize_qkv_prepare)."""
+    _check_qkv(q, k, v)
     out = torch.empty(q.shape, dtype=torch.float32, device=q.device) if out is None else out
+    _check_like(q, out, "out", torch.float32)
+    if out_int8 is not None:
+        _check_like(q, out_int8, "out_int8", torch.int8)
+    _check_workspace(workspace, q.device)
     shape = _shape(q, block_kv)
     check(lib().qflash_attention_dequant_prepared(
         _dev_ptr(q), _dev_ptr(k), _dev_ptr(v), ctypes.byref(shape), _lib.VARIANTS[variant],
@@ -164,15 +228,21 @@ def qflash_forward_fused(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, bloc
                          out_int8: torch.Tensor | None = None, stream=None):
     """The whole hot path in one cooperative launch: fp32 Q, K, V [P, N, d] ->
     quantize (in the kernel's prologue) -> integer attention -> fp32 output."""
-    assert q.shape == k.shape == v.shape and q.dim() == 3
-    assert q.dtype == k.dtype == v.dtype == torch.float32
+    _check_qkv(q, k, v, torch.float32)
     dev = q.device
     out = torch.empty(q.shape, dtype=torch.float32, device=dev) if out is None else out
     if codes is None:
         codes = [torch.empty(q.shape, dtype=torch.int8, device=dev) for _ in range(3)]
     scales = torch.empty(3, dtype=torch.float32, device=dev) if scales is None else scales
     if workspace is None:
-        workspace = torch.empty(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=dev)
+        workspace = torch.zeros(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=dev)
+    _check_like(q, out, "out", torch.float32)
+    for i, t in enumerate(codes):
+        _check_like(q, t, "codes[%d]" % i, torch.int8)
+    if out_int8 is not None:
+        _check_like(q, out_int8, "out_int8", torch.int8)
+    _check_scales(scales, 3, dev)
+    _check_workspace(workspace, dev)
     shape = _shape(q, block_kv)
     check(lib().qflash_forward_fused(
         _dev_ptr(q), _dev_ptr(k), _dev_ptr(v), ctypes.byref(shape), _lib.VARIANTS[variant],
@@ -203,7 +273,7 @@ class QFlashPipeline:
         self.qkv_q = [torch.empty(self.shape, dtype=torch.int8, device=dev) for _ in range(3)]
         self.scales = torch.empty(3, dtype=torch.float32, device=dev)
         self.o_q = torch.empty(self.shape, dtype=torch.int8, device=dev)
-        self.workspace = torch.empty(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=dev)
+        self.workspace = torch.zeros(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=dev)
         self.out = torch.empty(self.shape, dtype=torch.float32, device=dev)
 
     def launches(self, dtype=torch.float32) -> int:
@@ -215,6 +285,7 @@ class QFlashPipeline:
         return quant + (1 if self.mode == "two" else 2)
 
     def __call__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, stream=None):
+        _check_like(self.out, q, "q", q.dtype)   # the buffers were sized for self.shape
         if self.mode == "fused" and q.dtype == torch.float32:
             return qflash_forward_fused(q, k, v, self.block_kv, self.variant, out=self.out,
                                         codes=self.qkv_q, scales=self.scales,
@@ -240,7 +311,7 @@ def qflash_forward_per_head(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, h
     per-head quantization -> integer attention with per-head constants ->
     per-head dequantization.  Returns (y fp32, o int8, scales float32[3 heads],
     workspace) -- the int32 status of the constant derivation is workspace[0]."""
-    assert q.shape == k.shape == v.shape and q.dim() == 3 and q.dtype == torch.float32
+    _check_qkv(q, k, v, torch.float32)
     P, N, d = q.shape
     dev = q.device
     codes = [torch.empty(q.shape, dtype=torch.int8, device=dev) for _ in range(3)]
@@ -281,6 +352,8 @@ class QFlashPerHeadPipeline:
     def __call__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, stream=None):
         P, N, d = self.shape
         H = self.heads
+        _check_qkv(q, k, v, torch.float32)
+        _check_like(self.out, q, "q")
         c = self.codes
         check(lib().qflash_quantize_per_head(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v), P, N, d, H,
                                              _dev_ptr(c[0]), _dev_ptr(c[1]), _dev_ptr(c[2]),

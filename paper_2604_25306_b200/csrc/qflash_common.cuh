@@ -27,6 +27,13 @@ struct IntParams {
 static_assert(sizeof(IntParams) == 72, "IntParams layout");
 
 constexpr int kPdlDefault = 15;
+// Workspace layout of the device-scale paths (QFLASH_DSCALE_WORKSPACE_BYTES = 8192):
+// [0, 128) IntParams, [256, 4096) per-CTA amax partials (3 floats per CTA),
+// [4096, 5120) the 256-entry dequant table.
+constexpr int kWsPartialOffset = 256;
+constexpr int kWsDqTableOffset = 4096;
+constexpr int kWsMaxPartialCtas = (kWsDqTableOffset - kWsPartialOffset) / 12;  // = 320
+static_assert(kWsMaxPartialCtas == 320, "partials must end before the dequant table");
 constexpr int kHeadPrmStride = 80;   // bytes per head in the per-head constant table
 constexpr int kHeadPrmOffset = 128;  // table offset in the per-head workspace
 constexpr int kMaxHeads = 96;        // 128 + 96 * 80 <= QFLASH_DSCALE_WORKSPACE_BYTES

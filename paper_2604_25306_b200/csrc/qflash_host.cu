@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdint>
@@ -175,6 +176,22 @@ qflash_status make_tmap(CUtensorMap* m, const int8_t* base, int P, int N, int d,
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Attention kernel configuration override (qflash_debug_force_config, or the
+// QFLASH_ATTN_CFG environment variable read once): -1 = the host heuristic.
+std::atomic<int> g_force_config{-2};
+thread_local int g_last_config = -1;  // cfg | nseg << 4 of this thread's last launch
+int forced_config() {
+  int c = g_force_config.load(std::memory_order_relaxed);
+  if (c == -2) {
+    const char* env = getenv("QFLASH_ATTN_CFG");
+    c = (env != nullptr && env[0] >= '0' && env[0] <= '3') ? env[0] - '0' : -1;
+    int expected = -2;
+    g_force_config.compare_exchange_strong(expected, c);
+    c = g_force_config.load(std::memory_order_relaxed);
+  }
+  return c;
+}
+
 bool overlaps(const void* a, int64_t na, const void* b, int64_t nb) {
   const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
   return a0 < b0 + static_cast<uintptr_t>(nb) && b0 < a0 + static_cast<uintptr_t>(na);
@@ -244,6 +261,8 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
       if (dev >= 0 && dev < 64) sm_cache[dev] = sms;
     }
   }
+  // the fused step's per-CTA amax partials must fit the workspace (one CTA per SM)
+  if (fin != nullptr && sms > qf::kWsMaxPartialCtas) sms = qf::kWsMaxPartialCtas;
   // AUTO packs rows only when that saves a wave of one-tile-per-SM work: a
   // row-packed tile costs a little more (one TMA load and MMA per segment).
   const int64_t waves_generic = (tiles_generic + sms - 1) / sms;
@@ -274,11 +293,7 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   // warpgroups) or cfg 1 (two tiles, 2 column splits) where it fits TMEM /
   // shared memory; else cfg 0 (one tile, 4 column splits: lowest latency per
   // tile).  QFLASH_ATTN_CFG=0..3 overrides.
-  static int cfg_env = -2;
-  if (cfg_env == -2) {
-    const char* env = getenv("QFLASH_ATTN_CFG");
-    cfg_env = (env != nullptr && env[0] >= '0' && env[0] <= '3') ? env[0] - '0' : -1;
-  }
+  const int cfg_env = forced_config();
   // Measured (profiles/r1_cfg_ab.txt): multi-wave with several KV tiles -> cfg 1
   // (L14 b64: 848 vs 938 us for cfg 2); one KV tile (Swin windows) -> cfg 2.
   const int Tc_host = (N + bc_eff - 1) / bc_eff;
@@ -291,6 +306,7 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   if (cfg_env >= 0 && heads == 0 && qf::attention_supported(d, bc_eff, nseg, cfg_env)) cfg = cfg_env;
   if (!qf::attention_supported(d, bc_eff, nseg, cfg))
     return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "no kernel configuration for d=%d block=%d", d, bc_eff);
+  g_last_config = cfg | (nseg << 4);
   CUtensorMap tq, tk, tv;
   qflash_status st;
   if ((st = make_tmap(&tq, q, P, N, d, 128, 1)) != QFLASH_OK) return st;
@@ -317,8 +333,8 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
     }
     args.scales_out = fin->scales;
     args.prm_out = reinterpret_cast<qf::IntParams*>(fin->workspace);
-    args.partial = reinterpret_cast<float*>(static_cast<char*>(fin->workspace) + 256);
-    args.table_out = reinterpret_cast<uint32_t*>(static_cast<char*>(fin->workspace) + 4096);
+    args.partial = reinterpret_cast<float*>(static_cast<char*>(fin->workspace) + qf::kWsPartialOffset);
+    args.table_out = reinterpret_cast<uint32_t*>(static_cast<char*>(fin->workspace) + qf::kWsDqTableOffset);
     args.numel = static_cast<int64_t>(P) * N * d;
   }
   args.dbg_s = dbg_s;
@@ -610,13 +626,27 @@ qflash_status qflash_forward_fused(const float* q, const float* k, const float* 
   }
   const void* ins[3] = {q, k, v};
   const int8_t* codes[3] = {q_q, k_q, v_q};
+  // every written buffer (codes, o, y) must be disjoint from every input and from
+  // every other written buffer: the prologue re-reads inputs after other CTAs have
+  // started writing codes, and the TMA loads read codes while y / o are written
   for (int i = 0; i < 3; ++i) {
     for (int j = 0; j < 2; ++j)
       if (outs[j] && overlaps(outs[j], out_n[j], ins[i], 4 * n))
         return fail(QFLASH_ERR_INVALID_ARGUMENT, "outputs alias the inputs");
-    if (overlaps(codes[i], n, ins[i], 4 * n) || overlaps(reinterpret_cast<const int8_t*>(y), 4 * n, codes[i], n))
-      return fail(QFLASH_ERR_INVALID_ARGUMENT, "int8 buffers alias inputs or y");
+    for (int j = 0; j < 3; ++j) {
+      if (overlaps(codes[i], n, ins[j], 4 * n))
+        return fail(QFLASH_ERR_INVALID_ARGUMENT, "int8 code buffer %d aliases input %d", i, j);
+      if (j != i && overlaps(codes[i], n, codes[j], n))
+        return fail(QFLASH_ERR_INVALID_ARGUMENT, "int8 code buffers %d and %d alias", i, j);
+    }
+    if (overlaps(reinterpret_cast<const int8_t*>(y), 4 * n, codes[i], n))
+      return fail(QFLASH_ERR_INVALID_ARGUMENT, "int8 buffers alias y");
   }
+  const int8_t* ws = static_cast<const int8_t*>(workspace_dev);
+  for (int i = 0; i < 3; ++i)
+    if (overlaps(ws, QFLASH_DSCALE_WORKSPACE_BYTES, ins[i], 4 * n) ||
+        overlaps(ws, QFLASH_DSCALE_WORKSPACE_BYTES, codes[i], n))
+      return fail(QFLASH_ERR_INVALID_ARGUMENT, "workspace aliases a tensor");
   int dev = 0;
   if ((st = check_device(&dev)) != QFLASH_OK) return st;
   FusedIn fin;
@@ -739,6 +769,14 @@ qflash_status qflash_dequantize_per_head(const int8_t* x_q, const float* scales_
   if (e != cudaSuccess) return cuda_fail(e, "per-head dequantize launch");
   return QFLASH_OK;
 }
+
+qflash_status qflash_debug_force_config(int32_t cfg) {
+  if (cfg < -1 || cfg > 3) return fail(QFLASH_ERR_INVALID_ARGUMENT, "config %d not in [-1, 3]", cfg);
+  g_force_config.store(cfg, std::memory_order_relaxed);
+  return QFLASH_OK;
+}
+
+int32_t qflash_debug_last_config(void) { return g_last_config; }
 
 // Bring-up entry (include/qflash_debug.h): qflash_attention_int8_ex plus raw
 // dumps of S, P and the final (O, l) of CTA (problem 0, query tile 0).

@@ -45,7 +45,7 @@
 namespace qf {
 
 constexpr int kQThreads = 256;
-constexpr int kDqTableOffset = 4096;  // workspace bytes of the 256-entry dequant table
+constexpr int kDqTableOffset = kWsDqTableOffset;  // workspace bytes of the 256-entry dequant table
 static_assert(kQThreads == 256, "one thread per dequant-table entry");
 constexpr int kQElems = 16;  // elements per thread per iteration
 
@@ -644,7 +644,7 @@ static cudaError_t launch_fused_t(const QuantTensors& t, int ntensors, int64_t n
   }
   if (blocks > cap) return cudaErrorNotSupported;
   if (blocks < 1) blocks = 1;
-  if (blocks > 960) return cudaErrorNotSupported;  // partials must fit the workspace
+  if (blocks > kWsMaxPartialCtas) return cudaErrorNotSupported;  // partials end before the table
   switch (vpt) {
     case 1: return launch_fused_vpt<T, 1>(t, numel, partial, prm_out, head_dim, static_cast<int>(blocks), stream);
     case 2: return launch_fused_vpt<T, 2>(t, numel, partial, prm_out, head_dim, static_cast<int>(blocks), stream);

@@ -13,11 +13,14 @@ namespace qf {
 // x / s and fl32(x / s) could round differently (|x r - x / s| < 2^-16 for
 // |x / s| < 2^8; beyond 2^8 every value saturates to +-127 / -128 anyway).  Domain:
 // |x / s| < 2^22, which every caller guarantees (s = fl32(amax / 127) of the same
-// values, so |x / s| <= 127 (1 + 2^-22)).  FFMA + FADD + FFMA + FSETP + IADD.
+// values, so |x / s| <= 127 (1 + 2^-22)); a non-finite r (subnormal s) always takes
+// the exact path.  FFMA + FADD + FFMA + FSETP + IADD.
 __device__ __forceinline__ int32_t quant_fast(float x, float r, bool& bad) {
   const float t = __fmaf_rn(x, r, 12582912.0f);                 // 1.5 * 2^23
   const float fi = __fadd_rn(t, -12582912.0f);                  // rint(x r), exact
-  bad |= fabsf(__fmaf_rn(x, r, -fi)) >= 0.49993896484375f;      // 0.5 - 2^-14
+  // written as !(|.| < c) so that a NaN residual also takes the exact path: r = +Inf
+  // when s < 2^-128 (a subnormal scale), where x r is NaN / Inf
+  bad |= !(fabsf(__fmaf_rn(x, r, -fi)) < 0.49993896484375f);   // 0.5 - 2^-14
   return static_cast<int32_t>(__float_as_uint(t) - 0x4B400000u);  // int(rint(x r))
 }
 // the exact definition: IEEE division then round half away from zero (R1, R2)

@@ -185,6 +185,26 @@ def test_validation_before_any_cuda_call():
     assert L.qflash_quantize_qkv(vp(base), vp(base), vp(base), 7, 10, vp(base), vp(base),
                                  vp(base), vp(base), None) == _lib.QFLASH_ERR_INVALID_ARGUMENT
     assert L.qflash_dequantize(None, 1.0, 10, None, None) == _lib.QFLASH_ERR_INVALID_ARGUMENT
+    # fused step: every code buffer must be disjoint from every fp32 input and the
+    # other code buffers (k_q aliasing the fp32 q input was accepted)
+    f = [vp(base + i * 4 * n) for i in range(3)]                 # fp32 q, k, v
+    y, sc, ws = vp(base + 12 * n), vp(base + 16 * n), vp(base + 17 * n)
+    codes = [vp(base + 20 * n + i * n) for i in range(3)]
+    fused = L.qflash_forward_fused
+    fused.restype = ctypes.c_int
+    ok_codes = fused(*f, ctypes.byref(sh), 0, *codes, None, y, sc, ws, None)
+    assert ok_codes != _lib.QFLASH_ERR_INVALID_ARGUMENT          # (device check comes later)
+    for bad_codes in ([codes[0], f[0], codes[2]],                 # k_q aliases the q input
+                      [codes[0], codes[1], vp(base + 8 * n + 64)],  # v_q inside the v input
+                      [codes[0], codes[0], codes[2]]):            # q_q == k_q
+        assert fused(*f, ctypes.byref(sh), 0, *bad_codes, None, y, sc, ws,
+                     None) == _lib.QFLASH_ERR_INVALID_ARGUMENT
+    assert fused(*f, ctypes.byref(sh), 0, *codes, None, y, sc, f[1],
+                 None) == _lib.QFLASH_ERR_INVALID_ARGUMENT       # workspace aliases k
+    # configuration override of the debug header: range-checked, -1 = heuristic
+    assert L.qflash_debug_force_config(4) == _lib.QFLASH_ERR_INVALID_ARGUMENT
+    assert L.qflash_debug_force_config(-2) == _lib.QFLASH_ERR_INVALID_ARGUMENT
+    assert L.qflash_debug_force_config(-1) == _lib.QFLASH_OK
 
 
 # ----------------------------------------------------------------------------
@@ -259,3 +279,34 @@ def test_kernel_normalize_arithmetic():
         for O in Os:
             if -(1 << 31) <= O < (1 << 31):
                 assert _floor_div_kernel(O, l) == O // l, (O, l)
+
+
+def test_python_wrappers_check_buffers_before_the_abi():
+    # the library sizes every buffer from q's shape, so the
+    # wrappers reject a k / v / out / workspace that does not match -- before any
+    # pointer reaches the C ABI (these CPU tensors never get that far).
+    import torch
+    from paper_2604_25306_b200 import api
+    q = torch.zeros((2, 64, 32), dtype=torch.int8)
+    small = torch.zeros((2, 63, 32), dtype=torch.int8)
+    with pytest.raises(ValueError):
+        api.qflash_attention_int8(q, small, q, 0.05, 0.05, 0.05)
+    with pytest.raises(ValueError):
+        api.qflash_attention_int8(q, q, q, 0.05, 0.05, 0.05, out=small)
+    with pytest.raises(TypeError):
+        api.qflash_attention_int8(q, q.float(), q, 0.05, 0.05, 0.05)
+    ws_small = torch.zeros(16, dtype=torch.int32)
+    with pytest.raises(ValueError):
+        api.qflash_attention_int8_prepared(q, q, q, ws_small)
+    with pytest.raises(ValueError):
+        api.qflash_attention_dequant_prepared(q, q, q, torch.zeros(2048, dtype=torch.int32),
+                                              out=torch.zeros((2, 64, 16)))
+    f = torch.zeros((2, 64, 32))
+    with pytest.raises(ValueError):
+        api.qflash_forward_fused(f, f, f, codes=[q, q, small])
+    with pytest.raises(ValueError):
+        api.qflash_forward_fused(f, f, f, scales=torch.zeros(2))
+    with pytest.raises(ValueError):
+        api.qflash_attention_int8_dscale(q, q, q, torch.zeros(2))
+    with pytest.raises(TypeError):
+        api.qflash_dequantize(f, 1.0)

@@ -106,19 +106,90 @@ def test_adversarial_sets(orc, kind, N, d):
         assert np.array_equal(got, ref), (kind, sq, int((got != ref).sum()))
 
 
+def _fp32_scale_for(s, d):
+    """The largest fp32 s_q = s_k whose s = s_q s_k log2(e) / sqrt(d) (fp64, the
+    library's and the oracle's expression) is <= the target: the ABI's end points
+    2^-24 and 0.5 are reached from inside (never skipped)."""
+    sq = np.float32(np.sqrt(s * np.sqrt(d) / 1.4426950408889634))
+    for _ in range(64):
+        if float(sq) * float(sq) * 1.4426950408889634 / np.sqrt(d) <= s:
+            break
+        sq = np.nextafter(sq, np.float32(0))
+    return float(sq)
+
+
 @pytest.mark.parametrize("s", [2.0 ** -24 * 1.01, 1e-6, 3e-5, 2e-4, 1e-3, 7.7e-3, 0.05, 0.3, 0.5])
 def test_scale_range(orc, s):
     # sweep s = s_q s_k log2e / sqrt(d) over the ABI range: exercises the fast and
-    # general quotient magics, p_pre > 0 (large s) and the 127 clamp.
+    # general quotient magics, p_pre > 0 (large s) and the 127 clamp; s = 0.5 is the
+    # upper end point itself (s_inv = 2).
     d = 64
-    sq = float(np.sqrt(s * np.sqrt(d) / 1.4426950408889634))
+    sq = _fp32_scale_for(s, d)
+    p = qf.qflash_derive_params(sq, sq, d)        # must be inside the range
+    assert p["s"] <= s and p["s"] >= s * (1 - 1e-6)
+    if s == 0.5:
+        assert p["s_inv"] == 2
     q, k, v = gen_int8_qkv(2, 197, d, seed=3)
-    try:
-        ref = orc.attention(q, k, v, sq, sq, block_kv=64)
-    except ValueError:
-        pytest.skip("outside the range")
+    ref = orc.attention(q, k, v, sq, sq, block_kv=64)
     got = _gpu_attention(q, k, v, sq, sq, block_kv=64)
     assert np.array_equal(got, ref)
+
+
+# Every kernel configuration (qflash_attn_inst.cuh: cfg 0 CS4xQT1, 1 CS2xQT2, 2 row
+# owner + correction x QT2, 3 row owner x QT1) forced through the debug ABI on a
+# representative subset: generic and row-packed tiles, ragged KV tiles, T_c = 1 and
+# T_c = 9, d = 32 / 64 / 128, multi-wave grids, the fused one-launch step.
+CFG_CASES = [(3, 197, 64, 128, "generic"), (3, 197, 64, 128, "packed"), (3, 197, 64, 64, "generic"),
+             (97, 49, 32, 128, "packed"), (40, 49, 64, 128, "generic"), (3, 1025, 64, 128, "generic"),
+             (2, 257, 128, 128, "generic"), (400, 197, 64, 128, "packed"), (5, 300, 64, 256, "generic")]
+
+
+def _real_codes(orc, P, N, d, seed):
+    # int8 codes with the paper-like distribution: the shared generator's fp32
+    # workload quantized by the oracle (no input comes from the CUDA path)
+    return [orc.quantize(x)[0] for x in gen_real_qkv(P, N, d, seed=seed)]
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3])
+@pytest.mark.parametrize("P,N,d,bkv,variant", CFG_CASES)
+def test_forced_configuration(orc, cfg, P, N, d, bkv, variant):
+    if cfg % 2:
+        q, k, v = gen_int8_qkv(P, N, d, seed=P + N + cfg, kind="uniform")
+    else:
+        q, k, v = _real_codes(orc, P, N, d, seed=P + N + cfg)
+    ref = orc.attention(q, k, v, 0.05, 0.04, block_kv=bkv, nthreads=8)
+    _lib.force_config(cfg)
+    try:
+        got = _gpu_attention(q, k, v, 0.05, 0.04, block_kv=bkv, variant=variant)
+        ran, nseg = _lib.last_config()
+    finally:
+        _lib.force_config(-1)
+    assert (nseg > 1) == (variant == "packed")
+    # a configuration without an instantiation for this shape falls back to the heuristic
+    if ran != cfg:
+        assert not _config_fits(d, bkv if N > bkv else (64 if N <= 64 else 128 if N <= 128 else 256),
+                                nseg, *{0: (4, 1), 1: (2, 2), 2: (1, 2), 3: (1, 1)}[cfg])
+    assert np.array_equal(got, ref), (cfg, ran, int((got != ref).sum()))
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3])
+@pytest.mark.parametrize("name,batch", [("A3", 8), ("A4", 1), ("A1", 1)])
+def test_forced_configuration_fused_step(orc, cfg, name, batch):
+    q, k, v = gen_workload(name, batch, seed=cfg)
+    P, N, d = q.shape
+    _lib.force_config(cfg)
+    try:
+        y = qf.QFlashPipeline(P, N, d, mode="fused")(*_dev(q, k, v))
+        torch.cuda.synchronize()
+        ran, _ = _lib.last_config()
+    finally:
+        _lib.force_config(-1)
+    assert ran == cfg
+    qq, sq = orc.quantize(q)
+    kq, sk = orc.quantize(k)
+    vq, sv = orc.quantize(v)
+    ref = orc.dequantize(orc.attention(qq, kq, vq, sq, sk, block_kv=128, nthreads=8), sv)
+    assert np.array_equal(y.cpu().numpy().view(np.uint32), ref.view(np.uint32))
 
 
 def test_p_clamp_regime(orc):
@@ -257,6 +328,34 @@ def test_quantizer_bit_exact(orc, n, dtype):
     rq, rs = orc.quantize(ref_in)
     assert np.float32(s.item()).view(np.uint32) == np.float32(rs).view(np.uint32)
     assert np.array_equal(xq.cpu().numpy(), rq)
+
+
+@pytest.mark.parametrize("amax", [1e-38, 3e-40, 1e-44])
+def test_quantizer_subnormal_scale(orc, amax):
+    # s = fl32(amax / 127) subnormal: r = 1/s overflows to +Inf below 2^-128, so every
+    # element must take the exact IEEE-division path; amax <= 127 2^-150
+    # underflows s to 0 -> s = 1/127 (R3).  Codes and scale equal the oracle's.
+    rng = np.random.default_rng(7)
+    x = (rng.uniform(-1.0, 1.0, 4099) * amax).astype(np.float32)
+    x[0] = np.float32(amax)
+    x[1:4] = [0.0, np.float32(amax) / 2, -np.float32(amax) / 2]
+    rq, rs = orc.quantize(x)
+    xq, s = qf.qflash_quantize_per_tensor(torch.from_numpy(x).cuda())
+    assert np.float32(s.item()).view(np.uint32) == np.float32(rs).view(np.uint32)
+    assert np.array_equal(xq.cpu().numpy(), rq)
+    # the fused step's prologue quantizer (Q subnormal; K, V normal: s stays in range
+    # only for the codes -- the attention rejects s < 2^-24, so compare codes only)
+    q = x[:4096].reshape(2, 32, 64)
+    k = np.ones_like(q)
+    codes = [torch.empty(q.shape, dtype=torch.int8, device="cuda") for _ in range(3)]
+    ws = torch.zeros(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device="cuda")
+    sc = torch.empty(3, dtype=torch.float32, device="cuda")
+    qf.qflash_forward_fused(*_dev(q, k, k), codes=codes, scales=sc, workspace=ws)
+    torch.cuda.synchronize()
+    fq, fs = orc.quantize(q)
+    assert np.float32(sc[0].item()).view(np.uint32) == np.float32(fs).view(np.uint32)
+    assert np.array_equal(codes[0].cpu().numpy(), fq)
+    assert int(ws[0].item()) == _lib.QFLASH_ERR_SCALE_RANGE
 
 
 def test_quantizer_zero_and_ties(orc):

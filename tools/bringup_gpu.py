@@ -3,13 +3,14 @@
 Checks the stages of one CTA of the fused kernel against the oracle: S (step 1),
 packed P (steps 5-6), final O and l (steps 7-10), then the int8 output."""
 import ctypes
+import os
 import sys
 import traceback
 
 import numpy as np
 import torch
 
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle  # noqa: E402
 from paper_2604_25306_b200 import _lib  # noqa: E402
 from paper_2604_25306_b200.inputs import gen_int8_qkv, gen_workload  # noqa: E402

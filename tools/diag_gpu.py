@@ -1,11 +1,12 @@
 """Diagnose parity failures on the GPU (run by hand under gpurun)."""
 import ctypes
+import os
 import sys
 
 import numpy as np
 import torch
 
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle  # noqa: E402
 import paper_2604_25306_b200 as qf  # noqa: E402
 from paper_2604_25306_b200 import _lib  # noqa: E402

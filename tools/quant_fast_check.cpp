@@ -37,10 +37,13 @@ int main() {
   std::mt19937_64 rng(2604);
   std::uniform_real_distribution<double> ue(-9.0, 2.0);  // amax in [2^-9 ... 2^2] x 127
   long long checked = 0, flagged = 0, wrong = 0;
-  for (int si = 0; si < 400; ++si) {
-    // amax = 127 2^-k every fourth scale: s is a power of two, so exact ties occur
-    const float amax = si % 4 == 0 ? std::ldexp(127.0f, -(si % 20))
-                                   : static_cast<float>(std::exp2(ue(rng)) * 127.0);
+  for (int si = 0; si < 412; ++si) {
+    // amax = 127 2^-k every fourth scale: s is a power of two, so exact ties occur;
+    // the last 12 scales are subnormal (amax ~ 1e-38 .. 1e-43: r = 1/s overflows to
+    // +Inf below s = 2^-128, where every element must be flagged for the exact path)
+    const float amax = si >= 400 ? std::ldexp(1.7f, -126 - 2 * (si - 400))
+                       : si % 4 == 0 ? std::ldexp(127.0f, -(si % 20))
+                                     : static_cast<float>(std::exp2(ue(rng)) * 127.0);
     const float s = amax / 127.0f;  // fl32(amax / 127), as the quantize kernels compute it
     const float r = 1.0f / s;                           // __frcp_rn
     auto check = [&](float x) {
@@ -48,6 +51,11 @@ int main() {
       bool bad = false;
       const int v = qf::quant_fast(x, r, bad);
       ++checked;
+      if (std::isinf(r) && !bad) {
+        if (wrong < 10) printf("r = inf not flagged: s=%a x=%a\n", s, x);
+        ++wrong;
+        return;
+      }
       if (bad) {
         ++flagged;
         return;

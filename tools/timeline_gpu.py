@@ -1,11 +1,12 @@
 """Per-CTA timeline of the fused kernel (clock64 stamps of CTA (0,0)); run under gpurun."""
 import ctypes
+import os
 import sys
 
 import numpy as np
 import torch
 
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2604_25306_b200 import _lib  # noqa: E402
 from paper_2604_25306_b200.inputs import gen_int8_qkv  # noqa: E402
 
