@@ -194,6 +194,30 @@ QFLASH_API qflash_status qflash_forward_fused(const float* q, const float* k, co
                                               float* scales_dev, void* workspace_dev,
                                               qflash_stream_t stream);
 
+/* Sharded per-tensor quantization (Eq. 2 P:L241-246 with dynamic
+ * scales P:L703).  When several GPUs each hold a slab of ONE logical [P, N, d]
+ * tensor (contiguous problem ranges, qflash_partition), the per-tensor scale
+ * s = fl32(amax / 127) must be the amax over every slab:
+ *   qflash_amax_qkv        amax_dev[t] = max |x_t| over this device's slab of Q, K,
+ *                          V (fp32, numel elements each; device float[3], written;
+ *                          0 for numel = 0).  Inputs 16-byte aligned.
+ *   (caller)               MAX all-reduce of the 3 floats across the ranks
+ *   qflash_forward_fused_amax  qflash_forward_fused with the amax taken from
+ *                          amax_dev (device float[3], read) instead of computed: no
+ *                          amax pass and no first grid barrier.  amax_dev = NULL is
+ *                          qflash_forward_fused.  The output of each slab is then
+ *                          byte-identical to the same rows of a 1-GPU run on the
+ *                          whole tensor.  amax_dev must not alias a written buffer.
+ * Errors as qflash_forward_fused; asynchronous on `stream`. */
+QFLASH_API qflash_status qflash_amax_qkv(const float* q, const float* k, const float* v,
+                                         int64_t numel, float* amax_dev, qflash_stream_t stream);
+QFLASH_API qflash_status qflash_forward_fused_amax(const float* q, const float* k, const float* v,
+                                                   const qflash_attn_shape* shape,
+                                                   qflash_variant variant, int8_t* q_q,
+                                                   int8_t* k_q, int8_t* v_q, int8_t* o, float* y,
+                                                   float* scales_dev, void* workspace_dev,
+                                                   const float* amax_dev, qflash_stream_t stream);
+
 /* --------------------------------------------------------------------------
  * Per-head granularity (the paper's per-tensor scales are the
  * H = 1 case).  Problems are the flattened (batch,

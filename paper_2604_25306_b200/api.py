@@ -222,13 +222,29 @@ def qflash_attention_dequant_prepared(q: torch.Tensor, k: torch.Tensor, v: torch
     return out
 
 
+def qflash_amax_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                    out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Device float[3]: max |x| of fp32 Q, K, V (this device's slab)."""
+    _check_qkv(q, k, v, torch.float32)
+    out = torch.empty(3, dtype=torch.float32, device=q.device) if out is None else out
+    _check_scales(out, 3, q.device)
+    check(lib().qflash_amax_qkv(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v), q.numel(), _dev_ptr(out),
+                                _stream(stream)))
+    return out
+
+
 def qflash_forward_fused(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, block_kv: int = 128,
                          variant: str = "auto", out: torch.Tensor | None = None, codes=None,
                          scales: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
-                         out_int8: torch.Tensor | None = None, stream=None):
+                         out_int8: torch.Tensor | None = None, stream=None,
+                         amax: torch.Tensor | None = None):
     """The whole hot path in one cooperative launch: fp32 Q, K, V [P, N, d] ->
-    quantize (in the kernel's prologue) -> integer attention -> fp32 output."""
+    quantize (in the kernel's prologue) -> integer attention -> fp32 output.
+    amax (device float[3], optional): per-tensor amax supplied by the caller (e.g.
+    MAX-all-reduced over the ranks holding slabs of one tensor) instead of computed."""
     _check_qkv(q, k, v, torch.float32)
+    if amax is not None:
+        _check_scales(amax, 3, q.device)
     dev = q.device
     out = torch.empty(q.shape, dtype=torch.float32, device=dev) if out is None else out
     if codes is None:
@@ -244,11 +260,11 @@ def qflash_forward_fused(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, bloc
     _check_scales(scales, 3, dev)
     _check_workspace(workspace, dev)
     shape = _shape(q, block_kv)
-    check(lib().qflash_forward_fused(
+    check(lib().qflash_forward_fused_amax(
         _dev_ptr(q), _dev_ptr(k), _dev_ptr(v), ctypes.byref(shape), _lib.VARIANTS[variant],
         _dev_ptr(codes[0]), _dev_ptr(codes[1]), _dev_ptr(codes[2]),
         _dev_ptr(out_int8) if out_int8 is not None else None, _dev_ptr(out), _dev_ptr(scales),
-        _dev_ptr(workspace), _stream(stream)))
+        _dev_ptr(workspace), _dev_ptr(amax) if amax is not None else None, _stream(stream)))
     return out
 
 

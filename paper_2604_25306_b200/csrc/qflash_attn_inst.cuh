@@ -8,7 +8,7 @@
 
 namespace qf {
 
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FQ, bool PH = false>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ, bool PH = false>
 cudaError_t try_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const AttnArgs& args, int64_t tiles, int sms, cudaStream_t stream) {
   if constexpr (config_fits<D, BC, NSEG, CS, QT>()) {
@@ -23,7 +23,7 @@ cudaError_t try_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUten
 // cfg 2: CS = 1 x QT = 2 (two ping-ponging query tiles, each a row-owner softmax
 //        warpgroup + a correction warpgroup)
 // cfg 3: CS = 1 x QT = 1
-template <int D, bool DBG, bool FQ = false>
+template <int D, bool DBG, int FQ = 0>
 cudaError_t launch_attention_d(int BC, int nseg, int cfg, const CUtensorMap& tq,
                                const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& args,
                                int64_t tiles, int sms, cudaStream_t stream) {
@@ -47,11 +47,26 @@ cudaError_t launch_attention_ph_d(int BC, int nseg, const CUtensorMap& tq, const
                                   int sms, cudaStream_t stream) {
 #define QF_PH(bc, ns)           \
   if (BC == bc && nseg == ns)   \
-    return try_launch<D, bc, ns, 4, 1, false, false, true>(tq, tk, tv, args, tiles, sms, stream);
+    return try_launch<D, bc, ns, 4, 1, false, 0, true>(tq, tk, tv, args, tiles, sms, stream);
   QF_PH(64, 1) QF_PH(128, 1) QF_PH(256, 1)
   QF_PH(64, 2) QF_PH(128, 2) QF_PH(256, 2)
   QF_PH(64, 4) QF_PH(128, 4)
 #undef QF_PH
+  return cudaErrorNotSupported;
+}
+
+// Resident fused step (FQ = 2): generic tiles, cfg 0 (one query tile in flight,
+// CS = 4) or cfg 1 (two groups, CS = 2), T_c <= kStages.
+template <int D>
+cudaError_t launch_resident_d(int BC, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
+                              const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
+                              cudaStream_t stream) {
+#define QF_RS(bc)                                                                          \
+  if (BC == bc)                                                                            \
+    return cfg == 1 ? try_launch<D, bc, 1, 2, 2, false, 2>(tq, tk, tv, args, tiles, sms, stream) \
+                    : try_launch<D, bc, 1, 4, 1, false, 2>(tq, tk, tv, args, tiles, sms, stream);
+  QF_RS(64) QF_RS(128) QF_RS(256)
+#undef QF_RS
   return cudaErrorNotSupported;
 }
 

@@ -365,6 +365,13 @@ struct TileIter {
   }
   __device__ void init(const AttnArgs& a, uint32_t t) {
     i = 0;
+    if (a.resident) {  // resident fused step: CTA b = problem b, group g = query tiles g, g + QT, ...
+      problem = static_cast<int>(blockIdx.x);
+      off = (static_cast<int>(t) - static_cast<int>(blockIdx.x)) >= static_cast<int>(gridDim.x) ? kBlockR : 0;
+      if (off >= a.N) problem = a.P;
+      else fill(a);
+      return;
+    }
     if constexpr (NSEG == 1) {
       problem = a.Tr == 1 ? static_cast<int>(t) : static_cast<int>(__umulhi(t, a.tr_magic));
       off = (static_cast<int>(t) - problem * a.Tr) * kBlockR;
@@ -378,6 +385,12 @@ struct TileIter {
   __device__ bool valid(const AttnArgs& a) const { return problem < a.P; }
   __device__ void next(const AttnArgs& a) {
     ++i;
+    if (a.resident) {
+      off += a.g_mod;  // QT * 128
+      if (off >= a.N) problem = a.P;
+      else fill(a);
+      return;
+    }
     problem += a.g_div;
     off += a.g_mod;
     const int lim = NSEG == 1 ? a.Tr * kBlockR : a.N;
@@ -425,6 +438,129 @@ QF_DEV IntParams head_params(const AttnArgs& a, int problem) {
   const int q = a.H == 1 ? problem : static_cast<int>(__umulhi(static_cast<uint32_t>(problem), a.h_magic));
   const int h = problem - q * a.H;
   return *reinterpret_cast<const IntParams*>(reinterpret_cast<const char*>(a.head_prm) + kHeadPrmStride * h);
+}
+
+// tcgen05.ld of W consecutive 32-bit TMEM columns of this warp's lanes (no wait).
+template <int W>
+QF_DEV void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
+  if constexpr (W == 8) tmem_ld8(taddr, r);
+  else if constexpr (W == 16) tmem_ld16(taddr, r);
+  else if constexpr (W == 32) tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(r));
+  else tmem_ld<W>(taddr, r);
+}
+
+// Row max over the first `valid` of W columns (valid warp-uniform; <= 0: none).
+template <int W>
+QF_DEV int32_t row_max_masked(const uint32_t* s, int valid) {
+  int32_t t = INT32_MIN;
+  if (valid >= W) {
+#pragma unroll
+    for (int e = 0; e < W; ++e) t = max(t, static_cast<int32_t>(s[e]));
+  } else {
+#pragma unroll
+    for (int k = 0; k < W / 8; ++k) {
+      if (8 * k + 8 <= valid) {
+#pragma unroll
+        for (int e = 8 * k; e < 8 * k + 8; ++e) t = max(t, static_cast<int32_t>(s[e]));
+      } else if (8 * k < valid) {
+#pragma unroll
+        for (int e = 8 * k; e < 8 * k + 8; ++e)
+          if (e < valid) t = max(t, static_cast<int32_t>(s[e]));
+      }
+    }
+  }
+  return t;
+}
+
+// Steps (5)(6) for W <= 32 columns: P = Requant(ShiftExp2(S - m_new)) packed 4 per
+// word into pw[W / 4]; columns >= hv (warp-uniform) get P = 0; hv <= 0 leaves pw.
+template <int W, bool FASTQ>
+QF_DEV void p_pack(const uint32_t* sc, int hv, uint32_t mu, uint32_t nmu, uint32_t c3, uint32_t one,
+                   const IntParams& prm, uint32_t* pw) {
+  if (hv >= W) {
+#pragma unroll
+    for (int e = 0; e < W; e += 4)
+      pw[e / 4] = pack4_sat_s8(
+          shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e]), mu, nmu, c3, one, prm),
+          shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 1]), mu, nmu, c3, one, prm),
+          shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e + 2]), mu, nmu, c3, one, prm),
+          shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 3]), mu, nmu, c3, one, prm));
+  } else {
+#pragma unroll
+    for (int k = 0; k < W / 8; ++k) {
+      if (8 * k + 8 <= hv) {
+#pragma unroll
+        for (int e = 8 * k; e < 8 * k + 8; e += 4)
+          pw[e / 4] = pack4_sat_s8(
+              shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e]), mu, nmu, c3, one, prm),
+              shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 1]), mu, nmu, c3, one, prm),
+              shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e + 2]), mu, nmu, c3, one, prm),
+              shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 3]), mu, nmu, c3, one, prm));
+      } else if (8 * k < hv) {
+#pragma unroll
+        for (int e = 8 * k; e < 8 * k + 8; e += 4) {
+          int32_t pv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int32_t x = shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e + u]), mu, nmu, c3, one, prm);
+            pv[u] = (e + u < hv) ? x : 0;
+          }
+          pw[e / 4] = pack4_sat_s8(pv[0], pv[1], pv[2], pv[3]);
+        }
+      }
+    }
+  }
+}
+
+// Step (11) for one row's OW output columns [c OW, c OW + OW): O = floor(O / l)
+// saturated to int8 (R14), stored as int8 and/or dequantized fp32 (DQ row) at
+// flattened output row `orow` (row-packed tiles included).
+template <int D, int OW>
+QF_DEV void normalize_store(const AttnArgs& args, int64_t orow, int c, const uint32_t* o, uint32_t lraw,
+                            const uint32_t* recip) {
+  const Recip rc = make_recip(static_cast<int32_t>(lraw), recip);
+  bool bad = false;
+  uint32_t w[OW / 4];
+#pragma unroll
+  for (int e = 0; e < OW; e += 4)
+    w[e / 4] = pack4_sat_s8(floor_div(static_cast<int32_t>(o[e]), rc, bad),
+                            floor_div(static_cast<int32_t>(o[e + 1]), rc, bad),
+                            floor_div(static_cast<int32_t>(o[e + 2]), rc, bad),
+                            floor_div(static_cast<int32_t>(o[e + 3]), rc, bad));
+  if (bad) {  // (theoretical) quotient outside the table's exact range: long division
+#pragma unroll
+    for (int e = 0; e < OW; e += 4)
+      w[e / 4] = pack4_sat_s8(floor_div_exact(static_cast<int32_t>(o[e]), rc.l),
+                              floor_div_exact(static_cast<int32_t>(o[e + 1]), rc.l),
+                              floor_div_exact(static_cast<int32_t>(o[e + 2]), rc.l),
+                              floor_div_exact(static_cast<int32_t>(o[e + 3]), rc.l));
+  }
+  if (args.out != nullptr) {
+    int8_t* dst = args.out + orow * D + c * OW;
+    if constexpr (OW == 8) {
+      *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < OW / 16; ++e)
+        reinterpret_cast<uint4*>(dst)[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+    }
+  }
+  if (args.out_f32 != nullptr) {
+    // fused dequantization y = s_V * O^ (DQ row): the fp32 bit pattern of every
+    // int8 value comes from a 256-entry table the quantize kernel computed with
+    // the same IEEE multiply as qflash_dequantize -- the attention kernel itself
+    // stays integer-only.
+    const uint32_t dqt = smem_u32(recip + 1024);
+    uint32_t* ydst = reinterpret_cast<uint32_t*>(args.out_f32 + orow * D + c * OW);
+#pragma unroll
+    for (int e = 0; e < OW / 4; ++e) {
+      uint32_t y4[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        y4[b] = static_cast<uint32_t>(lds32(dqt + ((((w[e] >> (8 * b)) & 0xFFu) ^ 0x80u) << 2)));
+      reinterpret_cast<uint4*>(ydst)[e] = make_uint4(y4[0], y4[1], y4[2], y4[3]);
+    }
+  }
 }
 
 template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FASTQ, bool PH = false>
@@ -504,22 +640,7 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
           if (args.dbg_s != nullptr && dbg && j == 0)
             for (int e = 0; e < CW; ++e) args.dbg_s[row * BC + c0 + e] = static_cast<int32_t>(s[e]);
         }
-        if (valid >= CW) {
-#pragma unroll
-          for (int e = 0; e < CW; ++e) tmax = max(tmax, static_cast<int32_t>(s[e]));
-        } else {
-#pragma unroll
-          for (int k = 0; k < CW / 8; ++k) {
-            if (8 * k + 8 <= valid) {
-#pragma unroll
-              for (int e = 8 * k; e < 8 * k + 8; ++e) tmax = max(tmax, static_cast<int32_t>(s[e]));
-            } else if (8 * k < valid) {
-#pragma unroll
-              for (int e = 8 * k; e < 8 * k + 8; ++e)
-                if (e < valid) tmax = max(tmax, static_cast<int32_t>(s[e]));
-            }
-          }
-        }
+        tmax = row_max_masked<CW>(s, valid);
       }
       // (2)(3) combine the partial maxima of the group's CS warpgroups
       if constexpr (CS > 1) {
@@ -564,40 +685,7 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
             tmem_ld32(tS + c0 + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(sc));
             tmem_wait_ld();
           }
-          uint32_t* pw = pk + h * (HW / 4);
-          if (hv >= HW) {
-#pragma unroll
-            for (int e = 0; e < HW; e += 4)
-              pw[e / 4] = pack4_sat_s8(
-                  shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e]), mu, nmu, c3, one, prm),
-                  shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 1]), mu, nmu, c3, one, prm),
-                  shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e + 2]), mu, nmu, c3, one, prm),
-                  shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 3]), mu, nmu, c3, one, prm));
-          } else {
-#pragma unroll
-            for (int k = 0; k < HW / 8; ++k) {
-              if (8 * k + 8 <= hv) {
-#pragma unroll
-                for (int e = 8 * k; e < 8 * k + 8; e += 4)
-                  pw[e / 4] = pack4_sat_s8(
-                      shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e]), mu, nmu, c3, one, prm),
-                      shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 1]), mu, nmu, c3, one, prm),
-                      shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e + 2]), mu, nmu, c3, one, prm),
-                      shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 3]), mu, nmu, c3, one, prm));
-              } else if (8 * k < hv) {
-#pragma unroll
-                for (int e = 8 * k; e < 8 * k + 8; e += 4) {
-                  int32_t pv[4];
-#pragma unroll
-                  for (int u = 0; u < 4; ++u) {
-                    const int32_t x = shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e + u]), mu, nmu, c3, one, prm);
-                    pv[u] = (e + u < hv) ? x : 0;
-                  }
-                  pw[e / 4] = pack4_sat_s8(pv[0], pv[1], pv[2], pv[3]);
-                }
-              }
-            }
-          }
+          p_pack<HW, FASTQ>(sc, hv, mu, nmu, c3, one, prm, pk + h * (HW / 4));
         }
       }
       if constexpr (C::kSepP) {
@@ -717,53 +805,8 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
           if (c == 0) args.dbg_o[row * (D + 1) + D] = static_cast<int32_t>(lraw);
         }
       }
-      if (live) {
-        const Recip rc = make_recip(static_cast<int32_t>(lraw), recip);
-        bool bad = false;
-        uint32_t w[OW / 4];
-#pragma unroll
-        for (int e = 0; e < OW; e += 4)
-          w[e / 4] = pack4_sat_s8(floor_div(static_cast<int32_t>(o[e]), rc, bad),
-                                  floor_div(static_cast<int32_t>(o[e + 1]), rc, bad),
-                                  floor_div(static_cast<int32_t>(o[e + 2]), rc, bad),
-                                  floor_div(static_cast<int32_t>(o[e + 3]), rc, bad));
-        if (bad) {  // (theoretical) quotient outside the table's exact range: long division
-#pragma unroll
-          for (int e = 0; e < OW; e += 4)
-            w[e / 4] = pack4_sat_s8(floor_div_exact(static_cast<int32_t>(o[e]), rc.l),
-                                    floor_div_exact(static_cast<int32_t>(o[e + 1]), rc.l),
-                                    floor_div_exact(static_cast<int32_t>(o[e + 2]), rc.l),
-                                    floor_div_exact(static_cast<int32_t>(o[e + 3]), rc.l));
-        }
-        // flattened output row problem * N + off + row (row-packed tiles included)
-        const int64_t orow = static_cast<int64_t>(ti.problem) * N + ti.off + row;
-        if (args.out != nullptr) {
-          int8_t* dst = args.out + orow * D + c * OW;
-          if constexpr (OW == 8) {
-            *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
-          } else {
-#pragma unroll
-            for (int e = 0; e < OW / 16; ++e)
-              reinterpret_cast<uint4*>(dst)[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
-          }
-        }
-        if (args.out_f32 != nullptr) {
-          // fused dequantization y = s_V * O^ (DQ row): the fp32 bit pattern of
-          // every int8 value comes from a 256-entry table the quantize kernel
-          // computed with the same IEEE multiply as qflash_dequantize -- the
-          // attention kernel itself stays integer-only.
-          const uint32_t dqt = smem_u32(recip + 1024);
-          uint32_t* ydst = reinterpret_cast<uint32_t*>(args.out_f32 + orow * D + c * OW);
-#pragma unroll
-          for (int e = 0; e < OW / 4; ++e) {
-            uint32_t y4[4];
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-              y4[b] = static_cast<uint32_t>(lds32(dqt + ((((w[e] >> (8 * b)) & 0xFFu) ^ 0x80u) << 2)));
-            reinterpret_cast<uint4*>(ydst)[e] = make_uint4(y4[0], y4[1], y4[2], y4[3]);
-          }
-        }
-      }
+      if (live) normalize_store<D, OW>(args, static_cast<int64_t>(ti.problem) * N + ti.off + row, c, o,
+                                       lraw, recip);
     }
     if (dbg && ts_warp) QF_TS(101);
     // The O/l loads above completed (wait::ld) before this thread's next p_full
@@ -824,24 +867,8 @@ __device__ __forceinline__ void softmax_rc_role(const AttnArgs& args, const IntP
           tmem_ld32(tS + 32 * h2, *reinterpret_cast<uint32_t(*)[32]>(sc));
           if (h2 + 1 < NH) tmem_ld32(tS + 32 * h2 + 32, *reinterpret_cast<uint32_t(*)[32]>(sc + 32));
           tmem_wait_ld();
-          const int hv = valid - 32 * h2;
           constexpr int W = NH >= 2 ? 64 : 32;
-          if (hv >= W) {
-#pragma unroll
-            for (int e = 0; e < W; ++e) tmax = max(tmax, static_cast<int32_t>(sc[e]));
-          } else {
-#pragma unroll
-            for (int k = 0; k < W / 8; ++k) {
-              if (8 * k + 8 <= hv) {
-#pragma unroll
-                for (int e = 8 * k; e < 8 * k + 8; ++e) tmax = max(tmax, static_cast<int32_t>(sc[e]));
-              } else if (8 * k < hv) {
-#pragma unroll
-                for (int e = 8 * k; e < 8 * k + 8; ++e)
-                  if (e < hv) tmax = max(tmax, static_cast<int32_t>(sc[e]));
-              }
-            }
-          }
+          tmax = max(tmax, row_max_masked<W>(sc, valid - 32 * h2));
         }
       }
       const int32_t m_new = max(m, tmax);
@@ -865,40 +892,7 @@ __device__ __forceinline__ void softmax_rc_role(const AttnArgs& args, const IntP
             uint32_t sc[32];
             tmem_ld32(tS + 32 * h, sc);
             tmem_wait_ld();
-            uint32_t* pw = pk + 8 * h;
-            if (hv >= 32) {
-#pragma unroll
-              for (int e = 0; e < 32; e += 4)
-                pw[e / 4] = pack4_sat_s8(
-                    shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e]), mu, nmu, c3, one, prm),
-                    shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 1]), mu, nmu, c3, one, prm),
-                    shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e + 2]), mu, nmu, c3, one, prm),
-                    shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 3]), mu, nmu, c3, one, prm));
-            } else {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                if (8 * k + 8 <= hv) {
-#pragma unroll
-                  for (int e = 8 * k; e < 8 * k + 8; e += 4)
-                    pw[e / 4] = pack4_sat_s8(
-                        shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e]), mu, nmu, c3, one, prm),
-                        shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 1]), mu, nmu, c3, one, prm),
-                        shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e + 2]), mu, nmu, c3, one, prm),
-                        shift_exp2_requant<FASTQ, true>(static_cast<int32_t>(sc[e + 3]), mu, nmu, c3, one, prm));
-                } else if (8 * k < hv) {
-#pragma unroll
-                  for (int e = 8 * k; e < 8 * k + 8; e += 4) {
-                    int32_t pv[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                      const int32_t x = shift_exp2_requant<FASTQ, false>(static_cast<int32_t>(sc[e + u]), mu, nmu, c3, one, prm);
-                      pv[u] = (e + u < hv) ? x : 0;
-                    }
-                    pw[e / 4] = pack4_sat_s8(pv[0], pv[1], pv[2], pv[3]);
-                  }
-                }
-              }
-            }
+            p_pack<32, FASTQ>(sc, hv, mu, nmu, c3, one, prm, pk + 8 * h);
           }
         }
       }
@@ -932,7 +926,7 @@ __device__ __forceinline__ void softmax_rc_role(const AttnArgs& args, const IntP
 // then arrives on rel_full, which the MMA warp needs (with p_full) before
 // P V_j.  After the last KV tile: step (11) and the stores (int8 and/or the
 // fused dequantization), before the next tile's first rel_full arrival.
-template <int D, int BC, int NSEG, int QT, bool FQ>
+template <int D, int BC, int NSEG, int QT, int FQ>
 __device__ __forceinline__ void correction_role(const AttnArgs& args, const IntParams& prm,
                                                 uint32_t tmem_group,
                                                 GroupBars<Cfg<D, BC, NSEG, 1, QT>::kNumS> gb,
@@ -1117,10 +1111,31 @@ __device__ __forceinline__ float amax4(float m, const float4& v) {
   return fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
 }
 
+// Resident fused step (FQ = 2): where every codes tile lands in shared memory.
+struct RsLayout {
+  uint8_t* smem;   // 1024-aligned base
+  int group_smem;  // bytes per group
+  int q_off, k_off, v_off;
+  int q_bytes, kv_bytes;
+  int qt;          // groups (QT)
+  int bc;          // B_c (power of two)
+};
+// Byte offset of (row r, byte c) inside a TMA-loaded K-major tile with D-byte rows and
+// the UMMA swizzle of swizzle_layout<D>() (SW32 / SW64 / SW128 = Swizzle<1|2|3, 4, 3>:
+// address bits [4, 4 + b) ^= bits [7, 7 + b)), i.e. exactly where the TMA would put it.
 template <int D>
+QF_DEV uint32_t swz_off(int r, int c) {
+  const uint32_t x = static_cast<uint32_t>(r * D + c);
+  if constexpr (D == 32) return x ^ (((x >> 7) & 1u) << 4);
+  else if constexpr (D == 64) return x ^ (((x >> 7) & 3u) << 4);
+  else return x ^ (((x >> 7) & 7u) << 4);
+}
+
+template <int D, bool RS = false>
 __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float* scratch,
-                                                       IntParams* sprm, uint32_t* dq_table) {
-  namespace cg = cooperative_groups;
+                                                       IntParams* sprm, uint32_t* dq_table,
+                                                       const RsLayout* rs = nullptr) {
+
   constexpr int kVR = QF_KVR;  // register-resident 16-B vectors per tensor and thread
   QF_FQ_TS(a, 0);
   // Warp 0 moves no data: its lane 0 derives the integer constants (~1-2 us of
@@ -1132,11 +1147,43 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   const int64_t gtid = data_thread ? static_cast<int64_t>(blockIdx.x) * ndata_blk + threadIdx.x - 32
                                    : INT64_MAX / 2;
   const int64_t nvec = a.numel >> 2;
-  const bool resident = nvec <= kVR * nthr;  // the whole share stays in registers
+  // external amax (a.amax_in: e.g. MAX-all-reduced over the ranks that shard one
+  // logical tensor): no amax pass, no barrier 1
+  const bool ext = a.amax_in != nullptr;
+  const bool resident = !RS && !ext && nvec <= kVR * nthr;  // the whole share stays in registers
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float m[3] = {0.f, 0.f, 0.f};
   float4 reg[3][kVR];
-  if (resident) {
+  // RS: this CTA's problem (b = blockIdx.x) only -- Q, K, V concatenated as 3 nvp
+  // float4 vectors, vector i of the data thread at tid_d + u * ndata_blk
+  const int64_t nvp = RS ? (static_cast<int64_t>(a.N) * D) >> 2 : 0;
+  const int64_t pbase = RS ? static_cast<int64_t>(blockIdx.x) * nvp : 0;
+  const int tid_d = static_cast<int>(threadIdx.x) - 32;
+  float4 rr[RS ? kRsVR : 1];
+  if constexpr (RS) {
+#pragma unroll
+    for (int u = 0; u < kRsVR; ++u) {
+      const int64_t i = tid_d + static_cast<int64_t>(u) * ndata_blk;
+      const int t = (i >= nvp ? 1 : 0) + (i >= 2 * nvp ? 1 : 0);
+      const float4* src = reinterpret_cast<const float4*>(t == 0 ? a.xin[0] : t == 1 ? a.xin[1] : a.xin[2]);
+      rr[u] = (data_thread && i < 3 * nvp) ? __ldg(src + pbase + (i - t * nvp)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kRsVR; ++u) {
+      const int64_t i = tid_d + static_cast<int64_t>(u) * ndata_blk;
+      const int t = (i >= nvp ? 1 : 0) + (i >= 2 * nvp ? 1 : 0);
+      const float mx = amax4(0.f, rr[u]);
+      m[0] = t == 0 ? fmaxf(m[0], mx) : m[0];
+      m[1] = t == 1 ? fmaxf(m[1], mx) : m[1];
+      m[2] = t == 2 ? fmaxf(m[2], mx) : m[2];
+    }
+  }
+  if (ext) {
+    if (threadIdx.x < 3) scratch[96 + threadIdx.x] = __ldcg(a.amax_in + threadIdx.x);
+  } else {
+  if (RS) {
+    // (loaded above)
+  } else if (resident) {
     // every load of all three tensors in flight before the first reduction
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
@@ -1180,11 +1227,12 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   // No per-thread __threadfence: both grid barriers order memory themselves
   // (grid.sync(): bar.sync, then the arriving thread's gpu-scope fence + atomic;
   // barrier.cluster arrive.release / wait.acquire).  Dropping the redundant
-  // fences saved ~1 us of the A3 step (profiles/r1_cfg_ab.txt).
+  // fences saved ~1 us of the A3 step (profiles/r1_cfg_ab.txt).  A flag barrier
+  // (per-CTA tagged slots polled by every CTA, no atomics) was measured slower:
+  // 2.8 us vs 1.3 us -- the polling traffic competes with the stragglers' loads.
   if (a.cluster_grid) cluster_sync_all();
-  else cg::this_grid().sync();
+  else cooperative_groups::this_grid().sync();
   QF_FQ_TS(a, 2);
-  // 2. global scales (every CTA, identical): s = fl32(amax / 127), R3 for zeros
   if (warp < 3) {
     float b = 0.f;
     float pv[5];  // gridDim.x <= 160: every partial load in flight at once
@@ -1198,14 +1246,18 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
     for (int j = lane + 160; j < static_cast<int>(gridDim.x); j += 32) b = fmaxf(b, __ldcg(&a.partial[warp * gridDim.x + j]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
-    if (lane == 0) {
-      float sc = __fdiv_rn(b, 127.0f);
-      if (sc == 0.0f) sc = 1.0f / 127.0f;  // all-zero tensor (R3)
-      scratch[96 + warp] = sc;
-    }
+    if (lane == 0) scratch[96 + warp] = b;
+  }
+  }  // !ext
+  // 2. global scales (every CTA, identical): s = fl32(amax / 127), R3 for zeros
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    float sc = __fdiv_rn(scratch[96 + threadIdx.x], 127.0f);
+    if (sc == 0.0f) sc = 1.0f / 127.0f;  // all-zero tensor (R3)
+    scratch[100 + threadIdx.x] = sc;
   }
   __syncthreads();
-  const float s3[3] = {scratch[96], scratch[97], scratch[98]};
+  const float s3[3] = {scratch[100], scratch[101], scratch[102]};
   QF_FQ_TS_AT(a, 13, 0, 32);
   // the integer constants (one thread, ~1.3 us of fp64) overlap the quantization
   // of every other warp; the roles read *sprm only after the final __syncthreads
@@ -1234,7 +1286,40 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   float r3[3];
 #pragma unroll
   for (int t = 0; t < 3; ++t) r3[t] = __frcp_rn(s3[t]);
-  if (resident) {
+  if constexpr (RS) {
+    // codes -> the shared-memory tiles the MMAs read (TMA layout and swizzle), and
+    // the global code buffers (outputs); no second grid barrier: this CTA's
+    // attention reads only its own problem
+    constexpr int kV4 = D / 4;  // float4 per row
+#pragma unroll
+    for (int u = 0; u < kRsVR; ++u) {
+      const int64_t i = tid_d + static_cast<int64_t>(u) * ndata_blk;
+      if (data_thread && i < 3 * nvp) {
+        const int t = (i >= nvp ? 1 : 0) + (i >= 2 * nvp ? 1 : 0);
+        const int j = static_cast<int>(i - t * nvp);
+        const uint32_t w = quant4(rr[u], t == 0 ? s3[0] : t == 1 ? s3[1] : s3[2],
+                                  t == 0 ? r3[0] : t == 1 ? r3[1] : r3[2]);
+        reinterpret_cast<uint32_t*>(t == 0 ? a.xq[0] : t == 1 ? a.xq[1] : a.xq[2])[pbase + j] = w;
+        const int r = j / kV4;
+        const int c = (j - r * kV4) * 4;
+        if (t == 0) {
+          const int qt = r >> 7;
+          uint8_t* dst = rs->smem + (rs->qt == 2 ? qt * rs->group_smem : qt * rs->q_bytes) + rs->q_off;
+          *reinterpret_cast<uint32_t*>(dst + swz_off<D>(r & (kBlockR - 1), c)) = w;
+        } else {
+          const int jt = r / rs->bc;
+          const uint32_t o = swz_off<D>(r - jt * rs->bc, c);
+          for (int g = 0; g < rs->qt; ++g)
+            *reinterpret_cast<uint32_t*>(rs->smem + g * rs->group_smem + (t == 1 ? rs->k_off : rs->v_off) +
+                                         jt * rs->kv_bytes + o) = w;
+        }
+      }
+    }
+    fence_proxy_async_smem();  // generic-proxy smem writes -> tcgen05.mma operands
+    QF_FQ_TS(a, 4);
+    QF_FQ_TS(a, 5);
+    return;
+  } else if (resident) {
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
       uint32_t* dst = reinterpret_cast<uint32_t*>(a.xq[t]);
@@ -1268,14 +1353,14 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   fence_proxy_async_global();
   QF_FQ_TS_AT(a, 7, 0, 32);
   if (a.cluster_grid) cluster_sync_all();
-  else cg::this_grid().sync();
+  else cooperative_groups::this_grid().sync();
   fence_proxy_async_global();
   QF_FQ_TS(a, 5);
   QF_FQ_TS_AT(a, 10, 0, 32);
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FQ = false, bool PH = false>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ = 0, bool PH = false>
 __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
     qflash_attn_kernel(const __grid_constant__ CUtensorMap tm_q,
                        const __grid_constant__ CUtensorMap tm_k,
@@ -1347,7 +1432,11 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
   // dependent launch); every global access of this grid comes after the wait.
   griddep_wait();
   IntParams* sprm = reinterpret_cast<IntParams*>(smem + C::kPrm);
-  if constexpr (FQ) {
+  if constexpr (FQ == 2) {
+    const RsLayout rs{smem, C::kGroupSmem, C::kQ, C::kK, C::kV, C::kQBytes, C::kKVBytes, QT, BC};
+    fused_quantize_prologue<D, true>(args, reinterpret_cast<float*>(smem + C::kScratch), sprm, recip + 1024, &rs);
+    __syncthreads();
+  } else if constexpr (FQ) {
     fused_quantize_prologue<D>(args, reinterpret_cast<float*>(smem + C::kScratch), sprm, recip + 1024);
     __syncthreads();
   }
@@ -1387,18 +1476,27 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
           if (!(ok = status_ok())) break;
           mbar_wait_sleep(gb.q_empty(qb), ((ti.i >> 1) - 1) & 1, QF_SLEEP_PROD);
         }
+        if constexpr (FQ == 2) {
+          mbar_arrive(gb.q_full(qb));  // resident: the prologue wrote the codes tile
+        } else {
         mbar_arrive_expect_tx(gb.q_full(qb), ti.nseg * C::kQBytes);
         // segment s: rows of problem + s land at their tile rows, every other
         // tile row is out of range (row < 0 or >= N) and zero-filled
         for (int s = 0; s < ti.nseg; ++s)
           tma_load_3d(sQ + (qb * NSEG + s) * C::kQBytes, &tm_q, gb.q_full(qb), 0,
                       ti.off - s * args.N, ti.problem + s);
+        }
         if (!checked) ++nq;
         for (int j = 0; j < Tc; ++j, ++it) {
           const int st = it % kStages;
           if (it >= kStages) {
             if (!(ok = status_ok())) break;
             mbar_wait_sleep(gb.kv_empty(st), ((it / kStages) - 1) & 1, QF_SLEEP_PROD);
+          }
+          if constexpr (FQ == 2) {
+            mbar_arrive(gb.kv_full(st));  // resident: K, V codes stay in the ring (T_c <= kStages)
+            if (!checked) ++nkv;
+            continue;
           }
           mbar_arrive_expect_tx(gb.kv_full(st), ti.nseg * 2 * C::kKVBytes);
           for (int s = 0; s < ti.nseg; ++s) {
@@ -1578,7 +1676,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
 // Host-side launch (called by the instantiation units).  `tiles` = number of
 // work tiles; the persistent grid is G = min(ceil(tiles / QT), SMs) CTAs whose
 // group g visits tiles b + g G, b + g G + QT G, ...
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FQ = false, bool PH = false>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ = 0, bool PH = false>
 cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                           AttnArgs args, int64_t tiles, int sms, cudaStream_t stream) {
   using C = Cfg<D, BC, NSEG, CS, QT>;
@@ -1594,9 +1692,13 @@ cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CU
     if (dev >= 0 && dev < 16) configured[dev] = 1;
   }
   const int64_t need = (tiles + QT - 1) / QT;
-  const int64_t G = need < sms ? need : sms;
+  const int64_t G = FQ == 2 ? args.P : (need < sms ? need : sms);  // resident: CTA = problem
   const int64_t stride = QT * G;  // tiles between consecutive visits of one group
-  if (NSEG == 1) {
+  if (FQ == 2) {
+    args.resident = 1;
+    args.g_div = 0;
+    args.g_mod = QT * kBlockR;
+  } else if (NSEG == 1) {
     const int64_t Tr = args.Tr;
     args.tr_magic = Tr > 1 ? static_cast<uint32_t>(((1ull << 32) + Tr - 1) / Tr) : 0u;
     args.g_div = static_cast<int32_t>(stride / Tr);

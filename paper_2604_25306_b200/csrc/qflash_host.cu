@@ -38,6 +38,22 @@ cudaError_t launch_fused_d64(int BC, int nseg, int cfg, const CUtensorMap& tq, c
 cudaError_t launch_fused_d128(int BC, int nseg, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
                               const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
                               cudaStream_t stream);
+#define QF_DECL_RS(D)                                                                      \
+  cudaError_t launch_resident_d##D(int BC, int cfg, const CUtensorMap& tq, const CUtensorMap& tk, \
+                                   const CUtensorMap& tv, const AttnArgs& args, int64_t tiles,   \
+                                   int sms, cudaStream_t stream);
+QF_DECL_RS(32)
+QF_DECL_RS(64)
+QF_DECL_RS(128)
+#undef QF_DECL_RS
+inline cudaError_t launch_resident(int D, int BC, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
+                                   const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
+                                   cudaStream_t stream) {
+  if (D == 32) return launch_resident_d32(BC, cfg, tq, tk, tv, args, tiles, sms, stream);
+  if (D == 64) return launch_resident_d64(BC, cfg, tq, tk, tv, args, tiles, sms, stream);
+  if (D == 128) return launch_resident_d128(BC, cfg, tq, tk, tv, args, tiles, sms, stream);
+  return cudaErrorNotSupported;
+}
 cudaError_t launch_attention_ph(int D, int BC, int nseg, const CUtensorMap& tq,
                                 const CUtensorMap& tk, const CUtensorMap& tv,
                                 const AttnArgs& args, int64_t tiles, int sms,
@@ -75,6 +91,8 @@ inline cudaError_t launch_attention(int D, int BC, int nseg, int cfg, const CUte
 cudaError_t launch_quantize(const QuantTensors& t, int ntensors, int dtype, int64_t numel,
                             IntParams* prm_out, int32_t head_dim, cudaStream_t stream,
                             float* partial);
+cudaError_t launch_amax3(const float* q, const float* k, const float* v, int64_t numel, float* amax,
+                         cudaStream_t stream);
 cudaError_t launch_dequantize(const int8_t* xq, float scale, const float* scale_dev,
                               int64_t numel, float* y, cudaStream_t stream);
 }  // namespace qf
@@ -226,6 +244,7 @@ struct FusedIn {
   int8_t* xq[3];
   float* scales;
   void* workspace;
+  const float* amax_in;  // nullptr: the kernel computes the amax itself
 };
 
 qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
@@ -286,6 +305,27 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
       break;
     default: return fail(QFLASH_ERR_INVALID_ARGUMENT, "unknown variant %d", static_cast<int>(variant));
   }
+  // Resident fused step: at most one problem per SM, T_r, T_c <= 2 and
+  // the problem's fp32 Q, K, V fit the data threads' registers -> CTA b quantizes
+  // problem b straight into its shared-memory tiles (one grid barrier, no TMA).
+  bool resident = false;
+  int rs_cfg = 0;
+  {
+    static int rs_env = -1;
+    if (rs_env < 0) {
+      const char* e = getenv("QFLASH_RESIDENT");
+      rs_env = (e != nullptr && e[0] == '0') ? 0 : 1;
+    }
+    const int64_t Tc_rs = (N + bc_eff - 1) / bc_eff;
+    if (rs_env && fin != nullptr && heads == 0 && dbg_s == nullptr && dbg_p == nullptr && dbg_o == nullptr &&
+        dbg_t == nullptr && variant != QFLASH_VARIANT_PACKED && P <= sms && Tr <= 2 && Tc_rs <= 2 &&
+        3ll * N * d / 4 <= static_cast<int64_t>(qf::kRsVR) * (640 - 32)) {
+      rs_cfg = Tr == 2 ? 1 : 0;
+      resident = qf::attention_supported(d, bc_eff, 1, rs_cfg);
+      if (forced_config() >= 0) resident = resident && forced_config() == rs_cfg;
+    }
+  }
+  if (resident) packed = false;
   const int nseg = packed ? nseg_tpl : 1;
   const int64_t tiles = packed ? tiles_packed : tiles_generic;
   // Kernel configuration (qflash_attn_inst.cuh): with more than one wave of
@@ -304,9 +344,10 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
       if (cfg == 0 && qf::attention_supported(d, bc_eff, nseg, c)) cfg = c;
   }
   if (cfg_env >= 0 && heads == 0 && qf::attention_supported(d, bc_eff, nseg, cfg_env)) cfg = cfg_env;
+  if (resident) cfg = rs_cfg;
   if (!qf::attention_supported(d, bc_eff, nseg, cfg))
     return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "no kernel configuration for d=%d block=%d", d, bc_eff);
-  g_last_config = cfg | (nseg << 4);
+  g_last_config = cfg | (nseg << 4) | (resident ? 256 : 0);
   CUtensorMap tq, tk, tv;
   qflash_status st;
   if ((st = make_tmap(&tq, q, P, N, d, 128, 1)) != QFLASH_OK) return st;
@@ -332,6 +373,7 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
       args.xq[t] = fin->xq[t];
     }
     args.scales_out = fin->scales;
+    args.amax_in = fin->amax_in;
     args.prm_out = reinterpret_cast<qf::IntParams*>(fin->workspace);
     args.partial = reinterpret_cast<float*>(static_cast<char*>(fin->workspace) + qf::kWsPartialOffset);
     args.table_out = reinterpret_cast<uint32_t*>(static_cast<char*>(fin->workspace) + qf::kWsDqTableOffset);
@@ -351,6 +393,8 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
     args.H = heads;
     args.h_magic = static_cast<uint32_t>(((1ull << 32) + heads - 1) / heads);
     e = qf::launch_attention_ph(d, bc_eff, nseg, tq, tk, tv, args, tiles, sms, stream);
+  } else if (resident) {
+    e = qf::launch_resident(d, bc_eff, cfg, tq, tk, tv, args, tiles, sms, stream);
   } else {
     e = qf::launch_attention(d, bc_eff, nseg, cfg, tq, tk, tv, args, tiles, sms, dbg,
                              fin != nullptr, stream);
@@ -607,6 +651,37 @@ qflash_status qflash_forward_fused(const float* q, const float* k, const float* 
                                    int8_t* q_q, int8_t* k_q, int8_t* v_q, int8_t* o, float* y,
                                    float* scales_dev, void* workspace_dev,
                                    qflash_stream_t stream) {
+  return qflash_forward_fused_amax(q, k, v, shape, variant, q_q, k_q, v_q, o, y, scales_dev,
+                                   workspace_dev, nullptr, stream);
+}
+
+qflash_status qflash_amax_qkv(const float* q, const float* k, const float* v, int64_t numel,
+                              float* amax_dev, qflash_stream_t stream) {
+  if (numel < 0) return fail(QFLASH_ERR_INVALID_ARGUMENT, "numel < 0");
+  if (!amax_dev || (numel > 0 && (!q || !k || !v)))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || (reinterpret_cast<uintptr_t>(amax_dev) & 3u))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "q, k, v must be 16-byte aligned, amax_dev 4-byte aligned");
+  for (int i = 0; i < 3; ++i) {
+    const float* x = i == 0 ? q : i == 1 ? k : v;
+    if (numel > 0 && overlaps(reinterpret_cast<const int8_t*>(amax_dev), 12, x, 4 * numel))
+      return fail(QFLASH_ERR_INVALID_ARGUMENT, "amax_dev aliases an input");
+  }
+  int dev = 0;
+  qflash_status st;
+  if ((st = check_device(&dev)) != QFLASH_OK) return st;
+  cudaError_t e = qf::launch_amax3(q, k, v, numel, amax_dev, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "amax launch");
+  return QFLASH_OK;
+}
+
+qflash_status qflash_forward_fused_amax(const float* q, const float* k, const float* v,
+                                        const qflash_attn_shape* shape, qflash_variant variant,
+                                        int8_t* q_q, int8_t* k_q, int8_t* v_q, int8_t* o, float* y,
+                                        float* scales_dev, void* workspace_dev, const float* amax_dev,
+                                        qflash_stream_t stream) {
+  if (amax_dev != nullptr && (reinterpret_cast<uintptr_t>(amax_dev) & 3u))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "amax_dev must be 4-byte aligned");
   int bc = 0;
   qflash_status st = validate_shape(shape, &bc);
   if (st != QFLASH_OK) return st;
@@ -658,6 +733,14 @@ qflash_status qflash_forward_fused(const float* q, const float* k, const float* 
   fin.xq[2] = v_q;
   fin.scales = scales_dev;
   fin.workspace = workspace_dev;
+  fin.amax_in = amax_dev;
+  if (amax_dev != nullptr) {
+    const int8_t* am = reinterpret_cast<const int8_t*>(amax_dev);
+    if (overlaps(am, 12, ws, QFLASH_DSCALE_WORKSPACE_BYTES) ||
+        overlaps(am, 12, reinterpret_cast<const int8_t*>(scales_dev), 12) ||
+        overlaps(am, 12, reinterpret_cast<const int8_t*>(y), 4 * n))
+      return fail(QFLASH_ERR_INVALID_ARGUMENT, "amax_dev aliases a written buffer");
+  }
   return launch_common(q_q, k_q, v_q, shape, bc, variant, o, nullptr, nullptr,
                        reinterpret_cast<cudaStream_t>(stream), y, &fin, 0);
 }

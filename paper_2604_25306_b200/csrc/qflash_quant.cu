@@ -699,6 +699,54 @@ cudaError_t launch_quantize(const QuantTensors& t, int ntensors, int dtype, int6
   }
 }
 
+// amax of three fp32 tensors (blockIdx.y = tensor) -> amax[t] (zeroed by the host
+// first): block max, then an unsigned atomicMax on the bits (non-negative floats
+// order like their bit patterns).  Used by sharded quantization:
+// local amax -> MAX all-reduce -> qflash_forward_fused_amax.
+__global__ void __launch_bounds__(kQThreads) amax3_kernel(const float* __restrict__ q,
+                                                         const float* __restrict__ k,
+                                                         const float* __restrict__ v, int64_t numel,
+                                                         unsigned int* amax) {
+  const float* x = blockIdx.y == 0 ? q : (blockIdx.y == 1 ? k : v);
+  const int64_t nv = numel >> 2;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  float m0 = 0.f, m1 = 0.f;
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + stride < nv; i += 2 * stride) {
+    const float4 a = __ldg(x4 + i), b = __ldg(x4 + i + stride);
+    m0 = fmaxf(m0, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
+    m1 = fmaxf(m1, fmaxf(fmaxf(fabsf(b.x), fabsf(b.y)), fmaxf(fabsf(b.z), fabsf(b.w))));
+  }
+  if (i < nv) {
+    const float4 a = __ldg(x4 + i);
+    m0 = fmaxf(m0, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
+  }
+  for (int64_t j = nv * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < numel; j += stride)
+    m0 = fmaxf(m0, fabsf(x[j]));
+  float mm = fmaxf(m0, m1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+  __shared__ float red[kQThreads / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mm;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b = red[0];
+#pragma unroll
+    for (int w = 1; w < kQThreads / 32; ++w) b = fmaxf(b, red[w]);
+    atomicMax(amax + blockIdx.y, __float_as_uint(b));
+  }
+}
+
+cudaError_t launch_amax3(const float* q, const float* k, const float* v, int64_t numel, float* amax,
+                         cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(amax, 0, 3 * sizeof(float), stream);
+  if (e != cudaSuccess || numel == 0) return e;
+  dim3 grid(stream_grid((numel + 7) / 8, 3), 3);
+  amax3_kernel<<<grid, kQThreads, 0, stream>>>(q, k, v, numel, reinterpret_cast<unsigned int*>(amax));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dequantize(const int8_t* xq, float scale, const float* scale_dev, int64_t numel,
                               float* y, cudaStream_t stream) {
   dim3 grid(stream_grid((numel + 15) / 16, 1));

@@ -617,3 +617,50 @@ def test_device_constants_equal_host_constants(d):
         assert (rel, w[8], w[9], w[10], w[11], w[12]) == (
             hp["rel_magic"], hp["rel_shift"], hp["p_max"], hp["r_p"], hp["m_p"], hp["n"])
         assert s_dev == hp["s"]
+
+
+# ------------------------------------------------ sharded quantization
+@pytest.mark.parametrize("name,batch,world", [("A3", 8, 2), ("A1", 8, 3), ("A4", 1, 4), ("L14", 2, 2)])
+def test_sharded_fused_step_equals_single_gpu(orc, name, batch, world):
+    # Strong scaling of ONE logical batch: every "rank" (here: a slab on the same GPU)
+    # takes qflash_partition's contiguous problem range, computes its local amax
+    # (qflash_amax_qkv), the MAX all-reduce is emulated by torch.maximum, and
+    # qflash_forward_fused_amax quantizes with the global scales.  The concatenated
+    # slab outputs are byte-identical to the 1-GPU fused step on the whole batch, and
+    # the codes / scales to the oracle's quantizer.
+    q, k, v = gen_workload(name, batch, seed=11)
+    P = q.shape[0]
+    dq, dk, dv = _dev(q, k, v)
+    full = qf.qflash_forward_fused(dq, dk, dv).cpu().numpy()
+    slabs = [qf.qflash_partition(P, world, r) for r in range(world)]
+    amax = torch.zeros(3, device="cuda")
+    for b, c in slabs:
+        if c:
+            amax = torch.maximum(amax, qf.qflash_amax_qkv(dq[b:b + c], dk[b:b + c], dv[b:b + c]))
+    ref_amax = [np.float32(np.abs(x).max()) for x in (q, k, v)]
+    assert [np.float32(x) for x in amax.cpu().numpy()] == ref_amax
+    out = np.empty_like(full)
+    for b, c in slabs:
+        if not c:
+            continue
+        codes = [torch.empty((c,) + q.shape[1:], dtype=torch.int8, device="cuda") for _ in range(3)]
+        sc = torch.empty(3, dtype=torch.float32, device="cuda")
+        y = qf.qflash_forward_fused(dq[b:b + c], dk[b:b + c], dv[b:b + c], codes=codes, scales=sc,
+                                    amax=amax)
+        out[b:b + c] = y.cpu().numpy()
+        for t, x in enumerate((q, k, v)):
+            rq, rs = orc.quantize(x)
+            assert np.float32(sc[t].item()).view(np.uint32) == np.float32(rs).view(np.uint32)
+            assert np.array_equal(codes[t].cpu().numpy(), rq[b:b + c])
+    assert np.array_equal(out.view(np.uint32), full.view(np.uint32))
+
+
+def test_amax_qkv_edge_cases():
+    z = torch.zeros((2, 49, 32), device="cuda")
+    assert qf.qflash_amax_qkv(z, z, z).tolist() == [0.0, 0.0, 0.0]
+    e = torch.zeros((0, 49, 32), device="cuda")
+    assert qf.qflash_amax_qkv(e, e, e).tolist() == [0.0, 0.0, 0.0]
+    x = torch.randn((3, 197, 64), device="cuda")
+    x[1, 5, 7] = -1e30
+    a = qf.qflash_amax_qkv(x, x * 2, -x).cpu()
+    assert a.tolist() == [float(np.float32(1e30)), float(np.float32(2e30)), float(np.float32(1e30))]
