@@ -199,28 +199,108 @@ def run_reference(args):
     return 0
 
 
-def cpu_baseline(name, batch, w, block_kv, budget_s=12.0):
-    """The oracle timed on the host cores on a bounded sample (rank 0, N=1)."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline(name, batch, w, block_kv, budget_s=10.0):
+    """The oracle (as it stands) timed on the host cores on a bounded sample (rank 0,
+    N=1): all hardware threads, then a single thread on a smaller sample."""
     import oracle
     P, N, d = w.problems(batch), w.seq_len, w.head_dim
-    sample_p = min(P, max(1, {"L14": 4}.get(name, P)))
-    q, k, v = gen_real_qkv(sample_p, N, d, seed=0, family=w.family)
     cores = os.cpu_count() or 1
-    reps, t_total = 0, 0.0
-    while t_total < budget_s:
-        t0 = time.perf_counter()
-        qq, sq = oracle.quantize(q)
-        kq, sk = oracle.quantize(k)
-        vq, sv = oracle.quantize(v)
-        o = oracle.attention(qq, kq, vq, sq, sk, block_kv=block_kv, nthreads=cores)
-        oracle.dequantize(o, sv)
-        t_total += time.perf_counter() - t0
-        reps += 1
-    dt = t_total / reps
-    return {"value": algorithmic(sample_p, N, d)["int8_ops"] / dt / 1e12, "unit": "TOPS",
-            "cores": cores, "kind": "oracle",
-            "sample": f"{sample_p} of {P} problems x {reps} reps ({t_total:.1f} s), "
-                      "quantize+attention+dequantize, all host threads"}
+
+    def timed(sample_p, nthreads, budget):
+        q, k, v = gen_real_qkv(sample_p, N, d, seed=0, family=w.family)
+        reps, t_total = 0, 0.0
+        while t_total < budget:
+            t0 = time.perf_counter()
+            qq, sq = oracle.quantize(q)
+            kq, sk = oracle.quantize(k)
+            vq, sv = oracle.quantize(v)
+            o = oracle.attention(qq, kq, vq, sq, sk, block_kv=block_kv, nthreads=nthreads)
+            oracle.dequantize(o, sv)
+            t_total += time.perf_counter() - t0
+            reps += 1
+        dt = t_total / reps
+        return algorithmic(sample_p, N, d)["int8_ops"] / dt / 1e12, reps, t_total
+
+    sample_p = min(P, max(1, {"L14": 4}.get(name, P)))
+    v_all, reps, tt = timed(sample_p, cores, budget_s)
+    sample_1 = min(P, max(1, {"L14": 1}.get(name, min(P, 8))))
+    v_one, reps1, tt1 = timed(sample_1, 1, budget_s / 2)
+    return {"value": v_all, "unit": "TOPS", "cores": cores, "kind": "oracle",
+            "sample": f"{sample_p} of {P} problems x {reps} reps ({tt:.1f} s), "
+                      "quantize+attention+dequantize, all host threads",
+            "single_thread": {"value": v_one, "unit": "TOPS", "cores": 1,
+                              "sample": f"{sample_1} of {P} problems x {reps1} reps ({tt1:.1f} s)"},
+            "cpu_model": cpu_model()}
+
+
+def spawn_ranks(args):
+    """--gpus N without a torchrun environment: re-launch this script under
+    torch.distributed.run with one process per GPU (127.0.0.1 rendezvous)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    os.execvp(cmd[0], cmd)
+
+
+def measured_peaks(pk):
+    """Roofline denominators: the committed microbenchmarks (profiles/r2_peaks.json:
+    tcgen05 kind::i8 GEMM, ShiftExp2 integer mix), else nominal figures (stated)."""
+    out = {}
+    try:
+        out = json.load(open(os.path.join(ROOT, "profiles", "r2_peaks.json")))
+    except Exception:
+        pass
+    sm_clk_ghz = (pk.get("sm_max_mhz") or 1965.0) / 1e3
+    if "int8_tops" not in out:
+        out["int8_tops"] = 2.0 * pk.get("bf16_tflops", 1652.8)
+        out["int8_source"] = "nominal: measured bf16 burst x 2 (int8/bf16 ratio)"
+    if "alu_elems_per_s" not in out:
+        out["alu_elems_per_s"] = SMS * INT32_LANES * sm_clk_ghz * 1e9 / ALU_OPS_PER_ELEM
+        out["alu_source"] = "nominal: 148 SM x 128 int32 lanes x %.3f GHz / 10 ops per element" % sm_clk_ghz
+    return out
+
+
+def graph_time(graphs, stream, reps, warm=3):
+    """ms per replay of `graphs` (cycled), device events on `stream`, GPU kept busy."""
+    import torch
+    with torch.cuda.stream(stream):
+        for i in range(warm):
+            graphs[i % len(graphs)].replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(2_000_000)
+        e0.record(stream)
+        for i in range(reps):
+            graphs[i % len(graphs)].replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def capture(fn, stream):
+    import torch
+    with torch.cuda.stream(stream):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        fn()
+    return g
 
 
 def main():
@@ -232,10 +312,14 @@ def main():
     ap.add_argument("--workload", default=None, help="catalog name (default: BASELINE configs[1])")
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--block-kv", type=int, default=128)
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: each rank a batch-sized slab of a world x batch global batch, per-slab "
+                         "scales, no collective; strong: ONE batch partitioned over the ranks, global "
+                         "per-tensor scales via a MAX all-reduce of the amax every step")
     ap.add_argument("--ref-problems", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the per-stage timing set")
     ap.add_argument("--mode", default="fused", choices=["fused", "two", "three"],
                     help="step form: one cooperative launch (default), or 2 / 3 launches")
     ap.add_argument("--variant", default="auto", choices=["auto", "generic", "packed"],
@@ -247,14 +331,20 @@ def main():
 
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%d (launch one process per GPU)"
+                         % (args.gpus, world))
 
     import torch
     import torch.distributed as dist
 
     import paper_2604_25306_b200 as qfl
     from paper_2604_25306_b200 import _lib
+    from paper_2604_25306_b200.inputs import gen_real_qkv_slab
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -263,21 +353,22 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     name, batch, w = workload_from_args(args)
-    P_total, N, d = w.problems(batch), w.seq_len, w.head_dim
-    if args.scaling == "strong" and world > 1:
-        _, P_local = qfl.qflash_partition(P_total, world, rank)
-    else:
-        P_local = P_total
+    P_batch, N, d = w.problems(batch), w.seq_len, w.head_dim
+    strong = args.scaling == "strong" and world > 1
+    P_total = P_batch if args.scaling == "strong" else world * P_batch
+    p_begin, P_local = qfl.qflash_partition(P_total, world, rank)
     alg = algorithmic(P_local, N, d)
+    if args.scales == "per-head" and strong:
+        raise SystemExit("bench.py: --scales per-head supports weak scaling only")
 
-    # ---- input sets: fp32 Q, K, V resident in HBM, enough sets to defeat L2
+    # ---- input sets: fp32 Q, K, V of this rank's slab resident in HBM; enough sets
+    # (sign flips / rolls of the slab) that every step reads cold inputs (> 2x L2)
     set_bytes = alg["step_bytes"]
-    n_sets = int(min(64, max(2, np.ceil(2.0 * L2_BYTES / set_bytes) + 1)))
-    q0, k0, v0 = gen_real_qkv(P_local, N, d, seed=rank, family=w.family)
+    n_sets = int(min(64, max(2, np.ceil(2.0 * L2_BYTES / max(set_bytes, 1)) + 1)))
+    q0, k0, v0 = gen_real_qkv_slab(P_total, N, d, p_begin, P_local, seed=0, family=w.family)
     base = [torch.from_numpy(a).to(dev) for a in (q0, k0, v0)]
     sets = []
     for i in range(n_sets):
-        # distinct bytes per set (sign flips keep the distribution and the scales)
         sgn = -1.0 if (i % 2) else 1.0
         sets.append([(t * sgn).roll(shifts=i, dims=1).contiguous() for t in base])
     if args.scales == "per-head":
@@ -288,18 +379,30 @@ def main():
         pipes = [qfl.QFlashPipeline(P_local, N, d, block_kv=args.block_kv, device=dev, mode=args.mode,
                                     variant=args.variant)
                  for _ in range(n_sets)]
-
     stream = torch.cuda.Stream(device=dev)
-    graphs = []
-    with torch.cuda.stream(stream):
-        for p, s in zip(pipes, sets):  # eager once (sets up kernel attributes), then capture
-            p(*s)
-        torch.cuda.synchronize()
-        for p, s in zip(pipes, sets):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                p(*s)
-            graphs.append(g)
+    amax_bufs = [torch.zeros(3, dtype=torch.float32, device=dev) for _ in range(n_sets)]
+
+    if strong:
+        # per step: local amax (graph) -> NCCL MAX all-reduce of 3 floats (eager, on the
+        # stream) -> fused step with the global amax (graph)
+        g_amax = [capture(lambda s=s, a=a: qfl.qflash_amax_qkv(*s, out=a, stream=stream), stream)
+                  for s, a in zip(sets, amax_bufs)]
+        g_step = [capture(lambda p=p, s=s, a=a: qfl.qflash_forward_fused(
+            *s, args.block_kv, args.variant, out=p.out, codes=p.qkv_q, scales=p.scales,
+            workspace=p.workspace, stream=stream, amax=a), stream)
+            for p, s, a in zip(pipes, sets, amax_bufs)]
+
+        def run_step(i):
+            g_amax[i % n_sets].replay()
+            dist.all_reduce(amax_bufs[i % n_sets], op=dist.ReduceOp.MAX)
+            g_step[i % n_sets].replay()
+        launches_per_step = 2
+    else:
+        graphs = [capture(lambda p=p, s=s: p(*s, stream=stream), stream) for p, s in zip(pipes, sets)]
+
+        def run_step(i):
+            graphs[i % n_sets].replay()
+        launches_per_step = pipes[0].launches()
     torch.cuda.synchronize()
     status = int(pipes[0].workspace[0].item())
     if status != 0:
@@ -309,7 +412,7 @@ def main():
     sampler.start()
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
-            graphs[i % n_sets].replay()
+            run_step(i)
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, barrier + sync on both sides, device events
@@ -322,126 +425,127 @@ def main():
         torch.cuda._sleep(2_000_000)  # host head start so graph replays queue back to back
         ev0.record(stream)
         for i in range(args.steps):
-            graphs[i % n_sets].replay()
+            run_step(i)
         ev1.record(stream)
     torch.cuda.synchronize()
     t_host1 = time.perf_counter()
     if world > 1:
         dist.barrier()
     elapsed_ms = ev0.elapsed_time(ev1)
-    t_max = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+    t_all = torch.zeros(world, device=dev, dtype=torch.float64)
+    t_all[rank] = elapsed_ms
     if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    elapsed_ms = float(t_max.item())
+        dist.all_reduce(t_all, op=dist.ReduceOp.SUM)
+    rank_ms = [float(x) / args.steps for x in t_all.cpu().tolist()]
+    elapsed_ms = max(float(x) for x in t_all.cpu().tolist())
     ms_per_step = elapsed_ms / args.steps
-    ops_all = alg["int8_ops"] * (world if args.scaling == "weak" else 1) * args.steps
-    if args.scaling == "strong" and world > 1:
-        ops_all = algorithmic(P_total, N, d)["int8_ops"] * args.steps
-    value = ops_all / (elapsed_ms * 1e-3) / 1e12
+    # every rank processed its slab each step: the whole job's ops / max-over-ranks time
+    value = algorithmic(P_total, N, d)["int8_ops"] * args.steps / (elapsed_ms * 1e-3) / 1e12
     clocks = sampler.summary(t_host0, t_host1)
 
-    # ---- dominant kernel measured alone with events on its stream: the fused
-    # step kernel (quantize prologue + attention + dequantize epilogue) when the
-    # step is one launch, else the attention kernel with the fused dequantize
-    k_launch = min(args.steps, 2000)
-    one_launch = pipes[0].launches() == 1
+    # ---- dominant kernel, graph-timed like the step: the fused step kernel (the step
+    # itself when the step is one launch), else the attention launches alone
+    one_launch = (not strong) and launches_per_step == 1
     per_head = args.scales == "per-head"
-    ka, kb = [], []
-    with torch.cuda.stream(stream):
-        # head start covering the host cost of every eager launch (<= 50 us each),
-        # so each event pair brackets exactly one kernel with the GPU never idle
-        torch.cuda._sleep(int(k_launch * 50e-6 * 2.0e9))
-        for i in range(k_launch):
-            p = pipes[i % n_sets]
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            if one_launch:
-                p(*sets[i % n_sets], stream=stream)
-            elif per_head:
-                p.attention(stream=stream)
-            else:
-                qfl.qflash_attention_dequant_prepared(p.qkv_q[0], p.qkv_q[1], p.qkv_q[2],
-                                                      p.workspace, args.block_kv, args.variant,
-                                                      out=p.out, stream=stream)
-            b.record(stream)
-            ka.append(a)
-            kb.append(b)
-    torch.cuda.synchronize()
-    durs = sorted(x.elapsed_time(y) for x, y in zip(ka, kb))
-    attn_ms = statistics.mean(durs[: max(1, int(0.9 * len(durs)))])  # drop the slowest 10 %
-
-    # ---- for context: the two-launch form of the step, stage by stage (eager)
-    k_bd = 0 if per_head else min(args.steps, 500)
-    evs = []
-    with torch.cuda.stream(stream):
-        torch.cuda._sleep(int(k_bd * 120e-6 * 2.0e9))
-        for i in range(k_bd):
-            p = pipes[i % n_sets]
-            s_in = sets[i % n_sets]
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-            e[0].record(stream)
-            qfl.qflash_quantize_qkv_prepare(*s_in, outs=p.qkv_q, scales=p.scales,
-                                            workspace=p.workspace, stream=stream)
-            e[1].record(stream)
-            qfl.qflash_attention_dequant_prepared(p.qkv_q[0], p.qkv_q[1], p.qkv_q[2], p.workspace,
-                                                  args.block_kv, out=p.out, stream=stream)
-            e[2].record(stream)
-            evs.append(e)
-    torch.cuda.synchronize()
-    def _med(a, b):
-        return statistics.median(x[a].elapsed_time(x[b]) for x in evs) * 1e3 if evs else None
-    breakdown = {"two_launch_quantize_qkv_us": _med(0, 1), "two_launch_attention_dequant_us": _med(1, 2),
-                 "note": "eager launches, GPU kept busy; medians over %d steps" % k_bd}
-    # share of the step (the ncu launch list must agree on this share)
+    k_launch = min(args.steps, 2000)
+    if one_launch:
+        kgraphs = graphs
+        kname = "qflash_attn_kernel<FQ> (fused step: quantize prologue + attention + dequantize)"
+    elif strong:
+        kgraphs = g_step
+        kname = "qflash_attn_kernel<FQ> (fused step with the all-reduced amax)"
+    elif per_head:
+        kgraphs = [capture(lambda p=p: p.attention(stream=stream), stream) for p in pipes]
+        kname = "derive_per_head + qflash_attn_kernel<PH> (int8 out)"
+    else:
+        kgraphs = [capture(lambda p=p: qfl.qflash_attention_dequant_prepared(
+            p.qkv_q[0], p.qkv_q[1], p.qkv_q[2], p.workspace, args.block_kv, args.variant,
+            out=p.out, stream=stream), stream) for p in pipes]
+        kname = "qflash_attn_kernel (fused dequantize epilogue)"
+    attn_ms = graph_time(kgraphs, stream, k_launch)
     attn_share = attn_ms / ms_per_step
-    launches_per_step = pipes[0].launches()
 
-    kbytes = (alg["fused_step_bytes"] if one_launch else alg["attn_bytes"] if per_head
+    # ---- the per-stage timing set: attention alone on int8 inputs,
+    # the quantizer and the dequantizer alone (graphs, cold sets), single-call latency
+    extra = None
+    if not args.no_extra and not per_head:
+        p0 = pipes[0]
+        q_prep = [capture(lambda p=p, s=s: qfl.qflash_quantize_qkv_prepare(
+            *s, outs=p.qkv_q, scales=p.scales, workspace=p.workspace, stream=stream), stream)
+            for p, s in zip(pipes, sets)]
+        a_int8 = [capture(lambda p=p: qfl.qflash_attention_int8_prepared(
+            p.qkv_q[0], p.qkv_q[1], p.qkv_q[2], p.workspace, args.block_kv, args.variant,
+            out=p.o_q, stream=stream), stream) for p in pipes]
+        dq = [capture(lambda p=p: qfl.qflash_dequantize(p.o_q, p.scales[2:3], out=p.out, stream=stream),
+                      stream) for p in pipes]
+        t_q = graph_time(q_prep, stream, k_launch)
+        t_a = graph_time(a_int8, stream, k_launch)
+        t_d = graph_time(dq, stream, k_launch)
+        # single call, host wall clock around one synchronized eager step (launch included)
+        lat = []
+        for i in range(20):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            p0(*sets[i % n_sets], stream=stream)
+            torch.cuda.synchronize()
+            lat.append(time.perf_counter() - t0)
+        E = P_local * N * d
+        extra = {
+            "attention_int8_us": t_a * 1e3,
+            "attention_int8_tops": alg["int8_ops"] / (t_a * 1e-3) / 1e12,
+            "quantize_qkv_us": t_q * 1e3,
+            "quantize_qkv_gbs": 3 * E * 5 / (t_q * 1e-3) / 1e9,
+            "dequantize_us": t_d * 1e3,
+            "dequantize_gbs": E * 5 / (t_d * 1e-3) / 1e9,
+            "single_call_wall_us": statistics.median(lat) * 1e6,
+            "note": "CUDA-graph replays over the rotating cold sets; attention on the int8 codes "
+                    "(qflash_attention_int8_prepared), quantizer = qflash_quantize_qkv_prepare "
+                    "(bytes 3 E (4 + 1)), dequantizer bytes E (1 + 4); single call = host wall "
+                    "clock of one synchronized eager fused step",
+        }
+
+    kbytes = (alg["fused_step_bytes"] if (one_launch or strong) else alg["attn_bytes"] if per_head
               else alg["attn_dq_bytes"])
     pk = peaks()
-    sm_clk_ghz = (pk.get("sm_max_mhz") or 1965.0) / 1e3
-    alu_peak = SMS * INT32_LANES * sm_clk_ghz * 1e9 / 1e12      # T int32 ops/s
+    mp = measured_peaks(pk)
+    alu_peak = ALU_OPS_PER_ELEM * mp["alu_elems_per_s"] / 1e12
     alu_achieved = ALU_OPS_PER_ELEM * alg["score_elems"] / (attn_ms * 1e-3) / 1e12
-    int8_peak_tops = 2.0 * pk.get("bf16_tflops", 1674.9)          # measured bf16 x nominal 2x
     roofline = {
-        "kernel": ("qflash_attn_kernel<FQ> (fused step: quantize prologue + attention + dequantize)"
-                   if one_launch else "derive_per_head + qflash_attn_kernel<PH> (int8 out)" if per_head
-                   else "qflash_attn_kernel (fused dequantize epilogue)"),
+        "kernel": kname,
         "bound": "alu", "achieved": alu_achieved,
         "peak": alu_peak, "unit": "T int32-op/s", "frac": alu_achieved / alu_peak,
         "traffic": None,
         "per_unit": "10 int32 ops per score element (SURVEY 8(d)); units = N^2 P per launch",
-        "peak_source": "148 SM x 128 int32 lanes x %.3f GHz (B200_PROFILING sm max clock)" % sm_clk_ghz,
+        "peak_source": mp.get("alu_source"),
         "attn_us": attn_ms * 1e3, "attn_share_of_step": attn_share,
-        "step_breakdown": breakdown,
+        "attn_timing": "CUDA graph of the kernel's launches alone over the rotating sets",
         "tensor": {"achieved_tops": alg["int8_ops"] / (attn_ms * 1e-3) / 1e12,
-                   "peak_tops": int8_peak_tops,
-                   "frac": alg["int8_ops"] / (attn_ms * 1e-3) / 1e12 / int8_peak_tops,
-                   "peak_source": "measured bf16 burst x 2 (int8/bf16 nominal ratio)"},
+                   "peak_tops": mp["int8_tops"],
+                   "frac": alg["int8_ops"] / (attn_ms * 1e-3) / 1e12 / mp["int8_tops"],
+                   "peak_source": mp.get("int8_source")},
         "hbm": {"achieved_gbs": kbytes / (attn_ms * 1e-3) / 1e9,
                 "peak_gbs": pk.get("hbm_gbs"),
                 "frac": kbytes / (attn_ms * 1e-3) / 1e9 / pk.get("hbm_gbs", 6452.5),
                 "bytes_per_launch": kbytes,
-                "per_unit": "16 N d B per problem (fp32 Q, K, V in + fp32 O out)" if one_launch
+                "per_unit": "16 N d B per problem (fp32 Q, K, V in + fp32 O out)" if (one_launch or strong)
                             else "4 N d B per problem (int8 Q, K, V in + int8 O out)" if per_head
                             else "7 N d B per problem (int8 Q, K, V in + fp32 O out)"},
     }
     traffic_file = os.path.join(ROOT, "profiles", "attn_traffic.json")
     if os.path.exists(traffic_file):
         try:
-            tj = json.load(open(traffic_file)).get(f"{name}_b{batch}" + ("_fused" if one_launch else "_ph" if per_head else ""))
+            tj = json.load(open(traffic_file)).get(
+                f"{name}_b{batch}" + ("_fused" if one_launch else "_ph" if per_head else ""))
             if tj:
                 roofline["traffic"] = tj
         except Exception:
             pass
 
-    # ---- end to end through the public API with host buffers
+    # ---- end to end through the public serving API with host buffers (weak: each
+    # rank serves its own slab; strong: the slab's scales would need the collective,
+    # so e2e is reported for weak scaling only)
     e2e = None
-    if not args.no_e2e:
-        # end to end through the public serving API: every step copies that step's
-        # fp32 Q, K, V from pinned host memory, runs the hot path and copies the fp32
-        # output back; consecutive steps overlap on two buffer sets / streams
-        # (QFlashHostPipeline).  Two distinct host batches alternate.
+    if not args.no_e2e and not strong:
         host_sets = []
         for i in range(2):
             sgn = -1.0 if i else 1.0
@@ -467,7 +571,6 @@ def main():
         e1.record(torch.cuda.current_stream())
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1)
-        # the results are checked: both host outputs equal the device pipeline's
         ref_out = pipes[0](*[t_.to(dev) for t_ in host_sets[(k_e2e - 1) % 2]], stream=stream)
         torch.cuda.synchronize()
         assert torch.equal(ref_out.cpu(), houts[(k_e2e - 1) % 2]), "e2e output mismatch"
@@ -475,36 +578,81 @@ def main():
         if world > 1:
             dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
         e_ms = float(e_t.item())
-        e2e = {"value": alg["int8_ops"] * (world if args.scaling == "weak" else 1) * k_e2e
-                        / (e_ms * 1e-3) / 1e12,
+        e2e = {"value": algorithmic(P_total, N, d)["int8_ops"] * k_e2e / (e_ms * 1e-3) / 1e12,
                "unit": "TOPS", "h2d_bytes_per_step": 3 * 4 * P_local * N * d,
                "d2h_bytes_per_step": 4 * P_local * N * d, "ms_per_step": e_ms / k_e2e,
                "steps": k_e2e,
                "api": "QFlashHostPipeline (pinned host fp32 in/out, 2 buffer sets overlapping copies and compute)"}
     sampler.stop()
 
+    # ---- verification (outside the timed region): every rank's output of input set
+    # 0 is gathered with NCCL (sampled problems byte for byte + a checksum of the slab)
+    # and rank 0 compares it with its own 1-GPU run of the same rows
+    verify = None
+    if world > 1 and not per_head:
+        with torch.cuda.stream(stream):
+            run_step(0)
+        torch.cuda.synchronize()
+        y = pipes[0].out
+        samp = 2
+        loc = torch.zeros((samp, N, d), dtype=torch.float32, device=dev)
+        loc[:min(samp, P_local)] = y[:samp]
+        csum = y.view(torch.int32).to(torch.int64).sum().reshape(1)
+        g_s = [torch.empty_like(loc) for _ in range(world)]
+        g_c = [torch.empty_like(csum) for _ in range(world)]
+        dist.all_gather(g_s, loc)
+        dist.all_gather(g_c, csum)
+        ok = True
+        if rank == 0:
+            ref_q = [torch.from_numpy(a).to(dev) for a in
+                     gen_real_qkv_slab(P_total, N, d, 0, P_total, seed=0, family=w.family)]
+            for r in range(world):
+                b_r, c_r = qfl.qflash_partition(P_total, world, r)
+                if strong:  # the whole batch on this GPU, kernel-computed amax
+                    if r == 0:
+                        full = qfl.qflash_forward_fused(*ref_q, args.block_kv, args.variant)
+                    ref = full[b_r:b_r + c_r]
+                else:       # the slab alone on this GPU (its own per-tensor scales)
+                    ref = qfl.QFlashPipeline(c_r, N, d, block_kv=args.block_kv, device=dev, mode=args.mode,
+                                             variant=args.variant)(*[t[b_r:b_r + c_r].contiguous()
+                                                                     for t in ref_q])
+                ok = ok and torch.equal(ref[:samp].view(torch.int32), g_s[r][:min(samp, c_r)].view(torch.int32))
+                ok = ok and int(ref.view(torch.int32).to(torch.int64).sum()) == int(g_c[r].item())
+        verify = {"ok": bool(ok), "method": "NCCL all_gather of each rank's first %d problems + int64 "
+                  "checksum of its fp32 output, compared on rank 0 with a 1-GPU run of the same rows "
+                  "(%s)" % (samp, "whole batch" if strong else "each slab")}
+        if rank == 0 and not ok:
+            print("bench.py: multi-GPU verification FAILED", file=sys.stderr)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(name, batch, w, args.block_kv)
 
     if rank == 0:
+        step_desc = ("qflash_amax_qkv + NCCL all_reduce(MAX, 3 floats) + qflash_forward_fused_amax"
+                     if strong else
+                     "qflash_forward_fused (CUDA graph, 1 cooperative launch)" if launches_per_step == 1
+                     else "per-head quantize + derive + attention + dequantize (CUDA graph)"
+                     if per_head else "quantize_qkv_prepare + attention_dequant_prepared (CUDA graph)")
         line = {
             "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "us_per_call": ms_per_step * 1e3, "higher_is_better": True,
-            "scaling": args.scaling, "vs_baseline": None, "dtype": "s8/s32",
-            "data": "synthetic (SURVEY 8(d) recipe: channel-mean Gaussians, seed = rank)",
+            "scaling": "strong" if args.scaling == "strong" else "weak", "vs_baseline": None,
+            "dtype": "s8/s32",
+            "data": "synthetic (SURVEY 8(d) recipe: channel-mean Gaussians, chunk-seeded global batch)",
             "config": {"workload": f"{name} b{batch} ({w.source})", "problems": P_total,
                        "problems_per_rank": P_local, "seq_len": N, "head_dim": d,
-                       "block_kv": args.block_kv, "parallelism": f"independent problems x{world}",
-                       "step": ("qflash_forward_fused (CUDA graph, 1 cooperative launch)" if launches_per_step == 1
-                                else "per-head quantize + derive + attention + dequantize (CUDA graph)"
-                                if args.scales == "per-head"
-                                else "quantize_qkv_prepare + attention_dequant_prepared (CUDA graph)"),
-                       "scales": args.scales,
+                       "block_kv": args.block_kv,
+                       "parallelism": (f"{world} ranks x contiguous problem slabs (qflash_partition)"
+                                       + (", global scales via all_reduce" if strong else
+                                          ", per-slab scales, no collective" if world > 1 else "")),
+                       "step": step_desc, "scales": args.scales,
                        "l2": f"rotating {n_sets} input sets ({n_sets * set_bytes / 2**20:.0f} MiB > 2x L2)"},
+            "rank_ms_per_step": rank_ms,
             "gpu_launches": launches_per_step * args.steps,
-            "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clocks, "roofline": roofline, "stages": extra, "cpu_baseline": cpu, "e2e": e2e,
+            "verify": verify,
         }
         print(json.dumps(line))
     if world > 1:

@@ -55,21 +55,6 @@ cudaError_t launch_attention_ph_d(int BC, int nseg, const CUtensorMap& tq, const
   return cudaErrorNotSupported;
 }
 
-// Resident fused step (FQ = 2): generic tiles, cfg 0 (one query tile in flight,
-// CS = 4) or cfg 1 (two groups, CS = 2), T_c <= kStages.
-template <int D>
-cudaError_t launch_resident_d(int BC, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
-                              const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
-                              cudaStream_t stream) {
-#define QF_RS(bc)                                                                          \
-  if (BC == bc)                                                                            \
-    return cfg == 1 ? try_launch<D, bc, 1, 2, 2, false, 2>(tq, tk, tv, args, tiles, sms, stream) \
-                    : try_launch<D, bc, 1, 4, 1, false, 2>(tq, tk, tv, args, tiles, sms, stream);
-  QF_RS(64) QF_RS(128) QF_RS(256)
-#undef QF_RS
-  return cudaErrorNotSupported;
-}
-
 template <int D>
 constexpr bool supported_d(int BC, int nseg, int cfg) {
 #define QF_FITS(bc, ns)                                                                 \

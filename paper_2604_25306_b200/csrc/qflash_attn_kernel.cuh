@@ -365,13 +365,6 @@ struct TileIter {
   }
   __device__ void init(const AttnArgs& a, uint32_t t) {
     i = 0;
-    if (a.resident) {  // resident fused step: CTA b = problem b, group g = query tiles g, g + QT, ...
-      problem = static_cast<int>(blockIdx.x);
-      off = (static_cast<int>(t) - static_cast<int>(blockIdx.x)) >= static_cast<int>(gridDim.x) ? kBlockR : 0;
-      if (off >= a.N) problem = a.P;
-      else fill(a);
-      return;
-    }
     if constexpr (NSEG == 1) {
       problem = a.Tr == 1 ? static_cast<int>(t) : static_cast<int>(__umulhi(t, a.tr_magic));
       off = (static_cast<int>(t) - problem * a.Tr) * kBlockR;
@@ -385,12 +378,6 @@ struct TileIter {
   __device__ bool valid(const AttnArgs& a) const { return problem < a.P; }
   __device__ void next(const AttnArgs& a) {
     ++i;
-    if (a.resident) {
-      off += a.g_mod;  // QT * 128
-      if (off >= a.N) problem = a.P;
-      else fill(a);
-      return;
-    }
     problem += a.g_div;
     off += a.g_mod;
     const int lim = NSEG == 1 ? a.Tr * kBlockR : a.N;
@@ -1111,30 +1098,9 @@ __device__ __forceinline__ float amax4(float m, const float4& v) {
   return fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
 }
 
-// Resident fused step (FQ = 2): where every codes tile lands in shared memory.
-struct RsLayout {
-  uint8_t* smem;   // 1024-aligned base
-  int group_smem;  // bytes per group
-  int q_off, k_off, v_off;
-  int q_bytes, kv_bytes;
-  int qt;          // groups (QT)
-  int bc;          // B_c (power of two)
-};
-// Byte offset of (row r, byte c) inside a TMA-loaded K-major tile with D-byte rows and
-// the UMMA swizzle of swizzle_layout<D>() (SW32 / SW64 / SW128 = Swizzle<1|2|3, 4, 3>:
-// address bits [4, 4 + b) ^= bits [7, 7 + b)), i.e. exactly where the TMA would put it.
 template <int D>
-QF_DEV uint32_t swz_off(int r, int c) {
-  const uint32_t x = static_cast<uint32_t>(r * D + c);
-  if constexpr (D == 32) return x ^ (((x >> 7) & 1u) << 4);
-  else if constexpr (D == 64) return x ^ (((x >> 7) & 3u) << 4);
-  else return x ^ (((x >> 7) & 7u) << 4);
-}
-
-template <int D, bool RS = false>
 __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float* scratch,
-                                                       IntParams* sprm, uint32_t* dq_table,
-                                                       const RsLayout* rs = nullptr) {
+                                                       IntParams* sprm, uint32_t* dq_table) {
 
   constexpr int kVR = QF_KVR;  // register-resident 16-B vectors per tensor and thread
   QF_FQ_TS(a, 0);
@@ -1150,40 +1116,14 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   // external amax (a.amax_in: e.g. MAX-all-reduced over the ranks that shard one
   // logical tensor): no amax pass, no barrier 1
   const bool ext = a.amax_in != nullptr;
-  const bool resident = !RS && !ext && nvec <= kVR * nthr;  // the whole share stays in registers
+  const bool resident = !ext && nvec <= kVR * nthr;  // the whole share stays in registers
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float m[3] = {0.f, 0.f, 0.f};
   float4 reg[3][kVR];
-  // RS: this CTA's problem (b = blockIdx.x) only -- Q, K, V concatenated as 3 nvp
-  // float4 vectors, vector i of the data thread at tid_d + u * ndata_blk
-  const int64_t nvp = RS ? (static_cast<int64_t>(a.N) * D) >> 2 : 0;
-  const int64_t pbase = RS ? static_cast<int64_t>(blockIdx.x) * nvp : 0;
-  const int tid_d = static_cast<int>(threadIdx.x) - 32;
-  float4 rr[RS ? kRsVR : 1];
-  if constexpr (RS) {
-#pragma unroll
-    for (int u = 0; u < kRsVR; ++u) {
-      const int64_t i = tid_d + static_cast<int64_t>(u) * ndata_blk;
-      const int t = (i >= nvp ? 1 : 0) + (i >= 2 * nvp ? 1 : 0);
-      const float4* src = reinterpret_cast<const float4*>(t == 0 ? a.xin[0] : t == 1 ? a.xin[1] : a.xin[2]);
-      rr[u] = (data_thread && i < 3 * nvp) ? __ldg(src + pbase + (i - t * nvp)) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int u = 0; u < kRsVR; ++u) {
-      const int64_t i = tid_d + static_cast<int64_t>(u) * ndata_blk;
-      const int t = (i >= nvp ? 1 : 0) + (i >= 2 * nvp ? 1 : 0);
-      const float mx = amax4(0.f, rr[u]);
-      m[0] = t == 0 ? fmaxf(m[0], mx) : m[0];
-      m[1] = t == 1 ? fmaxf(m[1], mx) : m[1];
-      m[2] = t == 2 ? fmaxf(m[2], mx) : m[2];
-    }
-  }
   if (ext) {
     if (threadIdx.x < 3) scratch[96 + threadIdx.x] = __ldcg(a.amax_in + threadIdx.x);
   } else {
-  if (RS) {
-    // (loaded above)
-  } else if (resident) {
+  if (resident) {
     // every load of all three tensors in flight before the first reduction
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
@@ -1286,40 +1226,7 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   float r3[3];
 #pragma unroll
   for (int t = 0; t < 3; ++t) r3[t] = __frcp_rn(s3[t]);
-  if constexpr (RS) {
-    // codes -> the shared-memory tiles the MMAs read (TMA layout and swizzle), and
-    // the global code buffers (outputs); no second grid barrier: this CTA's
-    // attention reads only its own problem
-    constexpr int kV4 = D / 4;  // float4 per row
-#pragma unroll
-    for (int u = 0; u < kRsVR; ++u) {
-      const int64_t i = tid_d + static_cast<int64_t>(u) * ndata_blk;
-      if (data_thread && i < 3 * nvp) {
-        const int t = (i >= nvp ? 1 : 0) + (i >= 2 * nvp ? 1 : 0);
-        const int j = static_cast<int>(i - t * nvp);
-        const uint32_t w = quant4(rr[u], t == 0 ? s3[0] : t == 1 ? s3[1] : s3[2],
-                                  t == 0 ? r3[0] : t == 1 ? r3[1] : r3[2]);
-        reinterpret_cast<uint32_t*>(t == 0 ? a.xq[0] : t == 1 ? a.xq[1] : a.xq[2])[pbase + j] = w;
-        const int r = j / kV4;
-        const int c = (j - r * kV4) * 4;
-        if (t == 0) {
-          const int qt = r >> 7;
-          uint8_t* dst = rs->smem + (rs->qt == 2 ? qt * rs->group_smem : qt * rs->q_bytes) + rs->q_off;
-          *reinterpret_cast<uint32_t*>(dst + swz_off<D>(r & (kBlockR - 1), c)) = w;
-        } else {
-          const int jt = r / rs->bc;
-          const uint32_t o = swz_off<D>(r - jt * rs->bc, c);
-          for (int g = 0; g < rs->qt; ++g)
-            *reinterpret_cast<uint32_t*>(rs->smem + g * rs->group_smem + (t == 1 ? rs->k_off : rs->v_off) +
-                                         jt * rs->kv_bytes + o) = w;
-        }
-      }
-    }
-    fence_proxy_async_smem();  // generic-proxy smem writes -> tcgen05.mma operands
-    QF_FQ_TS(a, 4);
-    QF_FQ_TS(a, 5);
-    return;
-  } else if (resident) {
+  if (resident) {
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
       uint32_t* dst = reinterpret_cast<uint32_t*>(a.xq[t]);
@@ -1432,11 +1339,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
   // dependent launch); every global access of this grid comes after the wait.
   griddep_wait();
   IntParams* sprm = reinterpret_cast<IntParams*>(smem + C::kPrm);
-  if constexpr (FQ == 2) {
-    const RsLayout rs{smem, C::kGroupSmem, C::kQ, C::kK, C::kV, C::kQBytes, C::kKVBytes, QT, BC};
-    fused_quantize_prologue<D, true>(args, reinterpret_cast<float*>(smem + C::kScratch), sprm, recip + 1024, &rs);
-    __syncthreads();
-  } else if constexpr (FQ) {
+  if constexpr (FQ) {
     fused_quantize_prologue<D>(args, reinterpret_cast<float*>(smem + C::kScratch), sprm, recip + 1024);
     __syncthreads();
   }
@@ -1476,27 +1379,18 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
           if (!(ok = status_ok())) break;
           mbar_wait_sleep(gb.q_empty(qb), ((ti.i >> 1) - 1) & 1, QF_SLEEP_PROD);
         }
-        if constexpr (FQ == 2) {
-          mbar_arrive(gb.q_full(qb));  // resident: the prologue wrote the codes tile
-        } else {
         mbar_arrive_expect_tx(gb.q_full(qb), ti.nseg * C::kQBytes);
         // segment s: rows of problem + s land at their tile rows, every other
         // tile row is out of range (row < 0 or >= N) and zero-filled
         for (int s = 0; s < ti.nseg; ++s)
           tma_load_3d(sQ + (qb * NSEG + s) * C::kQBytes, &tm_q, gb.q_full(qb), 0,
                       ti.off - s * args.N, ti.problem + s);
-        }
         if (!checked) ++nq;
         for (int j = 0; j < Tc; ++j, ++it) {
           const int st = it % kStages;
           if (it >= kStages) {
             if (!(ok = status_ok())) break;
             mbar_wait_sleep(gb.kv_empty(st), ((it / kStages) - 1) & 1, QF_SLEEP_PROD);
-          }
-          if constexpr (FQ == 2) {
-            mbar_arrive(gb.kv_full(st));  // resident: K, V codes stay in the ring (T_c <= kStages)
-            if (!checked) ++nkv;
-            continue;
           }
           mbar_arrive_expect_tx(gb.kv_full(st), ti.nseg * 2 * C::kKVBytes);
           for (int s = 0; s < ti.nseg; ++s) {
@@ -1692,13 +1586,9 @@ cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CU
     if (dev >= 0 && dev < 16) configured[dev] = 1;
   }
   const int64_t need = (tiles + QT - 1) / QT;
-  const int64_t G = FQ == 2 ? args.P : (need < sms ? need : sms);  // resident: CTA = problem
+  const int64_t G = need < sms ? need : sms;
   const int64_t stride = QT * G;  // tiles between consecutive visits of one group
-  if (FQ == 2) {
-    args.resident = 1;
-    args.g_div = 0;
-    args.g_mod = QT * kBlockR;
-  } else if (NSEG == 1) {
+  if (NSEG == 1) {
     const int64_t Tr = args.Tr;
     args.tr_magic = Tr > 1 ? static_cast<uint32_t>(((1ull << 32) + Tr - 1) / Tr) : 0u;
     args.g_div = static_cast<int32_t>(stride / Tr);

@@ -34,7 +34,6 @@ constexpr int kWsPartialOffset = 256;
 constexpr int kWsDqTableOffset = 4096;
 constexpr int kWsMaxPartialCtas = (kWsDqTableOffset - kWsPartialOffset) / 12;  // = 320
 static_assert(kWsMaxPartialCtas == 320, "partials must end before the dequant table");
-constexpr int kRsVR = 16;  // resident fused step: register-resident 16-B vectors per data thread
 constexpr int kHeadPrmStride = 80;   // bytes per head in the per-head constant table
 constexpr int kHeadPrmOffset = 128;  // table offset in the per-head workspace
 constexpr int kMaxHeads = 96;        // 128 + 96 * 80 <= QFLASH_DSCALE_WORKSPACE_BYTES
@@ -70,7 +69,7 @@ struct AttnArgs {
                               // caller (sharded quantization), or nullptr (computed here)
   int32_t cluster_grid;       // fused step: 1 = the grid is one thread-block cluster
                               // (barrier.cluster replaces the grid barriers)
-  int32_t resident;           // resident fused step: CTA b = problem b, codes in smem
+  int32_t pad2;
   // bring-up dumps for CTA 0's first tile only; nullptr in production:
   int32_t* dbg_s;  // [128][BC] raw S of KV tile 0
   int32_t* dbg_p;  // [128][BC/4] packed P words of KV tile 0

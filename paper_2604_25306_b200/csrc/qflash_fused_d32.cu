@@ -8,9 +8,4 @@ cudaError_t launch_fused_d32(int BC, int nseg, int cfg, const CUtensorMap& tq,
                              int64_t tiles, int sms, cudaStream_t stream) {
   return launch_attention_d<32, false, 1>(BC, nseg, cfg, tq, tk, tv, args, tiles, sms, stream);
 }
-cudaError_t launch_resident_d32(int BC, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
-                                const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
-                                cudaStream_t stream) {
-  return launch_resident_d<32>(BC, cfg, tq, tk, tv, args, tiles, sms, stream);
-}
 }  // namespace qf

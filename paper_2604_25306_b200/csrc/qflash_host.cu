@@ -38,22 +38,6 @@ cudaError_t launch_fused_d64(int BC, int nseg, int cfg, const CUtensorMap& tq, c
 cudaError_t launch_fused_d128(int BC, int nseg, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
                               const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
                               cudaStream_t stream);
-#define QF_DECL_RS(D)                                                                      \
-  cudaError_t launch_resident_d##D(int BC, int cfg, const CUtensorMap& tq, const CUtensorMap& tk, \
-                                   const CUtensorMap& tv, const AttnArgs& args, int64_t tiles,   \
-                                   int sms, cudaStream_t stream);
-QF_DECL_RS(32)
-QF_DECL_RS(64)
-QF_DECL_RS(128)
-#undef QF_DECL_RS
-inline cudaError_t launch_resident(int D, int BC, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
-                                   const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
-                                   cudaStream_t stream) {
-  if (D == 32) return launch_resident_d32(BC, cfg, tq, tk, tv, args, tiles, sms, stream);
-  if (D == 64) return launch_resident_d64(BC, cfg, tq, tk, tv, args, tiles, sms, stream);
-  if (D == 128) return launch_resident_d128(BC, cfg, tq, tk, tv, args, tiles, sms, stream);
-  return cudaErrorNotSupported;
-}
 cudaError_t launch_attention_ph(int D, int BC, int nseg, const CUtensorMap& tq,
                                 const CUtensorMap& tk, const CUtensorMap& tv,
                                 const AttnArgs& args, int64_t tiles, int sms,
@@ -305,27 +289,6 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
       break;
     default: return fail(QFLASH_ERR_INVALID_ARGUMENT, "unknown variant %d", static_cast<int>(variant));
   }
-  // Resident fused step: at most one problem per SM, T_r, T_c <= 2 and
-  // the problem's fp32 Q, K, V fit the data threads' registers -> CTA b quantizes
-  // problem b straight into its shared-memory tiles (one grid barrier, no TMA).
-  bool resident = false;
-  int rs_cfg = 0;
-  {
-    static int rs_env = -1;
-    if (rs_env < 0) {
-      const char* e = getenv("QFLASH_RESIDENT");
-      rs_env = (e != nullptr && e[0] == '0') ? 0 : 1;
-    }
-    const int64_t Tc_rs = (N + bc_eff - 1) / bc_eff;
-    if (rs_env && fin != nullptr && heads == 0 && dbg_s == nullptr && dbg_p == nullptr && dbg_o == nullptr &&
-        dbg_t == nullptr && variant != QFLASH_VARIANT_PACKED && P <= sms && Tr <= 2 && Tc_rs <= 2 &&
-        3ll * N * d / 4 <= static_cast<int64_t>(qf::kRsVR) * (640 - 32)) {
-      rs_cfg = Tr == 2 ? 1 : 0;
-      resident = qf::attention_supported(d, bc_eff, 1, rs_cfg);
-      if (forced_config() >= 0) resident = resident && forced_config() == rs_cfg;
-    }
-  }
-  if (resident) packed = false;
   const int nseg = packed ? nseg_tpl : 1;
   const int64_t tiles = packed ? tiles_packed : tiles_generic;
   // Kernel configuration (qflash_attn_inst.cuh): with more than one wave of
@@ -344,10 +307,9 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
       if (cfg == 0 && qf::attention_supported(d, bc_eff, nseg, c)) cfg = c;
   }
   if (cfg_env >= 0 && heads == 0 && qf::attention_supported(d, bc_eff, nseg, cfg_env)) cfg = cfg_env;
-  if (resident) cfg = rs_cfg;
   if (!qf::attention_supported(d, bc_eff, nseg, cfg))
     return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "no kernel configuration for d=%d block=%d", d, bc_eff);
-  g_last_config = cfg | (nseg << 4) | (resident ? 256 : 0);
+  g_last_config = cfg | (nseg << 4);
   CUtensorMap tq, tk, tv;
   qflash_status st;
   if ((st = make_tmap(&tq, q, P, N, d, 128, 1)) != QFLASH_OK) return st;
@@ -393,8 +355,6 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
     args.H = heads;
     args.h_magic = static_cast<uint32_t>(((1ull << 32) + heads - 1) / heads);
     e = qf::launch_attention_ph(d, bc_eff, nseg, tq, tk, tv, args, tiles, sms, stream);
-  } else if (resident) {
-    e = qf::launch_resident(d, bc_eff, cfg, tq, tk, tv, args, tiles, sms, stream);
   } else {
     e = qf::launch_attention(d, bc_eff, nseg, cfg, tq, tk, tv, args, tiles, sms, dbg,
                              fin != nullptr, stream);

@@ -124,3 +124,25 @@ def gen_int8_qkv(P: int, N: int, d: int, seed: int = 0, kind: str = "uniform"):
 # Scales paired with the int8 adversarial sets: the regime of real workloads
 # (s_q = s_k ~ amax/127 for |x| up to ~7) unless a test overrides them.
 DEFAULT_INT8_SCALES = (0.055, 0.055, 0.03)
+
+
+# ------------------------------------------------ problem-addressable global batches
+SLAB_CHUNK = 16  # problems per independently seeded chunk
+
+
+def gen_real_qkv_slab(P_total: int, N: int, d: int, begin: int, count: int, seed: int = 0,
+                      family: str = "vit"):
+    """Problems [begin, begin + count) of a global [P_total, N, d] batch defined chunk by
+    chunk: chunk c (problems [16 c, 16 c + 16)) is gen_real_qkv(..., seed=[seed, c]).  Any
+    rank can generate its own slab (multi-GPU bench), and the concatenation over a
+    partition equals the slab of the whole batch."""
+    assert 0 <= begin and begin + count <= P_total
+    out = [np.empty((count, N, d), np.float32) for _ in range(3)]
+    c0, c1 = begin // SLAB_CHUNK, (begin + count + SLAB_CHUNK - 1) // SLAB_CHUNK
+    for c in range(c0, c1):
+        lo, hi = c * SLAB_CHUNK, min(P_total, (c + 1) * SLAB_CHUNK)
+        chunk = gen_real_qkv(hi - lo, N, d, seed=[seed, c], family=family)
+        a, b = max(lo, begin), min(hi, begin + count)
+        for t in range(3):
+            out[t][a - begin:b - begin] = chunk[t][a - lo:b - lo]
+    return tuple(out)
