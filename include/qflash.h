@@ -218,6 +218,34 @@ QFLASH_API qflash_status qflash_forward_fused_amax(const float* q, const float* 
                                                    float* scales_dev, void* workspace_dev,
                                                    const float* amax_dev, qflash_stream_t stream);
 
+/* qflash_forward_fused on the packed output of a QKV projection (
+ * dynamic quantization of the projection output P:L703, Eq. 2): qkv is
+ * ONE device fp32 tensor [P / heads, N, 3, heads, d] (batch x windows, tokens, {Q, K, V},
+ * heads, channels -- a Linear(d_model, 3 d_model) output viewed per head), problem p =
+ * b heads + h.  The prologue reads it with the (token, head) transpose and writes the
+ * [P, N, d] codes q_q / k_q / v_q itself: no permute pass.  heads must divide P.  The
+ * result equals qflash_forward_fused on the three permuted tensors byte for byte.
+ * Other arguments and errors as qflash_forward_fused (qkv 16-byte aligned). */
+QFLASH_API qflash_status qflash_forward_fused_qkv(const float* qkv, int32_t heads,
+                                                  const qflash_attn_shape* shape, qflash_variant variant,
+                                                  int8_t* q_q, int8_t* k_q, int8_t* v_q, int8_t* o,
+                                                  float* y, float* scales_dev, void* workspace_dev,
+                                                  qflash_stream_t stream);
+
+/* Scale Accumulation ablation (Eq. 13, App. B.1
+ * P:L762-805) -- the alternative the paper REJECTS, for the fig:tile_sqnr
+ * experiment only.  Algorithm 1 with step (8)(10) replaced by
+ *   O <- O alpha + (P V_j) s_inv,   l <- l alpha + rowsum(P_j) s_inv
+ * (floor(PV / s_alpha) with the integer inverse scale, reading R24) in int64, then
+ * O^ = sat8(floor(O / l)) (0 when l <= 0).  Values that leave int64 wrap modulo 2^64
+ * exactly like the CPU oracle's mode 1.  *flags_dev (device int32, written): bit 0 =
+ * some accumulator left int64, bit 1 = some accumulator left int32 (where an
+ * int32-accumulator kernel overflows).  Generic tiles, head_dim 32/64, block_kv
+ * 64/128; other arguments and errors as qflash_attention_int8 (s_O = s_V). */
+QFLASH_API qflash_status qflash_attention_int8_accum(const int8_t* q, const int8_t* k, const int8_t* v,
+                                                     float s_q, float s_k, const qflash_attn_shape* shape,
+                                                     int8_t* o, int32_t* flags_dev, qflash_stream_t stream);
+
 /* --------------------------------------------------------------------------
  * Per-head granularity (the paper's per-tensor scales are the
  * H = 1 case).  Problems are the flattened (batch,

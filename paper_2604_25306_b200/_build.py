@@ -11,7 +11,7 @@ BUILD = os.path.join(PKG, "_objs")
 LIB = os.path.join(PKG, "libqflash.so")
 SOURCES = ["qflash_attn_d32.cu", "qflash_attn_d64.cu", "qflash_attn_d128.cu", "qflash_attn_dbg.cu",
            "qflash_fused_d32.cu", "qflash_fused_d64.cu", "qflash_fused_d128.cu", "qflash_attn_ph.cu",
-           "qflash_quant.cu", "qflash_host.cu"]
+           "qflash_attn_acc.cu", "qflash_quant.cu", "qflash_host.cu"]
 HEADERS = ["ptx.cuh", "qflash_common.cuh", "qflash_params.cuh", "qflash_attn_kernel.cuh", "qflash_quant_elem.cuh",
            "qflash_attn_inst.cuh"]
 PUBLIC_HEADERS = ["qflash.h", "qflash_debug.h"]

@@ -34,7 +34,8 @@ EXPORTED = [
     "qflash_quantize_qkv_prepare", "qflash_attention_int8_prepared",
     "qflash_attention_dequant_prepared", "qflash_forward_fused",
     "qflash_quantize_per_head", "qflash_attention_int8_per_head", "qflash_dequantize_per_head",
-    "qflash_amax_qkv", "qflash_forward_fused_amax",
+    "qflash_amax_qkv", "qflash_forward_fused_amax", "qflash_attention_int8_accum",
+    "qflash_forward_fused_qkv",
 ]
 
 
@@ -96,6 +97,11 @@ def lib():
     L.qflash_forward_fused_amax.restype = st
     L.qflash_forward_fused_amax.argtypes = [vp, vp, vp, ctypes.POINTER(AttnShape), st, vp, vp, vp, vp,
                                             vp, vp, vp, vp, vp]
+    L.qflash_forward_fused_qkv.restype = st
+    L.qflash_forward_fused_qkv.argtypes = [vp, i32, ctypes.POINTER(AttnShape), st, vp, vp, vp, vp, vp, vp,
+                                           vp, vp]
+    L.qflash_attention_int8_accum.restype = st
+    L.qflash_attention_int8_accum.argtypes = [vp, vp, vp, f32, f32, ctypes.POINTER(AttnShape), vp, vp, vp]
     L.qflash_amax_qkv.restype = st
     L.qflash_amax_qkv.argtypes = [vp, vp, vp, i64, vp, vp]
     L.qflash_quantize_per_head.restype = st

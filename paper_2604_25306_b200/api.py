@@ -222,6 +222,22 @@ def qflash_attention_dequant_prepared(q: torch.Tensor, k: torch.Tensor, v: torch
     return out
 
 
+def qflash_attention_int8_accum(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, s_q: float,
+                                s_k: float, block_kv: int = 128, out: torch.Tensor | None = None,
+                                stream=None):
+    """Scale Accumulation ablation (Eq. 13, App. B.1 -- the paper's rejected form):
+    returns (int8 O^, flags) with flags bit 0 = int64 overflow, bit 1 = int32 overflow."""
+    _check_qkv(q, k, v)
+    out = torch.empty_like(q) if out is None else out
+    _check_like(q, out, "out", torch.int8)
+    flags = torch.zeros(1, dtype=torch.int32, device=q.device)
+    shape = _shape(q, block_kv)
+    check(lib().qflash_attention_int8_accum(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v), float(s_q),
+                                            float(s_k), ctypes.byref(shape), _dev_ptr(out),
+                                            _dev_ptr(flags), _stream(stream)))
+    return out, flags
+
+
 def qflash_amax_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
                     out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Device float[3]: max |x| of fp32 Q, K, V (this device's slab)."""
@@ -265,6 +281,40 @@ def qflash_forward_fused(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, bloc
         _dev_ptr(codes[0]), _dev_ptr(codes[1]), _dev_ptr(codes[2]),
         _dev_ptr(out_int8) if out_int8 is not None else None, _dev_ptr(out), _dev_ptr(scales),
         _dev_ptr(workspace), _dev_ptr(amax) if amax is not None else None, _stream(stream)))
+    return out
+
+
+def qflash_forward_fused_qkv(qkv: torch.Tensor, heads: int, block_kv: int = 128, variant: str = "auto",
+                             out: torch.Tensor | None = None, codes=None,
+                             scales: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+                             stream=None):
+    """The fused step on a packed QKV projection output qkv [B, N, 3, heads, d] fp32
+    (B = batch x windows): problems p = b * heads + h; returns y [B * heads, N, d]."""
+    if qkv.dtype != torch.float32 or qkv.dim() != 5 or qkv.shape[2] != 3 or qkv.shape[3] != heads:
+        raise ValueError("qkv must be fp32 [B, N, 3, heads, d]")
+    if not qkv.is_cuda or not qkv.is_contiguous():
+        raise ValueError("qkv must be a contiguous CUDA tensor")
+    B, N, _, H, d = qkv.shape
+    dev = qkv.device
+    shp = (B * H, N, d)
+    out = torch.empty(shp, dtype=torch.float32, device=dev) if out is None else out
+    if codes is None:
+        codes = [torch.empty(shp, dtype=torch.int8, device=dev) for _ in range(3)]
+    scales = torch.empty(3, dtype=torch.float32, device=dev) if scales is None else scales
+    if workspace is None:
+        workspace = torch.zeros(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=dev)
+    if tuple(out.shape) != shp or out.dtype != torch.float32 or out.device != dev:
+        raise ValueError("out must be fp32 %s" % (shp,))
+    for i, t in enumerate(codes):
+        if tuple(t.shape) != shp or t.dtype != torch.int8 or t.device != dev:
+            raise ValueError("codes[%d] must be int8 %s" % (i, shp))
+    _check_scales(scales, 3, dev)
+    _check_workspace(workspace, dev)
+    shape = AttnShape(B * H, N, d, block_kv)
+    check(lib().qflash_forward_fused_qkv(
+        _dev_ptr(qkv), H, ctypes.byref(shape), _lib.VARIANTS[variant], _dev_ptr(codes[0]),
+        _dev_ptr(codes[1]), _dev_ptr(codes[2]), None, _dev_ptr(out), _dev_ptr(scales),
+        _dev_ptr(workspace), _stream(stream)))
     return out
 
 

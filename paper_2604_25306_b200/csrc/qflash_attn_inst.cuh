@@ -8,11 +8,11 @@
 
 namespace qf {
 
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ, bool PH = false>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ, bool PH = false, bool ACC = false>
 cudaError_t try_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const AttnArgs& args, int64_t tiles, int sms, cudaStream_t stream) {
   if constexpr (config_fits<D, BC, NSEG, CS, QT>()) {
-    return launch_attn_t<D, BC, NSEG, CS, QT, DBG, FQ, PH>(tq, tk, tv, args, tiles, sms, stream);
+    return launch_attn_t<D, BC, NSEG, CS, QT, DBG, FQ, PH, ACC>(tq, tk, tv, args, tiles, sms, stream);
   } else {
     return cudaErrorNotSupported;
   }
@@ -52,6 +52,16 @@ cudaError_t launch_attention_ph_d(int BC, int nseg, const CUtensorMap& tq, const
   QF_PH(64, 2) QF_PH(128, 2) QF_PH(256, 2)
   QF_PH(64, 4) QF_PH(128, 4)
 #undef QF_PH
+  return cudaErrorNotSupported;
+}
+
+// Scale Accumulation ablation (Eq. 13, App. B.1): generic tiles, configuration 0.
+template <int D>
+cudaError_t launch_attention_acc_d(int BC, const CUtensorMap& tq, const CUtensorMap& tk,
+                                   const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
+                                   cudaStream_t stream) {
+  if (BC == 64) return try_launch<D, 64, 1, 4, 1, false, 0, false, true>(tq, tk, tv, args, tiles, sms, stream);
+  if (BC == 128) return try_launch<D, 128, 1, 4, 1, false, 0, false, true>(tq, tk, tv, args, tiles, sms, stream);
   return cudaErrorNotSupported;
 }
 

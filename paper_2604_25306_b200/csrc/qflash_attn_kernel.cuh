@@ -70,7 +70,10 @@ constexpr RecipTable make_recip_table() {
 }
 static __device__ const RecipTable g_recip = make_recip_table();
 
-constexpr int kStages = 2;
+constexpr int kMaxStages = 3;  // K/V ring stages reserved in the barrier layout
+#ifndef QF_KV_STAGES_C1
+#define QF_KV_STAGES_C1 2  // K/V ring depth of configuration 1 (3 measured: no gain, r2_experiments.md)
+#endif
 constexpr int kBlockR = 128;
 
 // Sleep (ns) between barrier probes of the waits off the critical path
@@ -125,12 +128,15 @@ struct Cfg {
   // shared memory (offsets from the 1024-aligned base)
   static constexpr int kQBytes = kBlockR * D;
   static constexpr int kKVBytes = BC * D;
-  static constexpr int kGroupSmem = 2 * NSEG * kQBytes + 2 * kStages * NSEG * kKVBytes;
+  // K/V ring depth: 3 for configuration 1 with generic tiles (the load of K/V tile j + 2
+  // starts once P V_{j-1} has released its stage, a round earlier than with 2), else 2
+  static constexpr int kSt = (QT == 2 && CS == 2 && NSEG == 1) ? QF_KV_STAGES_C1 : 2;
+  static constexpr int kGroupSmem = 2 * NSEG * kQBytes + 2 * kSt * NSEG * kKVBytes;
   static constexpr int kQ = 0;                               // [2][NSEG] (+ g kGroupSmem)
-  static constexpr int kK = 2 * NSEG * kQBytes;              // [kStages][NSEG]
-  static constexpr int kV = kK + kStages * NSEG * kKVBytes;  // [kStages][NSEG]
+  static constexpr int kK = 2 * NSEG * kQBytes;              // [kSt][NSEG]
+  static constexpr int kV = kK + kSt * NSEG * kKVBytes;      // [kSt][NSEG]
   static constexpr int kOnes = QT * kGroupSmem;              // second MN atom of [V | 1]
-  static constexpr int kBarsPerGroup = 2 * kStages + 4 + kNumS + 7;
+  static constexpr int kBarsPerGroup = 2 * kMaxStages + 4 + kNumS + 7;
   static constexpr int kBar = kOnes + BC * D;
   static constexpr int kTmemSlot = kBar + QT * kBarsPerGroup * 8;
   static constexpr int kRed = (kTmemSlot + 16 + 15) / 16 * 16;  // [QT][2][CS][128] int32
@@ -151,29 +157,30 @@ constexpr bool config_fits() {
          (BC / CS == 16 || BC / CS == 32 || BC / CS == 64 || (CS == 1 && BC == 128)) &&
          ((D / CS) % 8 == 0) &&
          (NSEG * (BC / 4) <= BC) &&
-         (QT * (2 * NSEG * kBlockR * D + 2 * kStages * NSEG * BC * D) + BC * D + 64 * 11 +
+         (QT * (2 * NSEG * kBlockR * D + 2 * ((QT == 2 && CS == 2 && NSEG == 1) ? QF_KV_STAGES_C1 : 2) * NSEG * BC * D) +
+              BC * D + 8 * QT * (2 * kMaxStages + 4 + 2 + 7) +
               QT * 2 * CS * 512 + 5120 + 640 + 2048 <=
           227 * 1024);
 }
 
-// Group barriers (8 B each): kv_full[kStages], kv_empty[kStages], q_full[2],
+// Group barriers (8 B each): kv_full[kMaxStages], kv_empty[kMaxStages], q_full[2],
 // q_empty[2], s_full[kNumS], p_full, o_full.
 template <int NUMS>
 struct GroupBars {
   uint64_t* base;
   QF_DEV uint64_t* kv_full(int s) const { return base + s; }
-  QF_DEV uint64_t* kv_empty(int s) const { return base + kStages + s; }
-  QF_DEV uint64_t* q_full(int b) const { return base + 2 * kStages + b; }
-  QF_DEV uint64_t* q_empty(int b) const { return base + 2 * kStages + 2 + b; }
-  QF_DEV uint64_t* s_full(int b) const { return base + 2 * kStages + 4 + b; }
+  QF_DEV uint64_t* kv_empty(int s) const { return base + kMaxStages + s; }
+  QF_DEV uint64_t* q_full(int b) const { return base + 2 * kMaxStages + b; }
+  QF_DEV uint64_t* q_empty(int b) const { return base + 2 * kMaxStages + 2 + b; }
+  QF_DEV uint64_t* s_full(int b) const { return base + 2 * kMaxStages + 4 + b; }
   // p_full(1), alpha_full(b) and rel_full are used by the row-owner roles (CS = 1),
   // where the softmax warpgroup may run one KV tile ahead of its consumers: the
   // double-buffered barriers (index it & 1, parity (it >> 1) & 1) never overrun.
-  QF_DEV uint64_t* p_full(int b = 0) const { return base + 2 * kStages + 4 + NUMS + b; }
-  QF_DEV uint64_t* o_full() const { return base + 2 * kStages + 6 + NUMS; }
-  QF_DEV uint64_t* alpha_full(int b) const { return base + 2 * kStages + 7 + NUMS + b; }
-  QF_DEV uint64_t* rel_full() const { return base + 2 * kStages + 9 + NUMS; }
-  QF_DEV uint64_t* s_empty() const { return base + 2 * kStages + 10 + NUMS; }  // kSepP
+  QF_DEV uint64_t* p_full(int b = 0) const { return base + 2 * kMaxStages + 4 + NUMS + b; }
+  QF_DEV uint64_t* o_full() const { return base + 2 * kMaxStages + 6 + NUMS; }
+  QF_DEV uint64_t* alpha_full(int b) const { return base + 2 * kMaxStages + 7 + NUMS + b; }
+  QF_DEV uint64_t* rel_full() const { return base + 2 * kMaxStages + 9 + NUMS; }
+  QF_DEV uint64_t* s_empty() const { return base + 2 * kMaxStages + 10 + NUMS; }  // kSepP
 };
 
 
@@ -499,6 +506,33 @@ QF_DEV void p_pack(const uint32_t* sc, int hv, uint32_t mu, uint32_t nmu, uint32
   }
 }
 
+// ---- Scale Accumulation (Eq. 13; the rejected alternative of App. B.1)
+// X <- X alpha + Y s_inv in int64 with two's-complement wrap (the oracle's int64 cast of
+// the exact int128 value); flags bit 0: the exact value left int64, bit 1: it left int32
+// (an int32-accumulator kernel would have overflowed).
+QF_DEV int64_t acc_update(int64_t X, int32_t alpha, int32_t Y, int32_t s_inv, uint32_t& flags) {
+  const __int128 v = static_cast<__int128>(X) * alpha + static_cast<__int128>(Y) * s_inv;
+  if (v > static_cast<__int128>(INT64_MAX) || v < static_cast<__int128>(INT64_MIN)) flags |= 1u;
+  if (v > static_cast<__int128>(INT32_MAX) || v < static_cast<__int128>(INT32_MIN)) flags |= 2u;
+  return static_cast<int64_t>(static_cast<unsigned __int128>(v));
+}
+// floor(a / b) for b > 0, integer-only restoring division (no FP lowering of `/`).
+QF_DEV int64_t floor_div64(int64_t a, int64_t b) {
+  const bool neg = a < 0;
+  uint64_t un = neg ? static_cast<uint64_t>(-(a + 1)) : static_cast<uint64_t>(a);  // ~a for a < 0
+  const uint64_t d = static_cast<uint64_t>(b);
+  uint64_t q = 0, r = 0;
+#pragma unroll 1
+  for (int i = 63; i >= 0; --i) {
+    r = (r << 1) | ((un >> i) & 1u);
+    if (r >= d) {
+      r -= d;
+      q |= (1ull << i);
+    }
+  }
+  return neg ? static_cast<int64_t>(~q) : static_cast<int64_t>(q);  // floor(a/b) = ~floor(~a/b), a < 0
+}
+
 // Step (11) for one row's OW output columns [c OW, c OW + OW): O = floor(O / l)
 // saturated to int8 (R14), stored as int8 and/or dequantized fp32 (DQ row) at
 // flattened output row `orow` (row-packed tiles included).
@@ -550,7 +584,7 @@ QF_DEV void normalize_store(const AttnArgs& args, int64_t orow, int c, const uin
   }
 }
 
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FASTQ, bool PH = false>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FASTQ, bool PH = false, bool ACC = false>
 __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntParams& prm_k,
                                              uint32_t tmem_group, GroupBars<Cfg<D, BC, NSEG, CS, QT>::kNumS> gb,
                                              uint32_t red_group, const uint32_t* recip, int g,
@@ -596,6 +630,30 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
     const uint32_t s_inv = PH ? rct.s_inv : rck.s_inv;
     const int sinv_log2 = PH ? rct.sinv_log2 : rck.sinv_log2;
     const int32_t rel_lthr = PH ? rct.rel_lthr : rck.rel_lthr;
+    // ACC (Eq. 13): int64 accumulators of this thread's O columns and l, in registers;
+    // P V_j lands fresh in TMEM every KV tile and is folded in here
+    int64_t o64[ACC ? OW : 1];
+    int64_t l64 = 0;
+    int32_t alpha_prev = 0;
+    uint32_t acc_flags = 0;
+    if constexpr (ACC) {
+#pragma unroll
+      for (int e = 0; e < OW; ++e) o64[e] = 0;
+    }
+    auto acc_fold = [&](int32_t al) {  // O <- O alpha + PV s_inv, l <- l alpha + rowsum(P) s_inv
+      if constexpr (!ACC) return;
+      if (!warp_live) return;
+      uint32_t o[OW], lc;
+      tmem_ld_cols<OW>(tO + c * OW, o);
+      tmem_ld1(tO + D + c, lc);  // an unreleased copy of rowsum(P_j) from the ones block
+      tmem_wait_ld();
+      uint32_t f = 0;
+#pragma unroll
+      for (int e = 0; e < OW; ++e)
+        o64[e] = acc_update(o64[e], al, static_cast<int32_t>(o[e]), static_cast<int32_t>(s_inv), f);
+      l64 = acc_update(l64, al, static_cast<int32_t>(lc), static_cast<int32_t>(s_inv), f);
+      if (live) acc_flags |= f;  // padding rows of the last query tile do not count
+    };
 
     for (int j = 0; j < Tc; ++j) {
       const int it = it0 + j;
@@ -707,7 +765,14 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
       // the P computation; skipped for j = 0 (O = l = 0) and for warps whose rows
       // all kept their maximum (alpha = s_inv is the identity, R10).  P V_j is
       // issued only after every warp's p_full arrival below, i.e. after the release.
-      if (j > 0) {
+      if constexpr (ACC) {
+        if (j > 0) {  // fold step j-1 (its alpha, its P V) before P V_j overwrites TMEM
+          mbar_wait(gb.o_full(), (it - 1) & 1);
+          tc_fence_after();
+          acc_fold(alpha_prev);
+        }
+        alpha_prev = alpha;
+      } else if (j > 0) {
         if constexpr (!C::kSepP) {
           mbar_wait(gb.o_full(), (it - 1) & 1);
           tc_fence_after();
@@ -777,6 +842,31 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
     if (!tables_ready) {
       named_bar_sync(15, C::kNWG * 128 + 32);
       tables_ready = true;
+    }
+    if constexpr (ACC) {
+      acc_fold(alpha_prev);
+      if (warp_live && live) {
+        uint32_t w[OW / 4];
+#pragma unroll
+        for (int e = 0; e < OW; e += 4) {
+          int32_t v4[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            int64_t q = l64 > 0 ? floor_div64(o64[e + u], l64) : 0;  // oracle: l <= 0 -> 0
+            v4[u] = static_cast<int32_t>(q > 127 ? 127 : (q < -128 ? -128 : q));
+          }
+          w[e / 4] = pack4_sat_s8(v4[0], v4[1], v4[2], v4[3]);
+        }
+        int8_t* dst = args.out + (static_cast<int64_t>(ti.problem) * N + ti.off + row) * D + c * OW;
+#pragma unroll
+        for (int e = 0; e < OW / 4; ++e) reinterpret_cast<uint32_t*>(dst)[e] = w[e];
+      }
+      if (warp_live) {
+        const uint32_t f = __reduce_or_sync(0xffffffffu, acc_flags);
+        if (lane == 0 && f != 0) atomicOr(args.acc_flags, static_cast<int32_t>(f));
+      }
+      it0 += Tc;
+      continue;
     }
     if (warp_live) {
       uint32_t lraw;
@@ -1078,6 +1168,24 @@ __device__ __forceinline__ void correction_role(const AttnArgs& args, const IntP
   } while (0)
 #endif
 #define QF_FQ_TS(a, k) QF_FQ_TS_AT(a, k, 0, 0)
+// Source float4 of output vector i (the [P, N, d] layout of tensor t) in the fused step's
+// input: the same index for three separate tensors; for a packed QKV projection output
+// [P / H, N, 3, H, d] (N2, dynamic quantization of the projection P:L703) the (n, h)
+// transpose: problem p = b H + h, row n, lane k4 -> ((b N + n) 3 + t) H d/4 + h d/4 + k4.
+template <int D>
+QF_DEV int64_t qkv_src_vec(const AttnArgs& a, int t, int64_t i) {
+  constexpr int R = D / 4;  // float4 per row
+  constexpr int kShift = D == 32 ? 3 : D == 64 ? 4 : 5;
+  if (a.qkv_H == 0) return i;
+  const uint64_t row = static_cast<uint64_t>(i) >> kShift;  // p N + n
+  const int k4 = static_cast<int>(i & (R - 1));
+  const uint64_t p = a.N == 1 ? row : __umul64hi(row, a.qkv_n_magic);  // (ceil(2^64 / 1) overflows)
+  const uint64_t n = row - p * static_cast<uint64_t>(a.N);
+  const uint64_t b = a.qkv_H == 1 ? p : __umul64hi(p, a.qkv_h_magic);
+  const uint64_t h = p - b * static_cast<uint64_t>(a.qkv_H);
+  return static_cast<int64_t>(((b * a.N + n) * 3 + t) * (static_cast<uint64_t>(a.qkv_H) * R) + h * R + k4);
+}
+
 // Quantize one float4 (4 elements) -> 4 packed int8 codes (exact, see qflash_quant_elem.cuh).
 __device__ __forceinline__ uint32_t quant4(const float4& v, float s, float r) {
   int32_t q[4];
@@ -1131,7 +1239,7 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
 #pragma unroll
       for (int u = 0; u < kVR; ++u) {
         const int64_t i = gtid + u * nthr;
-        reg[t][u] = i < nvec ? __ldg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        reg[t][u] = i < nvec ? ldg_stream(src + qkv_src_vec<D>(a, t, i)) : make_float4(0.f, 0.f, 0.f, 0.f);  // no L1 allocation
       }
     }
 #pragma unroll
@@ -1144,8 +1252,8 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
         const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
-        v[t][0] = __ldg(src + i);
-        v[t][1] = i + nthr < nvec ? __ldg(src + i + nthr) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[t][0] = __ldg(src + qkv_src_vec<D>(a, t, i));
+        v[t][1] = i + nthr < nvec ? __ldg(src + qkv_src_vec<D>(a, t, i + nthr)) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int t = 0; t < 3; ++t) m[t] = amax4(amax4(m[t], v[t][0]), v[t][1]);
@@ -1243,8 +1351,8 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
         const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
-        v[t][0] = __ldcg(src + i);
-        v[t][1] = two ? __ldcg(src + i + nthr) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[t][0] = __ldcg(src + qkv_src_vec<D>(a, t, i));
+        v[t][1] = two ? __ldcg(src + qkv_src_vec<D>(a, t, i + nthr)) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
@@ -1267,7 +1375,7 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ = 0, bool PH = false>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ = 0, bool PH = false, bool ACC = false>
 __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
     qflash_attn_kernel(const __grid_constant__ CUtensorMap tm_q,
                        const __grid_constant__ CUtensorMap tm_k,
@@ -1303,7 +1411,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
     prefetch_tmap(&tm_v);
     for (int g = 0; g < QT; ++g) {
       const Bars gb{bars + g * C::kBarsPerGroup};
-      for (int s = 0; s < kStages; ++s) {
+      for (int s = 0; s < kMaxStages; ++s) {
         mbar_init(gb.kv_full(s), 1);
         mbar_init(gb.kv_empty(s), 1);
       }
@@ -1387,11 +1495,12 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
                       ti.off - s * args.N, ti.problem + s);
         if (!checked) ++nq;
         for (int j = 0; j < Tc; ++j, ++it) {
-          const int st = it % kStages;
-          if (it >= kStages) {
+          const int st = it % C::kSt;
+          if (it >= C::kSt) {
             if (!(ok = status_ok())) break;
-            mbar_wait_sleep(gb.kv_empty(st), ((it / kStages) - 1) & 1, QF_SLEEP_PROD);
+            mbar_wait_sleep(gb.kv_empty(st), ((it / C::kSt) - 1) & 1, QF_SLEEP_PROD);
           }
+          if (ti.i == 0 && blockIdx.x == 0 && g == 0 && j < 7) QF_TS(5 + 4 * j);
           mbar_arrive_expect_tx(gb.kv_full(st), ti.nseg * 2 * C::kKVBytes);
           for (int s = 0; s < ti.nseg; ++s) {
             tma_load_3d(sK + (st * NSEG + s) * C::kKVBytes, &tm_k, gb.kv_full(st), 0, j * BC,
@@ -1461,9 +1570,9 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
           if (ti.i == 0 && blockIdx.x == 0 && g == 0) QF_TS(2);
           auto issue_qk = [&](int j) {
             const int it = it0 + j;
-            const int st = it % kStages;
+            const int st = it % C::kSt;
             const int sb = (C::kNumS == 2) ? (it & 1) : 0;
-            mbar_wait(gb.kv_full(st), (it / kStages) & 1);
+            mbar_wait(gb.kv_full(st), (it / C::kSt) & 1);
             if constexpr (C::kSepP) {
               if (it > 0) mbar_wait(gb.s_empty(), (it - 1) & 1);  // S_{it-1} read by every softmax warp
             }
@@ -1481,11 +1590,12 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
               }
             }
             mma_commit(gb.s_full(sb));
+            if (ti.i == 0 && blockIdx.x == 0 && g == 0 && j < 7) QF_TS(6 + 4 * j);
             if (j == Tc - 1) mma_commit(gb.q_empty(qb));  // last read of this Q tile
           };
           auto issue_pv = [&](int j) {
             const int it = it0 + j;
-            const int st = it % kStages;
+            const int st = it % C::kSt;
             const int sb = (C::kNumS == 2) ? (it & 1) : 0;
             // (8) O (+)= sum_s P_s [V_{s,j} | 1] : M=128, N=D+16, K=BC in steps of 32 keys.
             if constexpr (C::kRC) {
@@ -1504,7 +1614,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
                 const uint64_t db = make_smem_desc(vk, ones_addr - v_addr, 8 * D, kSwz);
                 mma_i8_ts(tO, C::kSepP ? tG + C::kPCol + 8 * kk : tG + sb * BC + p_col_k<BC, C::kCW>(kk, s),
                           db, kIdescPV,
-                          (j > 0 || s > 0 || kk > 0) ? 1u : 0u);
+                          ((!ACC && j > 0) || s > 0 || kk > 0) ? 1u : 0u);  // ACC: P V_j fresh per tile
               }
             }
             mma_commit(gb.kv_empty(st));
@@ -1546,9 +1656,11 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
       const uint32_t tG = tmem_base + g * C::kGroupCols;
       // (PH: the header's q_shift / s_inv / m_p encode "every head takes the fast path")
       if (prm.q_shift == 0 && static_cast<uint64_t>(prm.s_inv) * static_cast<uint64_t>(prm.m_p) < (1ull << 32))
-        softmax_role<D, BC, NSEG, CS, QT, DBG, true, PH>(args, prm, tG, gb, red_group, recip, g, c, warp & 3, lane);
+        softmax_role<D, BC, NSEG, CS, QT, DBG, true, PH, ACC>(args, prm, tG, gb, red_group, recip, g, c, warp & 3,
+                                                              lane);
       else
-        softmax_role<D, BC, NSEG, CS, QT, DBG, false, PH>(args, prm, tG, gb, red_group, recip, g, c, warp & 3, lane);
+        softmax_role<D, BC, NSEG, CS, QT, DBG, false, PH, ACC>(args, prm, tG, gb, red_group, recip, g, c, warp & 3,
+                                                               lane);
       }
     }
   }
@@ -1570,18 +1682,20 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
 // Host-side launch (called by the instantiation units).  `tiles` = number of
 // work tiles; the persistent grid is G = min(ceil(tiles / QT), SMs) CTAs whose
 // group g visits tiles b + g G, b + g G + QT G, ...
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ = 0, bool PH = false>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ = 0, bool PH = false, bool ACC = false>
 cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                           AttnArgs args, int64_t tiles, int sms, cudaStream_t stream) {
   using C = Cfg<D, BC, NSEG, CS, QT>;
   static_assert(C::kAlloc <= 227 * 1024, "shared memory budget");
   static_assert(!PH || CS > 1, "per-head constants: column-split configurations only");
-  auto kern = qflash_attn_kernel<D, BC, NSEG, CS, QT, DBG, FQ, PH>;
+  static_assert(!ACC || (CS > 1 && NSEG == 1 && !FQ && !PH), "scale accumulation: cfg 0/1 generic tiles");
+  auto kern = qflash_attn_kernel<D, BC, NSEG, CS, QT, DBG, FQ, PH, ACC>;
+  constexpr int kSmem = C::kAlloc;
   static int configured[16] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 16 || !configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kAlloc);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 16) configured[dev] = 1;
   }
@@ -1603,7 +1717,8 @@ cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CU
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(G));
   cfg.blockDim = dim3(C::kThreads);
-  cfg.dynamicSmemBytes = C::kAlloc;
+  cfg.dynamicSmemBytes = kSmem;
+
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   if constexpr (FQ) {

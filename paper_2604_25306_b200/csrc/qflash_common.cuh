@@ -67,6 +67,13 @@ struct AttnArgs {
   uint32_t h_magic;           // ceil(2^32 / H): problem / H = umulhi(problem, h_magic)
   const float* amax_in;       // fused step: device float[3] amax of Q, K, V supplied by the
                               // caller (sharded quantization), or nullptr (computed here)
+  int32_t* acc_flags;         // scale-accumulation ablation (Eq. 13): overflow flags, or nullptr
+  // fused step, packed QKV projection output: xin[0..2] all point at one
+  // [P / H, N, 3, H, d] fp32 tensor; qkv_H = H (0: three separate [P, N, d] tensors)
+  int32_t qkv_H;
+  int32_t pad3;
+  uint64_t qkv_n_magic;       // ceil(2^64 / N): floor(x / N) = umul64hi(x, magic), x < 2^32
+  uint64_t qkv_h_magic;       // ceil(2^64 / H)
   int32_t cluster_grid;       // fused step: 1 = the grid is one thread-block cluster
                               // (barrier.cluster replaces the grid barriers)
   int32_t pad2;

@@ -38,6 +38,9 @@ cudaError_t launch_fused_d64(int BC, int nseg, int cfg, const CUtensorMap& tq, c
 cudaError_t launch_fused_d128(int BC, int nseg, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
                               const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
                               cudaStream_t stream);
+cudaError_t launch_attention_acc(int D, int BC, const CUtensorMap& tq, const CUtensorMap& tk,
+                                 const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
+                                 cudaStream_t stream);
 cudaError_t launch_attention_ph(int D, int BC, int nseg, const CUtensorMap& tq,
                                 const CUtensorMap& tk, const CUtensorMap& tv,
                                 const AttnArgs& args, int64_t tiles, int sms,
@@ -229,6 +232,7 @@ struct FusedIn {
   float* scales;
   void* workspace;
   const float* amax_in;  // nullptr: the kernel computes the amax itself
+  int qkv_heads;         // > 0: x[0] is one packed [P / H, N, 3, H, d] projection output
 };
 
 qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
@@ -237,7 +241,8 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
                             const qf::IntParams* dev_prm, cudaStream_t stream, float* y,
                             const FusedIn* fin, int heads,
                             int32_t* dbg_s = nullptr, int32_t* dbg_p = nullptr,
-                            int32_t* dbg_o = nullptr, long long* dbg_t = nullptr) {
+                            int32_t* dbg_o = nullptr, long long* dbg_t = nullptr,
+                            int32_t* acc_flags = nullptr) {
   const int P = shape->num_problems, N = shape->seq_len, d = shape->head_dim;
   // KV block: with T_c = 1 every B_c >= N gives the same result (one block), so
   // take the smallest supported one; otherwise B_c = block_kv as requested.
@@ -271,6 +276,7 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   const int64_t waves_generic = (tiles_generic + sms - 1) / sms;
   const int64_t waves_packed = (tiles_packed + sms - 1) / sms;
   bool packed;
+  if (acc_flags != nullptr) variant = QFLASH_VARIANT_GENERIC;  // the Eq. 13 ablation: generic tiles
   switch (variant) {
     case QFLASH_VARIANT_AUTO:
       // one wave: pack when it saves a wave (A3 b8: 192 -> 148 tiles); several waves:
@@ -307,6 +313,7 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
       if (cfg == 0 && qf::attention_supported(d, bc_eff, nseg, c)) cfg = c;
   }
   if (cfg_env >= 0 && heads == 0 && qf::attention_supported(d, bc_eff, nseg, cfg_env)) cfg = cfg_env;
+  if (acc_flags != nullptr) cfg = 0;
   if (!qf::attention_supported(d, bc_eff, nseg, cfg))
     return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "no kernel configuration for d=%d block=%d", d, bc_eff);
   g_last_config = cfg | (nseg << 4);
@@ -336,11 +343,17 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
     }
     args.scales_out = fin->scales;
     args.amax_in = fin->amax_in;
+    if (fin->qkv_heads > 0) {
+      args.qkv_H = fin->qkv_heads;
+      args.qkv_n_magic = ~0ull / static_cast<uint64_t>(N) + 1ull;  // ceil(2^64 / N) (N = 1, H = 1: identity)
+      args.qkv_h_magic = ~0ull / static_cast<uint64_t>(fin->qkv_heads) + 1ull;
+    }
     args.prm_out = reinterpret_cast<qf::IntParams*>(fin->workspace);
     args.partial = reinterpret_cast<float*>(static_cast<char*>(fin->workspace) + qf::kWsPartialOffset);
     args.table_out = reinterpret_cast<uint32_t*>(static_cast<char*>(fin->workspace) + qf::kWsDqTableOffset);
     args.numel = static_cast<int64_t>(P) * N * d;
   }
+  args.acc_flags = acc_flags;
   args.dbg_s = dbg_s;
   args.dbg_p = dbg_p;
   args.dbg_o = dbg_o;
@@ -349,7 +362,9 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   args.Tr = static_cast<int32_t>(Tr);
   const bool dbg = dbg_s != nullptr || dbg_p != nullptr || dbg_o != nullptr || dbg_t != nullptr;
   cudaError_t e;
-  if (heads > 0) {  // per-head constants (configuration 0)
+  if (acc_flags != nullptr) {
+    e = qf::launch_attention_acc(d, bc_eff, tq, tk, tv, args, tiles, sms, stream);
+  } else if (heads > 0) {  // per-head constants (configuration 0)
     args.head_prm = reinterpret_cast<const qf::IntParams*>(reinterpret_cast<const char*>(dev_prm) +
                                                           qf::kHeadPrmOffset);
     args.H = heads;
@@ -615,6 +630,33 @@ qflash_status qflash_forward_fused(const float* q, const float* k, const float* 
                                    workspace_dev, nullptr, stream);
 }
 
+qflash_status qflash_attention_int8_accum(const int8_t* q, const int8_t* k, const int8_t* v, float s_q,
+                                         float s_k, const qflash_attn_shape* shape, int8_t* o,
+                                         int32_t* flags_dev, qflash_stream_t stream) {
+  int bc = 0;
+  qflash_status st = validate_shape(shape, &bc);
+  if (st != QFLASH_OK) return st;
+  if (shape->head_dim == 128) return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "scale accumulation: head_dim 32 or 64");
+  const int N = shape->seq_len;
+  const int bc_eff = N <= bc ? (N <= 64 ? 64 : N <= 128 ? 128 : 256) : bc;
+  if (bc_eff > 128) return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "scale accumulation: block_kv 64 or 128");
+  const int64_t bytes = static_cast<int64_t>(shape->num_problems) * N * shape->head_dim;
+  if ((st = validate_qkvo(q, k, v, o, bytes)) != QFLASH_OK) return st;
+  if (!flags_dev || (reinterpret_cast<uintptr_t>(flags_dev) & 3u))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "flags_dev must be a 4-byte aligned device int32");
+  if (overlaps(flags_dev, 4, o, bytes)) return fail(QFLASH_ERR_INVALID_ARGUMENT, "flags_dev aliases o");
+  qf::IntParams prm;
+  const int rc = qf::derive_core(s_q, s_k, shape->head_dim, &prm, nullptr);
+  if (rc != QFLASH_OK) return fail(static_cast<qflash_status>(rc), "scale out of range");
+  int dev = 0;
+  if ((st = check_device(&dev)) != QFLASH_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(flags_dev, 0, 4, s);
+  if (e != cudaSuccess) return cuda_fail(e, "flags reset");
+  return launch_common(q, k, v, shape, bc, QFLASH_VARIANT_GENERIC, o, &prm, nullptr, s, nullptr, nullptr, 0,
+                       nullptr, nullptr, nullptr, nullptr, flags_dev);
+}
+
 qflash_status qflash_amax_qkv(const float* q, const float* k, const float* v, int64_t numel,
                               float* amax_dev, qflash_stream_t stream) {
   if (numel < 0) return fail(QFLASH_ERR_INVALID_ARGUMENT, "numel < 0");
@@ -635,7 +677,34 @@ qflash_status qflash_amax_qkv(const float* q, const float* k, const float* v, in
   return QFLASH_OK;
 }
 
+static qflash_status forward_fused_impl(const float* q, const float* k, const float* v, int qkv_heads,
+                                        const qflash_attn_shape* shape, qflash_variant variant,
+                                        int8_t* q_q, int8_t* k_q, int8_t* v_q, int8_t* o, float* y,
+                                        float* scales_dev, void* workspace_dev, const float* amax_dev,
+                                        qflash_stream_t stream);
+
 qflash_status qflash_forward_fused_amax(const float* q, const float* k, const float* v,
+                                        const qflash_attn_shape* shape, qflash_variant variant,
+                                        int8_t* q_q, int8_t* k_q, int8_t* v_q, int8_t* o, float* y,
+                                        float* scales_dev, void* workspace_dev, const float* amax_dev,
+                                        qflash_stream_t stream) {
+  return forward_fused_impl(q, k, v, 0, shape, variant, q_q, k_q, v_q, o, y, scales_dev, workspace_dev,
+                            amax_dev, stream);
+}
+
+qflash_status qflash_forward_fused_qkv(const float* qkv, int32_t heads, const qflash_attn_shape* shape,
+                                       qflash_variant variant, int8_t* q_q, int8_t* k_q, int8_t* v_q,
+                                       int8_t* o, float* y, float* scales_dev, void* workspace_dev,
+                                       qflash_stream_t stream) {
+  if (!shape) return fail(QFLASH_ERR_INVALID_ARGUMENT, "shape is NULL");
+  if (heads < 1 || shape->num_problems % heads != 0)
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "heads must be >= 1 and divide num_problems (%d, %d)",
+                heads, shape->num_problems);
+  return forward_fused_impl(qkv, qkv, qkv, heads, shape, variant, q_q, k_q, v_q, o, y, scales_dev,
+                            workspace_dev, nullptr, stream);
+}
+
+static qflash_status forward_fused_impl(const float* q, const float* k, const float* v, int qkv_heads,
                                         const qflash_attn_shape* shape, qflash_variant variant,
                                         int8_t* q_q, int8_t* k_q, int8_t* v_q, int8_t* o, float* y,
                                         float* scales_dev, void* workspace_dev, const float* amax_dev,
@@ -660,16 +729,17 @@ qflash_status qflash_forward_fused_amax(const float* q, const float* k, const fl
       return fail(QFLASH_ERR_INVALID_ARGUMENT, "int8 buffers must be 16-byte aligned");
   }
   const void* ins[3] = {q, k, v};
+  const int64_t in_bytes = qkv_heads > 0 ? 12 * n : 4 * n;  // packed QKV: one [P/H, N, 3, H, d] tensor
   const int8_t* codes[3] = {q_q, k_q, v_q};
   // every written buffer (codes, o, y) must be disjoint from every input and from
   // every other written buffer: the prologue re-reads inputs after other CTAs have
   // started writing codes, and the TMA loads read codes while y / o are written
   for (int i = 0; i < 3; ++i) {
     for (int j = 0; j < 2; ++j)
-      if (outs[j] && overlaps(outs[j], out_n[j], ins[i], 4 * n))
+      if (outs[j] && overlaps(outs[j], out_n[j], ins[i], in_bytes))
         return fail(QFLASH_ERR_INVALID_ARGUMENT, "outputs alias the inputs");
     for (int j = 0; j < 3; ++j) {
-      if (overlaps(codes[i], n, ins[j], 4 * n))
+      if (overlaps(codes[i], n, ins[j], in_bytes))
         return fail(QFLASH_ERR_INVALID_ARGUMENT, "int8 code buffer %d aliases input %d", i, j);
       if (j != i && overlaps(codes[i], n, codes[j], n))
         return fail(QFLASH_ERR_INVALID_ARGUMENT, "int8 code buffers %d and %d alias", i, j);
@@ -679,7 +749,7 @@ qflash_status qflash_forward_fused_amax(const float* q, const float* k, const fl
   }
   const int8_t* ws = static_cast<const int8_t*>(workspace_dev);
   for (int i = 0; i < 3; ++i)
-    if (overlaps(ws, QFLASH_DSCALE_WORKSPACE_BYTES, ins[i], 4 * n) ||
+    if (overlaps(ws, QFLASH_DSCALE_WORKSPACE_BYTES, ins[i], in_bytes) ||
         overlaps(ws, QFLASH_DSCALE_WORKSPACE_BYTES, codes[i], n))
       return fail(QFLASH_ERR_INVALID_ARGUMENT, "workspace aliases a tensor");
   int dev = 0;
@@ -694,6 +764,7 @@ qflash_status qflash_forward_fused_amax(const float* q, const float* k, const fl
   fin.scales = scales_dev;
   fin.workspace = workspace_dev;
   fin.amax_in = amax_dev;
+  fin.qkv_heads = qkv_heads;
   if (amax_dev != nullptr) {
     const int8_t* am = reinterpret_cast<const int8_t*>(amax_dev);
     if (overlaps(am, 12, ws, QFLASH_DSCALE_WORKSPACE_BYTES) ||

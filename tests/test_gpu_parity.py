@@ -664,3 +664,70 @@ def test_amax_qkv_edge_cases():
     x[1, 5, 7] = -1e30
     a = qf.qflash_amax_qkv(x, x * 2, -x).cpu()
     assert a.tolist() == [float(np.float32(1e30)), float(np.float32(2e30)), float(np.float32(1e30))]
+
+
+# ------------------------------------------------ Scale Accumulation ablation
+@pytest.mark.parametrize("N,d,bkv", [(49, 32, 64), (197, 64, 64), (197, 64, 128), (256, 64, 64),
+                                     (300, 32, 64), (1025, 64, 128)])
+def test_scale_accumulation_matches_oracle_mode1(orc, N, d, bkv):
+    # Eq. 13 in int64 with the oracle's wrap-around, bit-exact to oracle
+    # mode 1 on real-valued inputs (T_c = 1 .. 9), and the int64-overflow flag equal to
+    # the oracle's; int64 overflow implies int32 overflow.
+    w = "vit" if d == 64 else "swin"
+    q, k, v = gen_real_qkv(3, N, d, seed=N + bkv, family=w)
+    (qq, sq), (kq, sk), (vq, sv) = (orc.quantize(x) for x in (q, k, v))
+    ref, ovf = orc.attention(qq, kq, vq, sq, sk, block_kv=bkv, mode=1, return_overflow=True)
+    got, flags = qf.qflash_attention_int8_accum(*_dev(qq, kq, vq), sq, sk, block_kv=bkv)
+    f = int(flags.item())
+    assert np.array_equal(got.cpu().numpy(), ref), (N, d, bkv, int((got.cpu().numpy() != ref).sum()))
+    assert bool(f & 1) == ovf
+    assert not (f & 1) or (f & 2)
+
+
+def test_scale_accumulation_single_tile_equals_release(orc):
+    # T_c = 1: O = PV s_inv, l = rowsum s_inv -> floor(O / l) = floor(PV / rowsum), the
+    # same output as Scale Release (no release ever happens); no int64 overflow
+    q, k, v = gen_int8_qkv(4, 100, 64, seed=3)
+    got, flags = qf.qflash_attention_int8_accum(*_dev(q, k, v), 0.05, 0.05, block_kv=128)
+    rel = orc.attention(q, k, v, 0.05, 0.05, block_kv=128)
+    assert np.array_equal(got.cpu().numpy(), rel)
+    assert not (int(flags.item()) & 1)
+
+
+# ------------------------------------------------ packed QKV projection output
+def _pack_qkv(q, k, v, H):
+    P, N, d = q.shape
+    B = P // H
+    qkv = np.empty((B, N, 3, H, d), np.float32)
+    for t, x in enumerate((q, k, v)):
+        qkv[:, :, t] = x.reshape(B, H, N, d).transpose(0, 2, 1, 3)
+    return qkv
+
+
+@pytest.mark.parametrize("name,batch", [("A1", 1), ("A3", 8), ("A4", 1), ("A7", 8), ("L14", 1)])
+def test_fused_step_packed_qkv(orc, name, batch):
+    # the fused step reading a [B, N, 3, H, d] projection output directly (no permute pass)
+    # == the oracle on the three permuted tensors: codes, scales and fp32 output bit-exact
+    w = CATALOG[name]
+    q, k, v = gen_workload(name, batch, seed=21)
+    H = w.heads
+    qkv = torch.from_numpy(_pack_qkv(q, k, v, H)).cuda()
+    codes = [torch.empty(q.shape, dtype=torch.int8, device="cuda") for _ in range(3)]
+    sc = torch.empty(3, dtype=torch.float32, device="cuda")
+    y = qf.qflash_forward_fused_qkv(qkv, H, codes=codes, scales=sc).cpu().numpy()
+    (qq, sq), (kq, sk), (vq, sv) = (orc.quantize(x) for x in (q, k, v))
+    for t, (c, s) in enumerate(((qq, sq), (kq, sk), (vq, sv))):
+        assert np.array_equal(codes[t].cpu().numpy(), c)
+        assert np.float32(sc[t].item()).view(np.uint32) == np.float32(s).view(np.uint32)
+    ref = orc.dequantize(orc.attention(qq, kq, vq, sq, sk, block_kv=128), sv)
+    assert np.array_equal(y.view(np.uint32), ref.view(np.uint32))
+
+
+def test_fused_step_packed_qkv_rejects_bad_heads():
+    qkv = torch.zeros((2, 49, 3, 3, 32), device="cuda")
+    with pytest.raises(ValueError):
+        qf.qflash_forward_fused_qkv(qkv, 4)
+    shape = _lib.AttnShape(7, 49, 32, 128)
+    st = _lib.lib().qflash_forward_fused_qkv(qkv.data_ptr(), 3, shape, 0, None, None, None, None, None,
+                                             None, None, None)
+    assert st == _lib.QFLASH_ERR_INVALID_ARGUMENT

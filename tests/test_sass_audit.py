@@ -41,11 +41,11 @@ def _functions():
 
 def test_attention_kernels_integer_only_and_tensor_core():
     funcs = _functions()
-    # template <D, B_c, NSEG, CS, QT, DBG, FQ>: DBG = false, FQ = false are the
-    # integer-only attention kernels; FQ = true adds the Eq. 2 quantizer prologue
+    # template <D, B_c, NSEG, CS, QT, DBG, FQ, PH, ACC>: DBG = false, FQ = 0 are the
+    # integer-only attention kernels (ACC: the Eq. 13 ablation); FQ = 1 adds the Eq. 2 quantizer prologue
     # (fp32 by definition) in front of the same integer code
-    prod = {n: ops for n, ops in funcs.items() if "qflash_attn_kernel" in n and "ELb0ELb0E" in n}
-    fused = [n for n in funcs if "qflash_attn_kernel" in n and "ELb0ELb1E" in n]
+    prod = {n: ops for n, ops in funcs.items() if "qflash_attn_kernel" in n and "ELb0ELi0E" in n}
+    fused = [n for n in funcs if "qflash_attn_kernel" in n and "ELb0ELi1E" in n]
     assert len(fused) >= 20
     assert len(prod) >= 20, sorted(funcs)[:10]
     for name, ops in prod.items():

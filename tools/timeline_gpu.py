@@ -15,6 +15,8 @@ NAMES = {0: "entry", 1: "setup done", 2: "mma: Q landed", 100: "softmax: final P
 for j in range(7):
     NAMES[3 + 4 * j] = f"mma: KV{j} landed"
     NAMES[4 + 4 * j] = f"mma: P{j} ready"
+    NAMES[5 + 4 * j] = f"prod: KV{j} load issued"
+    NAMES[6 + 4 * j] = f"mma: QK{j} issued"
     NAMES[40 + 8 * j] = f"softmax: S{j} ready"
     NAMES[41 + 8 * j] = f"softmax: max{j} exchanged"
     NAMES[42 + 8 * j] = f"softmax: P{j} start"
