@@ -74,6 +74,12 @@ QF_DEV bool mbar_test_wait(uint32_t bar, uint32_t parity) {
 // Wait with a sleep between probes: for warps whose wait is usually long and not
 // on the critical path (producers, correction warps), so that their polling does
 // not take issue slots from the computing warps of the same SM sub-partition.
+// Busy-polling wait (no suspend): for a single thread on a latency-critical edge.
+QF_DEV void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_test_wait(a, parity)) {
+  }
+}
 QF_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
   const uint32_t a = smem_u32(bar);
   while (!mbar_test_wait(a, parity)) __nanosleep(ns);

@@ -43,6 +43,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include <cooperative_groups.h>
 
@@ -603,7 +604,6 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
   const bool dbg_on = DBG && blockIdx.x == 0 && g == 0;
   const bool ts_warp = dbg_on && c == 0 && quarter == 0 && lane == 0;
   const RowConsts rck = row_consts(prm_k, Tc);  // per-tensor constants (PH: per tile below)
-  bool tables_ready = false;  // named barrier 15: step (11) / dequant tables in smem
 
   TileIter<NSEG> ti;
   ti.init(args, blockIdx.x + g * gridDim.x);
@@ -839,10 +839,6 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
     mbar_wait(gb.o_full(), itl & 1);
     tc_fence_after();
     if (dbg && ts_warp) QF_TS(100);
-    if (!tables_ready) {
-      named_bar_sync(15, C::kNWG * 128 + 32);
-      tables_ready = true;
-    }
     if constexpr (ACC) {
       acc_fold(alpha_prev);
       if (warp_live && live) {
@@ -890,7 +886,6 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
     // arrival, so the next tile's first P V (which overwrites O) cannot race them.
     it0 += Tc;
   }
-  if (!tables_ready) named_bar_arrive(15, C::kNWG * 128 + 32);  // a group without tiles
 }
 
 // ---------------------------------------------------------------- row-owner roles (CS = 1)
@@ -1023,7 +1018,6 @@ __device__ __forceinline__ void correction_role(const AttnArgs& args, const IntP
     const int64_t t = (static_cast<int64_t>(A) - static_cast<int64_t>(prm.s_inv)) / 384 - 2 * Tc;
     rel_lthr = t < 0 ? -1 : (t > 0x7FFFFFFF ? 0x7FFFFFFF : static_cast<int32_t>(t));
   }
-  bool tables_ready = false;
   TileIter<NSEG> ti;
   ti.init(args, blockIdx.x + g * gridDim.x);
   int it0 = 0;
@@ -1085,10 +1079,6 @@ __device__ __forceinline__ void correction_role(const AttnArgs& args, const IntP
     // (11) O_i = floor(O / l), saturated (R14), stores
     mbar_wait(gb.o_full(), (it0 + Tc - 1) & 1);
     tc_fence_after();
-    if (!tables_ready) {
-      named_bar_sync(15, C::kNWG * 128 + 32);
-      tables_ready = true;
-    }
     if (warp_live) {
       uint32_t lraw;
       tmem_ld1(tO + D, lraw);
@@ -1141,7 +1131,6 @@ __device__ __forceinline__ void correction_role(const AttnArgs& args, const IntP
     }
     it0 += Tc;
   }
-  if (!tables_ready) named_bar_arrive(15, C::kNWG * 128 + 32);
 }
 
 // ---------------------------------------------------------------- fused-step prologue
@@ -1172,11 +1161,11 @@ __device__ __forceinline__ void correction_role(const AttnArgs& args, const IntP
 // input: the same index for three separate tensors; for a packed QKV projection output
 // [P / H, N, 3, H, d] (N2, dynamic quantization of the projection P:L703) the (n, h)
 // transpose: problem p = b H + h, row n, lane k4 -> ((b N + n) 3 + t) H d/4 + h d/4 + k4.
-template <int D>
+template <int D, bool PACKED>
 QF_DEV int64_t qkv_src_vec(const AttnArgs& a, int t, int64_t i) {
   constexpr int R = D / 4;  // float4 per row
   constexpr int kShift = D == 32 ? 3 : D == 64 ? 4 : 5;
-  if (a.qkv_H == 0) return i;
+  if constexpr (!PACKED) return i;
   const uint64_t row = static_cast<uint64_t>(i) >> kShift;  // p N + n
   const int k4 = static_cast<int>(i & (R - 1));
   const uint64_t p = a.N == 1 ? row : __umul64hi(row, a.qkv_n_magic);  // (ceil(2^64 / 1) overflows)
@@ -1232,32 +1221,43 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
     if (threadIdx.x < 3) scratch[96 + threadIdx.x] = __ldcg(a.amax_in + threadIdx.x);
   } else {
   if (resident) {
-    // every load of all three tensors in flight before the first reduction
+    // every load of all three tensors in flight before the first reduction (packed
+    // QKV input: the same loads with the (token, head) transpose of the addresses)
+    auto load_all = [&](auto packed) {
 #pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
+      for (int t = 0; t < 3; ++t) {
+        const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
 #pragma unroll
-      for (int u = 0; u < kVR; ++u) {
-        const int64_t i = gtid + u * nthr;
-        reg[t][u] = i < nvec ? ldg_stream(src + qkv_src_vec<D>(a, t, i)) : make_float4(0.f, 0.f, 0.f, 0.f);  // no L1 allocation
+        for (int u = 0; u < kVR; ++u) {
+          const int64_t i = gtid + u * nthr;
+          reg[t][u] = i < nvec ? ldg_stream(src + qkv_src_vec<D, decltype(packed)::value>(a, t, i))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);  // no L1 allocation
+        }
       }
-    }
+    };
+    if (a.qkv_H == 0) load_all(std::false_type{});
+    else load_all(std::true_type{});
 #pragma unroll
     for (int t = 0; t < 3; ++t)
 #pragma unroll
       for (int u = 0; u < kVR; ++u) m[t] = amax4(m[t], reg[t][u]);
   } else {
-    for (int64_t i = gtid; i < nvec; i += 2 * nthr) {  // 6 16-B loads in flight
-      float4 v[3][2];
+    auto stream_amax = [&](auto packed) {
+      constexpr bool PK = decltype(packed)::value;
+      for (int64_t i = gtid; i < nvec; i += 2 * nthr) {  // 6 16-B loads in flight
+        float4 v[3][2];
 #pragma unroll
-      for (int t = 0; t < 3; ++t) {
-        const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
-        v[t][0] = __ldg(src + qkv_src_vec<D>(a, t, i));
-        v[t][1] = i + nthr < nvec ? __ldg(src + qkv_src_vec<D>(a, t, i + nthr)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int t = 0; t < 3; ++t) {
+          const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
+          v[t][0] = __ldg(src + qkv_src_vec<D, PK>(a, t, i));
+          v[t][1] = i + nthr < nvec ? __ldg(src + qkv_src_vec<D, PK>(a, t, i + nthr)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int t = 0; t < 3; ++t) m[t] = amax4(amax4(m[t], v[t][0]), v[t][1]);
       }
-#pragma unroll
-      for (int t = 0; t < 3; ++t) m[t] = amax4(amax4(m[t], v[t][0]), v[t][1]);
-    }
+    };
+    if (a.qkv_H == 0) stream_amax(std::false_type{});
+    else stream_amax(std::true_type{});
   }
 #pragma unroll
   for (int t = 0; t < 3; ++t) {
@@ -1345,22 +1345,27 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
       }
     }
   } else {
-    for (int64_t i = gtid; i < nvec; i += 2 * nthr) {
-      const bool two = i + nthr < nvec;
-      float4 v[3][2];
+    auto stream_quant = [&](auto packed) {
+      constexpr bool PK = decltype(packed)::value;
+      for (int64_t i = gtid; i < nvec; i += 2 * nthr) {
+        const bool two = i + nthr < nvec;
+        float4 v[3][2];
 #pragma unroll
-      for (int t = 0; t < 3; ++t) {
-        const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
-        v[t][0] = __ldcg(src + qkv_src_vec<D>(a, t, i));
-        v[t][1] = two ? __ldcg(src + qkv_src_vec<D>(a, t, i + nthr)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+        for (int t = 0; t < 3; ++t) {
+          const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
+          v[t][0] = __ldcg(src + qkv_src_vec<D, PK>(a, t, i));
+          v[t][1] = two ? __ldcg(src + qkv_src_vec<D, PK>(a, t, i + nthr)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
 #pragma unroll
-      for (int t = 0; t < 3; ++t) {
-        uint32_t* dst = reinterpret_cast<uint32_t*>(a.xq[t]);
-        dst[i] = quant4(v[t][0], s3[t], r3[t]);
-        if (two) dst[i + nthr] = quant4(v[t][1], s3[t], r3[t]);
+        for (int t = 0; t < 3; ++t) {
+          uint32_t* dst = reinterpret_cast<uint32_t*>(a.xq[t]);
+          dst[i] = quant4(v[t][0], s3[t], r3[t]);
+          if (two) dst[i + nthr] = quant4(v[t][1], s3[t], r3[t]);
+        }
       }
-    }
+    };
+    if (a.qkv_H == 0) stream_quant(std::false_type{});
+    else stream_quant(std::true_type{});
   }
   // int8 codes (generic-proxy stores) -> TMA loads of other CTAs after the barrier
   QF_FQ_TS(a, 4);
@@ -1434,6 +1439,9 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
     tmem_alloc(tmem_slot, kTmemCols);
     tmem_relinquish();
   }
+  // reciprocal table of step (11) (a constant: loaded before the grid dependency wait)
+  for (int i = threadIdx.x; i < 256; i += C::kThreads)
+    reinterpret_cast<uint4*>(recip)[i] = reinterpret_cast<const uint4*>(g_recip.v)[i];
   // ones block of the extended V operand (any layout: every byte is 1)
   for (int i = threadIdx.x; i < BC * D / 16; i += C::kThreads)
     reinterpret_cast<uint4*>(sOnes)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
@@ -1451,6 +1459,15 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
     fused_quantize_prologue<D>(args, reinterpret_cast<float*>(smem + C::kScratch), sprm, recip + 1024);
     __syncthreads();
   }
+  if constexpr (!FQ) {
+    if (args.out_f32 != nullptr) {  // fused dequantization table (256 fp32 bit patterns)
+      if (threadIdx.x < 64)
+        reinterpret_cast<uint4*>(recip + 1024)[threadIdx.x] = reinterpret_cast<const uint4*>(args.dq_table)[threadIdx.x];
+      __syncthreads();
+    }
+  }
+  // (the fused step's prologue built the dequant table before its final __syncthreads:
+  // every table the epilogue reads is in shared memory before the roles start)
   const IntParams* dprm = FQ ? sprm : args.dev_prm;  // constants in memory, or nullptr (by value)
 
   if (warp < 2) {
@@ -1524,25 +1541,6 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
     if (warp < 2) {
       // (producer role above)
     } else if (warp < 4) {
-      if (warp == 3) {
-        // reciprocal table for step (11) -> shared memory, off the critical path:
-        // the softmax warps sync on named barrier 15 before their first normalization.
-        {
-          uint4 t[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) t[k] = reinterpret_cast<const uint4*>(g_recip.v)[lane + 32 * k];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) reinterpret_cast<uint4*>(recip)[lane + 32 * k] = t[k];
-          if (!FQ && args.out_f32 != nullptr) {  // fused dequantization table (256 fp32 bit patterns)
-            const uint4* src = reinterpret_cast<const uint4*>(args.dq_table);
-            const uint4 a = src[lane], b = src[lane + 32];
-            reinterpret_cast<uint4*>(recip + 1024)[lane] = a;
-            reinterpret_cast<uint4*>(recip + 1024)[lane + 32] = b;
-          }
-        }
-        __threadfence_block();
-        named_bar_arrive(15, C::kNWG * 128 + 32);
-      }
       // ========================================================= MMA issuer of group `warp - 2`
       // Issue order within a tile (tcgen05.mma of one thread execute in order,
       // which also orders every TMEM WAR hazard between P V and a later Q K^T):
@@ -1642,7 +1640,6 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
         const bool fastq = prm.q_shift == 0 &&
                            static_cast<uint64_t>(prm.s_inv) * static_cast<uint64_t>(prm.m_p) < (1ull << 32);
         if ((wg & 1) == 0) {
-          named_bar_arrive(15, C::kNWG * 128 + 32);  // softmax threads never read the tables
           if (fastq) softmax_rc_role<D, BC, NSEG, QT, true>(args, prm, tG, gb, abuf, g, warp & 3, lane);
           else softmax_rc_role<D, BC, NSEG, QT, false>(args, prm, tG, gb, abuf, g, warp & 3, lane);
         } else {
