@@ -326,6 +326,9 @@ def main():
                     help="attention tiling (auto: row-packed when it saves a wave)")
     ap.add_argument("--scales", default="per-tensor", choices=["per-tensor", "per-head"],
                     help="granularity (per-head = SURVEY 8(f) N1; 5 launches per step)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo: collectives through host copies, ranks may "
+                         "share a GPU -- a functional test of the multi-rank path on one device)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -346,11 +349,32 @@ def main():
     from paper_2604_25306_b200.inputs import gen_real_qkv_slab
 
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    gloo = args.dist_backend == "gloo"
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def all_reduce(t, op):
+        if gloo:  # gloo collectives on host copies
+            h = t.cpu()
+            dist.all_reduce(h, op=op)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=op)
+
+    def all_gather(outs, t):
+        if gloo:
+            hs = [torch.empty_like(t, device="cpu") for _ in outs]
+            dist.all_gather(hs, t.cpu())
+            for o, h in zip(outs, hs):
+                o.copy_(h)
+        else:
+            dist.all_gather(outs, t)
 
     name, batch, w = workload_from_args(args)
     P_batch, N, d = w.problems(batch), w.seq_len, w.head_dim
@@ -394,7 +418,7 @@ def main():
 
         def run_step(i):
             g_amax[i % n_sets].replay()
-            dist.all_reduce(amax_bufs[i % n_sets], op=dist.ReduceOp.MAX)
+            all_reduce(amax_bufs[i % n_sets], dist.ReduceOp.MAX)
             g_step[i % n_sets].replay()
         launches_per_step = 2
     else:
@@ -435,7 +459,7 @@ def main():
     t_all = torch.zeros(world, device=dev, dtype=torch.float64)
     t_all[rank] = elapsed_ms
     if world > 1:
-        dist.all_reduce(t_all, op=dist.ReduceOp.SUM)
+        all_reduce(t_all, dist.ReduceOp.SUM)
     rank_ms = [float(x) / args.steps for x in t_all.cpu().tolist()]
     elapsed_ms = max(float(x) for x in t_all.cpu().tolist())
     ms_per_step = elapsed_ms / args.steps
@@ -576,7 +600,7 @@ def main():
         assert torch.equal(ref_out.cpu(), houts[(k_e2e - 1) % 2]), "e2e output mismatch"
         e_t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
         if world > 1:
-            dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
+            all_reduce(e_t, dist.ReduceOp.MAX)
         e_ms = float(e_t.item())
         e2e = {"value": algorithmic(P_total, N, d)["int8_ops"] * k_e2e / (e_ms * 1e-3) / 1e12,
                "unit": "TOPS", "h2d_bytes_per_step": 3 * 4 * P_local * N * d,
@@ -600,8 +624,8 @@ def main():
         csum = y.view(torch.int32).to(torch.int64).sum().reshape(1)
         g_s = [torch.empty_like(loc) for _ in range(world)]
         g_c = [torch.empty_like(csum) for _ in range(world)]
-        dist.all_gather(g_s, loc)
-        dist.all_gather(g_c, csum)
+        all_gather(g_s, loc)
+        all_gather(g_c, csum)
         ok = True
         if rank == 0:
             ref_q = [torch.from_numpy(a).to(dev) for a in
@@ -618,7 +642,7 @@ def main():
                                                                      for t in ref_q])
                 ok = ok and torch.equal(ref[:samp].view(torch.int32), g_s[r][:min(samp, c_r)].view(torch.int32))
                 ok = ok and int(ref.view(torch.int32).to(torch.int64).sum()) == int(g_c[r].item())
-        verify = {"ok": bool(ok), "method": "NCCL all_gather of each rank's first %d problems + int64 "
+        verify = {"ok": bool(ok), "method": args.dist_backend.upper() + " all_gather of each rank's first %d problems + int64 "
                   "checksum of its fp32 output, compared on rank 0 with a 1-GPU run of the same rows "
                   "(%s)" % (samp, "whole batch" if strong else "each slab")}
         if rank == 0 and not ok:

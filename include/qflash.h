@@ -246,6 +246,22 @@ QFLASH_API qflash_status qflash_attention_int8_accum(const int8_t* q, const int8
                                                      float s_q, float s_k, const qflash_attn_shape* shape,
                                                      int8_t* o, int32_t* flags_dev, qflash_stream_t stream);
 
+/* Ablation steps of the paper's Table on the same kernel
+ * skeleton (int8 Q K^T and int8 P V on tcgen05, generic tiles, configuration 0):
+ *   QFLASH_ABLATION_V3: integer ShiftExp2 + requant (the method's P bytes), but O and l
+ *       accumulated in fp32: O <- O (alpha / s_inv) + P V_j (no integer ScaleRelease);
+ *   QFLASH_ABLATION_V2: floating-point softmax: P = rint(127 exp2(s (S - m))) with
+ *       ex2.approx, alpha = exp2(s (m_old - m_new)), int8 P V, fp32 accumulation.
+ * y: device fp32 [P, N, d] = s_v O / l.  Not integer-only and not bit-exact to anything:
+ * for the speed / accuracy comparison with the method (qflash_attention_int8 = V4).
+ * head_dim 32/64, block_kv 64/128; errors as qflash_attention_int8. */
+#define QFLASH_ABLATION_V2 2
+#define QFLASH_ABLATION_V3 3
+QFLASH_API qflash_status qflash_attention_ablation(const int8_t* q, const int8_t* k, const int8_t* v,
+                                                   float s_q, float s_k, float s_v,
+                                                   const qflash_attn_shape* shape, int32_t variant,
+                                                   float* y, qflash_stream_t stream);
+
 /* --------------------------------------------------------------------------
  * Per-head granularity (the paper's per-tensor scales are the
  * H = 1 case).  Problems are the flattened (batch,

@@ -35,7 +35,7 @@ EXPORTED = [
     "qflash_attention_dequant_prepared", "qflash_forward_fused",
     "qflash_quantize_per_head", "qflash_attention_int8_per_head", "qflash_dequantize_per_head",
     "qflash_amax_qkv", "qflash_forward_fused_amax", "qflash_attention_int8_accum",
-    "qflash_forward_fused_qkv",
+    "qflash_forward_fused_qkv", "qflash_attention_ablation",
 ]
 
 
@@ -100,6 +100,8 @@ def lib():
     L.qflash_forward_fused_qkv.restype = st
     L.qflash_forward_fused_qkv.argtypes = [vp, i32, ctypes.POINTER(AttnShape), st, vp, vp, vp, vp, vp, vp,
                                            vp, vp]
+    L.qflash_attention_ablation.restype = st
+    L.qflash_attention_ablation.argtypes = [vp, vp, vp, f32, f32, f32, ctypes.POINTER(AttnShape), i32, vp, vp]
     L.qflash_attention_int8_accum.restype = st
     L.qflash_attention_int8_accum.argtypes = [vp, vp, vp, f32, f32, ctypes.POINTER(AttnShape), vp, vp, vp]
     L.qflash_amax_qkv.restype = st

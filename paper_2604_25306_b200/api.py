@@ -238,6 +238,24 @@ def qflash_attention_int8_accum(q: torch.Tensor, k: torch.Tensor, v: torch.Tenso
     return out, flags
 
 
+ABLATIONS = {"V2": 2, "V3": 3}
+
+
+def qflash_attention_ablation(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, s_q: float,
+                              s_k: float, s_v: float, variant: str, block_kv: int = 128,
+                              out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """The paper's ablation steps on B200: "V3" integer exp + FP accumulation,
+    "V2" FP exp2 softmax + int8 P V; fp32 y = s_V O / l (qflash_attention_int8 is V4)."""
+    _check_qkv(q, k, v)
+    out = torch.empty(q.shape, dtype=torch.float32, device=q.device) if out is None else out
+    _check_like(q, out, "out", torch.float32)
+    shape = _shape(q, block_kv)
+    check(lib().qflash_attention_ablation(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v), float(s_q), float(s_k),
+                                          float(s_v), ctypes.byref(shape), ABLATIONS[variant],
+                                          _dev_ptr(out), _stream(stream)))
+    return out
+
+
 def qflash_amax_qkv(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
                     out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Device float[3]: max |x| of fp32 Q, K, V (this device's slab)."""

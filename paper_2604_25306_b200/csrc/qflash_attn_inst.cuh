@@ -8,11 +8,11 @@
 
 namespace qf {
 
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ, bool PH = false, bool ACC = false>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ, bool PH = false, int VAR = 0>
 cudaError_t try_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const AttnArgs& args, int64_t tiles, int sms, cudaStream_t stream) {
   if constexpr (config_fits<D, BC, NSEG, CS, QT>()) {
-    return launch_attn_t<D, BC, NSEG, CS, QT, DBG, FQ, PH, ACC>(tq, tk, tv, args, tiles, sms, stream);
+    return launch_attn_t<D, BC, NSEG, CS, QT, DBG, FQ, PH, VAR>(tq, tk, tv, args, tiles, sms, stream);
   } else {
     return cudaErrorNotSupported;
   }
@@ -55,13 +55,14 @@ cudaError_t launch_attention_ph_d(int BC, int nseg, const CUtensorMap& tq, const
   return cudaErrorNotSupported;
 }
 
-// Scale Accumulation ablation (Eq. 13, App. B.1): generic tiles, configuration 0.
-template <int D>
-cudaError_t launch_attention_acc_d(int BC, const CUtensorMap& tq, const CUtensorMap& tk,
+// Ablation variants (generic tiles, configuration 0): VAR 1 = Scale Accumulation (Eq. 13,
+// App. B.1), VAR 2 = V3 (integer exp, FP accumulation), VAR 3 = V2 (FP exp2, int8 P V).
+template <int D, int VAR>
+cudaError_t launch_attention_var_d(int BC, const CUtensorMap& tq, const CUtensorMap& tk,
                                    const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
                                    cudaStream_t stream) {
-  if (BC == 64) return try_launch<D, 64, 1, 4, 1, false, 0, false, true>(tq, tk, tv, args, tiles, sms, stream);
-  if (BC == 128) return try_launch<D, 128, 1, 4, 1, false, 0, false, true>(tq, tk, tv, args, tiles, sms, stream);
+  if (BC == 64) return try_launch<D, 64, 1, 4, 1, false, 0, false, VAR>(tq, tk, tv, args, tiles, sms, stream);
+  if (BC == 128) return try_launch<D, 128, 1, 4, 1, false, 0, false, VAR>(tq, tk, tv, args, tiles, sms, stream);
   return cudaErrorNotSupported;
 }
 

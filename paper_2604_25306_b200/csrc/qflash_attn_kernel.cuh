@@ -534,6 +534,26 @@ QF_DEV int64_t floor_div64(int64_t a, int64_t b) {
   return neg ? static_cast<int64_t>(~q) : static_cast<int64_t>(q);  // floor(a/b) = ~floor(~a/b), a < 0
 }
 
+// ---- FP softmax of the V2 ablation (N4): P = rint(127 exp2(s (S - m))) in fp32 --
+QF_DEV float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+template <int W>
+QF_DEV void p_pack_fp(const uint32_t* sc, int hv, int32_t m_new, float s_f, uint32_t* pw) {
+#pragma unroll
+  for (int e = 0; e < W; e += 4) {
+    int32_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float p = ex2_approx(static_cast<float>(static_cast<int32_t>(sc[e + u]) - m_new) * s_f);
+      v[u] = (e + u < hv) ? __float2int_rn(127.0f * p) : 0;
+    }
+    pw[e / 4] = pack4_sat_s8(v[0], v[1], v[2], v[3]);
+  }
+}
+
 // Step (11) for one row's OW output columns [c OW, c OW + OW): O = floor(O / l)
 // saturated to int8 (R14), stored as int8 and/or dequantized fp32 (DQ row) at
 // flattened output row `orow` (row-packed tiles included).
@@ -585,7 +605,7 @@ QF_DEV void normalize_store(const AttnArgs& args, int64_t orow, int c, const uin
   }
 }
 
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FASTQ, bool PH = false, bool ACC = false>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FASTQ, bool PH = false, int VAR = 0>
 __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntParams& prm_k,
                                              uint32_t tmem_group, GroupBars<Cfg<D, BC, NSEG, CS, QT>::kNumS> gb,
                                              uint32_t red_group, const uint32_t* recip, int g,
@@ -630,29 +650,50 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
     const uint32_t s_inv = PH ? rct.s_inv : rck.s_inv;
     const int sinv_log2 = PH ? rct.sinv_log2 : rck.sinv_log2;
     const int32_t rel_lthr = PH ? rct.rel_lthr : rck.rel_lthr;
-    // ACC (Eq. 13): int64 accumulators of this thread's O columns and l, in registers;
-    // P V_j lands fresh in TMEM every KV tile and is folded in here
-    int64_t o64[ACC ? OW : 1];
+    // Ablation variants (VAR > 0): P V_j lands fresh in TMEM every KV tile and is folded
+    // into register accumulators of this thread's O columns and l --
+    //   VAR 1 (Eq. 13, N3): int64, O <- O alpha + PV s_inv (flags: int64 / int32 overflow);
+    //   VAR 2 (V3, N4): fp32, O <- O (alpha / s_inv) + PV  (integer exp, FP accumulation);
+    //   VAR 3 (V2, N4): fp32, O <- O alpha_f + PV           (FP exp2 softmax, int8 P V).
+    constexpr bool kAcc = VAR == 1;
+    constexpr bool kFp = VAR >= 2;
+    int64_t o64[kAcc ? OW : 1];
+    float of[kFp ? OW : 1];
     int64_t l64 = 0;
+    float lf = 0.f;
     int32_t alpha_prev = 0;
+    float alpha_prev_f = 0.f;
     uint32_t acc_flags = 0;
-    if constexpr (ACC) {
+    if constexpr (kAcc) {
 #pragma unroll
       for (int e = 0; e < OW; ++e) o64[e] = 0;
     }
-    auto acc_fold = [&](int32_t al) {  // O <- O alpha + PV s_inv, l <- l alpha + rowsum(P) s_inv
-      if constexpr (!ACC) return;
+    if constexpr (kFp) {
+#pragma unroll
+      for (int e = 0; e < OW; ++e) of[e] = 0.f;
+    }
+    const float s_f = static_cast<float>(prm.s);              // VAR 3: real logit scale (log2 domain)
+    const float rinv_f = 1.0f / static_cast<float>(s_inv);   // VAR 2: 1 / s_inv
+    auto acc_fold = [&](int32_t al, float al_f) {
+      if constexpr (VAR == 0) return;
       if (!warp_live) return;
       uint32_t o[OW], lc;
       tmem_ld_cols<OW>(tO + c * OW, o);
       tmem_ld1(tO + D + c, lc);  // an unreleased copy of rowsum(P_j) from the ones block
       tmem_wait_ld();
-      uint32_t f = 0;
+      if constexpr (kAcc) {  // O <- O alpha + PV s_inv, l <- l alpha + rowsum(P) s_inv
+        uint32_t f = 0;
 #pragma unroll
-      for (int e = 0; e < OW; ++e)
-        o64[e] = acc_update(o64[e], al, static_cast<int32_t>(o[e]), static_cast<int32_t>(s_inv), f);
-      l64 = acc_update(l64, al, static_cast<int32_t>(lc), static_cast<int32_t>(s_inv), f);
-      if (live) acc_flags |= f;  // padding rows of the last query tile do not count
+        for (int e = 0; e < OW; ++e)
+          o64[e] = acc_update(o64[e], al, static_cast<int32_t>(o[e]), static_cast<int32_t>(s_inv), f);
+        l64 = acc_update(l64, al, static_cast<int32_t>(lc), static_cast<int32_t>(s_inv), f);
+        if (live) acc_flags |= f;  // padding rows of the last query tile do not count
+      } else {
+        const float a = VAR == 2 ? static_cast<float>(al) * rinv_f : al_f;
+#pragma unroll
+        for (int e = 0; e < OW; ++e) of[e] = fmaf(of[e], a, static_cast<float>(static_cast<int32_t>(o[e])));
+        lf = fmaf(lf, a, static_cast<float>(static_cast<int32_t>(lc)));
+      }
     };
 
     for (int j = 0; j < Tc; ++j) {
@@ -703,6 +744,8 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
       const int32_t m_new = max(m, tmax);
       // (4) alpha = ShiftExp2(m_old - m_new)
       const int32_t alpha = shift_exp2<FASTQ>(m - m_new, prm);
+      float alpha_f = 0.f;  // VAR 3: exp2(s (m_old - m_new)) in fp32
+      if constexpr (VAR == 3) alpha_f = ex2_approx(static_cast<float>(m - m_new) * s_f);
 
       // (5)(6) P = Requant(ShiftExp2(S - m_new)), 4 x int8 per TMEM column.
       const uint32_t mu = static_cast<uint32_t>(m_new);
@@ -730,7 +773,10 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
             tmem_ld32(tS + c0 + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(sc));
             tmem_wait_ld();
           }
-          p_pack<HW, FASTQ>(sc, hv, mu, nmu, c3, one, prm, pk + h * (HW / 4));
+          if constexpr (VAR == 3)
+            p_pack_fp<HW>(sc, hv, m_new, s_f, pk + h * (HW / 4));
+          else
+            p_pack<HW, FASTQ>(sc, hv, mu, nmu, c3, one, prm, pk + h * (HW / 4));
         }
       }
       if constexpr (C::kSepP) {
@@ -765,13 +811,14 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
       // the P computation; skipped for j = 0 (O = l = 0) and for warps whose rows
       // all kept their maximum (alpha = s_inv is the identity, R10).  P V_j is
       // issued only after every warp's p_full arrival below, i.e. after the release.
-      if constexpr (ACC) {
+      if constexpr (VAR != 0) {
         if (j > 0) {  // fold step j-1 (its alpha, its P V) before P V_j overwrites TMEM
           mbar_wait(gb.o_full(), (it - 1) & 1);
           tc_fence_after();
-          acc_fold(alpha_prev);
+          acc_fold(alpha_prev, alpha_prev_f);
         }
         alpha_prev = alpha;
+        alpha_prev_f = alpha_f;
       } else if (j > 0) {
         if constexpr (!C::kSepP) {
           mbar_wait(gb.o_full(), (it - 1) & 1);
@@ -839,8 +886,20 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
     mbar_wait(gb.o_full(), itl & 1);
     tc_fence_after();
     if (dbg && ts_warp) QF_TS(100);
-    if constexpr (ACC) {
-      acc_fold(alpha_prev);
+    if constexpr (VAR >= 2) {
+      acc_fold(alpha_prev, alpha_prev_f);
+      if (warp_live && live) {  // y = s_V O / l in fp32 (the FP variants' natural output)
+        const float k = args.s_v / lf;
+        float* ydst = args.out_f32 + (static_cast<int64_t>(ti.problem) * N + ti.off + row) * D + c * OW;
+#pragma unroll
+        for (int e = 0; e < OW; e += 4)
+          *reinterpret_cast<float4*>(ydst + e) = make_float4(of[e] * k, of[e + 1] * k, of[e + 2] * k, of[e + 3] * k);
+      }
+      it0 += Tc;
+      continue;
+    }
+    if constexpr (VAR == 1) {
+      acc_fold(alpha_prev, 0.f);
       if (warp_live && live) {
         uint32_t w[OW / 4];
 #pragma unroll
@@ -1380,7 +1439,7 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ = 0, bool PH = false, bool ACC = false>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ = 0, bool PH = false, int VAR = 0>
 __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
     qflash_attn_kernel(const __grid_constant__ CUtensorMap tm_q,
                        const __grid_constant__ CUtensorMap tm_k,
@@ -1459,7 +1518,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
     fused_quantize_prologue<D>(args, reinterpret_cast<float*>(smem + C::kScratch), sprm, recip + 1024);
     __syncthreads();
   }
-  if constexpr (!FQ) {
+  if constexpr (!FQ && VAR < 2) {
     if (args.out_f32 != nullptr) {  // fused dequantization table (256 fp32 bit patterns)
       if (threadIdx.x < 64)
         reinterpret_cast<uint4*>(recip + 1024)[threadIdx.x] = reinterpret_cast<const uint4*>(args.dq_table)[threadIdx.x];
@@ -1612,7 +1671,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
                 const uint64_t db = make_smem_desc(vk, ones_addr - v_addr, 8 * D, kSwz);
                 mma_i8_ts(tO, C::kSepP ? tG + C::kPCol + 8 * kk : tG + sb * BC + p_col_k<BC, C::kCW>(kk, s),
                           db, kIdescPV,
-                          ((!ACC && j > 0) || s > 0 || kk > 0) ? 1u : 0u);  // ACC: P V_j fresh per tile
+                          ((VAR == 0 && j > 0) || s > 0 || kk > 0) ? 1u : 0u);  // ablations: P V_j fresh per tile
               }
             }
             mma_commit(gb.kv_empty(st));
@@ -1653,10 +1712,10 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
       const uint32_t tG = tmem_base + g * C::kGroupCols;
       // (PH: the header's q_shift / s_inv / m_p encode "every head takes the fast path")
       if (prm.q_shift == 0 && static_cast<uint64_t>(prm.s_inv) * static_cast<uint64_t>(prm.m_p) < (1ull << 32))
-        softmax_role<D, BC, NSEG, CS, QT, DBG, true, PH, ACC>(args, prm, tG, gb, red_group, recip, g, c, warp & 3,
+        softmax_role<D, BC, NSEG, CS, QT, DBG, true, PH, VAR>(args, prm, tG, gb, red_group, recip, g, c, warp & 3,
                                                               lane);
       else
-        softmax_role<D, BC, NSEG, CS, QT, DBG, false, PH, ACC>(args, prm, tG, gb, red_group, recip, g, c, warp & 3,
+        softmax_role<D, BC, NSEG, CS, QT, DBG, false, PH, VAR>(args, prm, tG, gb, red_group, recip, g, c, warp & 3,
                                                                lane);
       }
     }
@@ -1679,14 +1738,14 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
 // Host-side launch (called by the instantiation units).  `tiles` = number of
 // work tiles; the persistent grid is G = min(ceil(tiles / QT), SMs) CTAs whose
 // group g visits tiles b + g G, b + g G + QT G, ...
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ = 0, bool PH = false, bool ACC = false>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ = 0, bool PH = false, int VAR = 0>
 cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                           AttnArgs args, int64_t tiles, int sms, cudaStream_t stream) {
   using C = Cfg<D, BC, NSEG, CS, QT>;
   static_assert(C::kAlloc <= 227 * 1024, "shared memory budget");
   static_assert(!PH || CS > 1, "per-head constants: column-split configurations only");
-  static_assert(!ACC || (CS > 1 && NSEG == 1 && !FQ && !PH), "scale accumulation: cfg 0/1 generic tiles");
-  auto kern = qflash_attn_kernel<D, BC, NSEG, CS, QT, DBG, FQ, PH, ACC>;
+  static_assert(VAR == 0 || (CS > 1 && NSEG == 1 && !FQ && !PH), "ablation variants: cfg 0/1 generic tiles");
+  auto kern = qflash_attn_kernel<D, BC, NSEG, CS, QT, DBG, FQ, PH, VAR>;
   constexpr int kSmem = C::kAlloc;
   static int configured[16] = {0};
   int dev = 0;

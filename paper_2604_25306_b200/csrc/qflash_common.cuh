@@ -68,6 +68,8 @@ struct AttnArgs {
   const float* amax_in;       // fused step: device float[3] amax of Q, K, V supplied by the
                               // caller (sharded quantization), or nullptr (computed here)
   int32_t* acc_flags;         // scale-accumulation ablation (Eq. 13): overflow flags, or nullptr
+  int32_t variant;            // ablation variant (0 = the method; 1 Eq. 13; 2 V3; 3 V2)
+  float s_v;                  // V2 / V3 ablations: s_V for the fp32 output y = s_V O / l
   // fused step, packed QKV projection output: xin[0..2] all point at one
   // [P / H, N, 3, H, d] fp32 tensor; qkv_H = H (0: three separate [P, N, d] tensors)
   int32_t qkv_H;

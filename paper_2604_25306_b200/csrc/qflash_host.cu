@@ -38,7 +38,7 @@ cudaError_t launch_fused_d64(int BC, int nseg, int cfg, const CUtensorMap& tq, c
 cudaError_t launch_fused_d128(int BC, int nseg, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
                               const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
                               cudaStream_t stream);
-cudaError_t launch_attention_acc(int D, int BC, const CUtensorMap& tq, const CUtensorMap& tk,
+cudaError_t launch_attention_var(int var, int D, int BC, const CUtensorMap& tq, const CUtensorMap& tk,
                                  const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
                                  cudaStream_t stream);
 cudaError_t launch_attention_ph(int D, int BC, int nseg, const CUtensorMap& tq,
@@ -158,8 +158,44 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 
 // 3-D int8 tensor map over [P][N][d] with box {d, rows, probs}.  Rows outside
 // [0, N) of a box are zero-filled by the TMA unit (ragged tiles, row-packed Q).
-qflash_status make_tmap(CUtensorMap* m, const int8_t* base, int P, int N, int d, int rows,
-                        int probs) {
+// A tensor map is a pure function of (base, P, N, d, rows, probs): the last few encodings
+// are cached per thread so repeated eager calls on the same buffers (serving loops,
+// single-call latency) skip cuTensorMapEncodeTiled.
+struct TmapKey {
+  const int8_t* base;
+  int P, N, d, rows, probs, dev;
+  bool operator==(const TmapKey& o) const {
+    return base == o.base && P == o.P && N == o.N && d == o.d && rows == o.rows && probs == o.probs &&
+           dev == o.dev;
+  }
+};
+constexpr int kTmapCache = 16;
+thread_local TmapKey g_tmap_key[kTmapCache];
+thread_local CUtensorMap g_tmap_val[kTmapCache];
+thread_local int g_tmap_n = 0, g_tmap_next = 0;
+
+qflash_status make_tmap_uncached(CUtensorMap* m, const int8_t* base, int P, int N, int d, int rows,
+                                 int probs);
+qflash_status make_tmap(CUtensorMap* m, const int8_t* base, int P, int N, int d, int rows, int probs) {
+  int dev = -1;
+  cudaGetDevice(&dev);
+  const TmapKey key{base, P, N, d, rows, probs, dev};
+  for (int i = 0; i < g_tmap_n; ++i)
+    if (g_tmap_key[i] == key) {
+      *m = g_tmap_val[i];
+      return QFLASH_OK;
+    }
+  qflash_status st = make_tmap_uncached(m, base, P, N, d, rows, probs);
+  if (st != QFLASH_OK) return st;
+  g_tmap_key[g_tmap_next] = key;
+  g_tmap_val[g_tmap_next] = *m;
+  g_tmap_next = (g_tmap_next + 1) % kTmapCache;
+  if (g_tmap_n < kTmapCache) ++g_tmap_n;
+  return QFLASH_OK;
+}
+
+qflash_status make_tmap_uncached(CUtensorMap* m, const int8_t* base, int P, int N, int d, int rows,
+                                 int probs) {
   auto enc = get_encode_fn();
   if (!enc) return fail(QFLASH_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(N),
@@ -242,7 +278,7 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
                             const FusedIn* fin, int heads,
                             int32_t* dbg_s = nullptr, int32_t* dbg_p = nullptr,
                             int32_t* dbg_o = nullptr, long long* dbg_t = nullptr,
-                            int32_t* acc_flags = nullptr) {
+                            int32_t* acc_flags = nullptr, int abl_var = 0, float abl_sv = 0.f) {
   const int P = shape->num_problems, N = shape->seq_len, d = shape->head_dim;
   // KV block: with T_c = 1 every B_c >= N gives the same result (one block), so
   // take the smallest supported one; otherwise B_c = block_kv as requested.
@@ -276,7 +312,7 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   const int64_t waves_generic = (tiles_generic + sms - 1) / sms;
   const int64_t waves_packed = (tiles_packed + sms - 1) / sms;
   bool packed;
-  if (acc_flags != nullptr) variant = QFLASH_VARIANT_GENERIC;  // the Eq. 13 ablation: generic tiles
+  if (abl_var != 0) variant = QFLASH_VARIANT_GENERIC;  // ablation variants: generic tiles
   switch (variant) {
     case QFLASH_VARIANT_AUTO:
       // one wave: pack when it saves a wave (A3 b8: 192 -> 148 tiles); several waves:
@@ -313,7 +349,7 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
       if (cfg == 0 && qf::attention_supported(d, bc_eff, nseg, c)) cfg = c;
   }
   if (cfg_env >= 0 && heads == 0 && qf::attention_supported(d, bc_eff, nseg, cfg_env)) cfg = cfg_env;
-  if (acc_flags != nullptr) cfg = 0;
+  if (abl_var != 0) cfg = 0;
   if (!qf::attention_supported(d, bc_eff, nseg, cfg))
     return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "no kernel configuration for d=%d block=%d", d, bc_eff);
   g_last_config = cfg | (nseg << 4);
@@ -330,9 +366,13 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   if (host_prm) args.prm = *host_prm;
   args.dev_prm = dev_prm;
   args.out = o;
-  if (y != nullptr && fin == nullptr) {
+  if (y != nullptr && fin == nullptr && abl_var == 0) {
     args.out_f32 = y;
     args.dq_table = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(dev_prm) + 4096);
+  }
+  if (abl_var >= 2) {  // V3 / V2 ablations: fp32 y = s_V O / l written by the epilogue
+    args.out_f32 = y;
+    args.s_v = abl_sv;
   }
   if (fin != nullptr) {  // fused step: the kernel quantizes fin->x into q/k/v itself
     args.out_f32 = y;
@@ -354,6 +394,7 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
     args.numel = static_cast<int64_t>(P) * N * d;
   }
   args.acc_flags = acc_flags;
+  args.variant = abl_var;
   args.dbg_s = dbg_s;
   args.dbg_p = dbg_p;
   args.dbg_o = dbg_o;
@@ -362,8 +403,8 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   args.Tr = static_cast<int32_t>(Tr);
   const bool dbg = dbg_s != nullptr || dbg_p != nullptr || dbg_o != nullptr || dbg_t != nullptr;
   cudaError_t e;
-  if (acc_flags != nullptr) {
-    e = qf::launch_attention_acc(d, bc_eff, tq, tk, tv, args, tiles, sms, stream);
+  if (abl_var != 0) {
+    e = qf::launch_attention_var(abl_var, d, bc_eff, tq, tk, tv, args, tiles, sms, stream);
   } else if (heads > 0) {  // per-head constants (configuration 0)
     args.head_prm = reinterpret_cast<const qf::IntParams*>(reinterpret_cast<const char*>(dev_prm) +
                                                           qf::kHeadPrmOffset);
@@ -654,7 +695,39 @@ qflash_status qflash_attention_int8_accum(const int8_t* q, const int8_t* k, cons
   cudaError_t e = cudaMemsetAsync(flags_dev, 0, 4, s);
   if (e != cudaSuccess) return cuda_fail(e, "flags reset");
   return launch_common(q, k, v, shape, bc, QFLASH_VARIANT_GENERIC, o, &prm, nullptr, s, nullptr, nullptr, 0,
-                       nullptr, nullptr, nullptr, nullptr, flags_dev);
+                       nullptr, nullptr, nullptr, nullptr, flags_dev, 1);
+}
+
+qflash_status qflash_attention_ablation(const int8_t* q, const int8_t* k, const int8_t* v, float s_q,
+                                       float s_k, float s_v, const qflash_attn_shape* shape,
+                                       int32_t variant, float* y, qflash_stream_t stream) {
+  int bc = 0;
+  qflash_status st = validate_shape(shape, &bc);
+  if (st != QFLASH_OK) return st;
+  if (variant != QFLASH_ABLATION_V2 && variant != QFLASH_ABLATION_V3)
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "ablation variant %d not in {2 (V2), 3 (V3)}", variant);
+  if (shape->head_dim == 128) return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "ablations: head_dim 32 or 64");
+  const int N = shape->seq_len;
+  const int bc_eff = N <= bc ? (N <= 64 ? 64 : N <= 128 ? 128 : 256) : bc;
+  if (bc_eff > 128) return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "ablations: block_kv 64 or 128");
+  const int64_t n = static_cast<int64_t>(shape->num_problems) * N * shape->head_dim;
+  if (!q || !k || !v || !y) return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(y))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "q, k, v, y must be 16-byte aligned");
+  const int8_t* yb = reinterpret_cast<const int8_t*>(y);
+  if (overlaps(yb, 4 * n, q, n) || overlaps(yb, 4 * n, k, n) || overlaps(yb, 4 * n, v, n))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "y aliases an input");
+  if (!(s_v > 0.0f) || !std::isfinite(s_v)) return fail(QFLASH_ERR_SCALE_RANGE, "s_v must be positive");
+  qf::IntParams prm;
+  const int rc = qf::derive_core(s_q, s_k, shape->head_dim, &prm, nullptr);
+  if (rc != QFLASH_OK) return fail(static_cast<qflash_status>(rc), "scale out of range");
+  int dev = 0;
+  if ((st = check_device(&dev)) != QFLASH_OK) return st;
+  // internal variant numbering: 2 = V3 (integer exp, FP accumulation), 3 = V2 (FP exp)
+  const int var = variant == QFLASH_ABLATION_V3 ? 2 : 3;
+  return launch_common(q, k, v, shape, bc, QFLASH_VARIANT_GENERIC, nullptr, &prm, nullptr,
+                       reinterpret_cast<cudaStream_t>(stream), y, nullptr, 0, nullptr, nullptr, nullptr,
+                       nullptr, nullptr, var, s_v);
 }
 
 qflash_status qflash_amax_qkv(const float* q, const float* k, const float* v, int64_t numel,

@@ -731,3 +731,23 @@ def test_fused_step_packed_qkv_rejects_bad_heads():
     st = _lib.lib().qflash_forward_fused_qkv(qkv.data_ptr(), 3, shape, 0, None, None, None, None, None,
                                              None, None, None)
     assert st == _lib.QFLASH_ERR_INVALID_ARGUMENT
+
+
+# ------------------------------------------------ ablation steps V3 / V2
+@pytest.mark.parametrize("name,batch", [("A2", 1), ("A7", 8), ("A1", 8)])
+def test_ablation_variants_accuracy(orc, name, batch):
+    # V3 (integer exp, FP accumulation) and V2 (FP exp2 softmax, int8 P V) are not exact:
+    # both must stay in the paper's SQNR regime against FP64 attention, and V3 (same P
+    # bytes as the method, exact fp32 accumulation of exact int32 P V) within a few LSB
+    # of the method's dequantized output
+    from oracle.fp_reference import attention_fp64, sqnr_db
+    q, k, v = gen_workload(name, batch, seed=4)
+    (qq, sq), (kq, sk), (vq, sv) = (orc.quantize(x) for x in (q, k, v))
+    dq, dk, dv = _dev(qq, kq, vq)
+    ref = attention_fp64(q, k, v)
+    v4 = qf.qflash_attention_int8(dq, dk, dv, sq, sk, sv)[0].cpu().numpy().astype(np.float64) * sv
+    y3 = qf.qflash_attention_ablation(dq, dk, dv, sq, sk, sv, "V3").cpu().numpy()
+    y2 = qf.qflash_attention_ablation(dq, dk, dv, sq, sk, sv, "V2").cpu().numpy()
+    s4, s3, s2 = sqnr_db(ref, v4), sqnr_db(ref, y3), sqnr_db(ref, y2)
+    assert s3 >= 29.0 and s2 >= 29.0 and s4 >= 29.0, (s4, s3, s2)
+    assert np.abs(y3 - v4).max() <= 3.0 * sv

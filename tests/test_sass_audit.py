@@ -44,7 +44,11 @@ def test_attention_kernels_integer_only_and_tensor_core():
     # template <D, B_c, NSEG, CS, QT, DBG, FQ, PH, ACC>: DBG = false, FQ = 0 are the
     # integer-only attention kernels (ACC: the Eq. 13 ablation); FQ = 1 adds the Eq. 2 quantizer prologue
     # (fp32 by definition) in front of the same integer code
-    prod = {n: ops for n, ops in funcs.items() if "qflash_attn_kernel" in n and "ELb0ELi0E" in n}
+    # (VAR 2 / 3 are the floating-point ablation steps V3 / V2 of SURVEY 8(f) N4: excluded)
+    prod = {n: ops for n, ops in funcs.items() if "qflash_attn_kernel" in n and "ELb0ELi0E" in n
+            and not re.search(r"ELi[23]EEEv", n)}
+    abl = [n for n in funcs if "qflash_attn_kernel" in n and re.search(r"ELi[23]EEEv", n)]
+    assert len(abl) >= 4, "ablation instantiations"
     fused = [n for n in funcs if "qflash_attn_kernel" in n and "ELb0ELi1E" in n]
     assert len(fused) >= 20
     assert len(prod) >= 20, sorted(funcs)[:10]
