@@ -41,15 +41,18 @@ def _functions():
 
 def test_attention_kernels_integer_only_and_tensor_core():
     funcs = _functions()
-    # template <D, B_c, NSEG, CS, QT, DBG, FQ, PH, ACC>: DBG = false, FQ = 0 are the
-    # integer-only attention kernels (ACC: the Eq. 13 ablation); FQ = 1 adds the Eq. 2 quantizer prologue
-    # (fp32 by definition) in front of the same integer code
-    # (VAR 2 / 3 are the floating-point ablation steps V3 / V2 of SURVEY 8(f) N4: excluded)
-    prod = {n: ops for n, ops in funcs.items() if "qflash_attn_kernel" in n and "ELb0ELi0E" in n
-            and not re.search(r"ELi[23]EEEv", n)}
-    abl = [n for n in funcs if "qflash_attn_kernel" in n and re.search(r"ELi[23]EEEv", n)]
+    # template <D, B_c, NSEG, CS, QT, DBG, FQ, PH, VAR>: DBG = false, FQ = 0 are the
+    # integer-only attention kernels (VAR 1: the Eq. 13 ablation, integer too); FQ = 1 adds
+    # the Eq. 2 quantizer prologue (fp32 by definition) in front of the same integer code;
+    # VAR 2 / 3 are the floating-point ablation steps V3 / V2 of SURVEY 8(f) N4 (excluded)
+    pat = re.compile(r"qflash_attn_kernelILi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELb([01])ELi(\d)"
+                     r"ELb([01])ELi(\d)EEEv")
+    tpl = {n: pat.search(n) for n in funcs if "qflash_attn_kernel" in n}
+    assert all(tpl.values()), [n for n, m in tpl.items() if not m][:3]
+    prod = {n: funcs[n] for n, m in tpl.items() if m.group(6) == "0" and m.group(7) == "0" and m.group(9) in "01"}
+    fused = [n for n, m in tpl.items() if m.group(6) == "0" and m.group(7) == "1"]
+    abl = [n for n, m in tpl.items() if m.group(9) in "23"]
     assert len(abl) >= 4, "ablation instantiations"
-    fused = [n for n in funcs if "qflash_attn_kernel" in n and "ELb0ELi1E" in n]
     assert len(fused) >= 20
     assert len(prod) >= 20, sorted(funcs)[:10]
     for name, ops in prod.items():
