@@ -8,3 +8,4 @@ for wl in A1 A2 A3 A4 A5 A6 A7 SwinB-s1 SwinB-s2 SwinB-s3 SwinB-s4; do
 done
 timeout 200 python bench.py --workload L14 --batch 64 --steps 20 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 > gpurun_out/sweep_L14_b64.json
 timeout 200 python bench.py --workload L14 --batch 64 --steps 20 --warmup 3 --no-cpu-baseline --no-e2e --mode two 2>&1 | tail -1 > gpurun_out/sweep_L14_b64_two.json
+timeout 300 python bench.py 2>&1 | tail -1 > gpurun_out/r2_bench_default_final.json
