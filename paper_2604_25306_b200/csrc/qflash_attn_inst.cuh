@@ -40,11 +40,16 @@ cudaError_t launch_attention_d(int BC, int nseg, int cfg, const CUtensorMap& tq,
   return cudaErrorNotSupported;
 }
 
-// Per-head constants (cfg 0 only): one instantiation per (B_c, NSEG).
+// Per-head constants: cfg 0 (CS = 4 x QT = 1) for every (B_c, NSEG), and cfg 1 (CS = 2 x
+// QT = 2: multi-wave with several KV tiles, e.g. L14) for generic tiles.
 template <int D>
-cudaError_t launch_attention_ph_d(int BC, int nseg, const CUtensorMap& tq, const CUtensorMap& tk,
+cudaError_t launch_attention_ph_d(int BC, int nseg, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
                                   const CUtensorMap& tv, const AttnArgs& args, int64_t tiles,
                                   int sms, cudaStream_t stream) {
+  if (cfg == 1 && nseg == 1) {
+    if (BC == 64) return try_launch<D, 64, 1, 2, 2, false, 0, true>(tq, tk, tv, args, tiles, sms, stream);
+    if (BC == 128) return try_launch<D, 128, 1, 2, 2, false, 0, true>(tq, tk, tv, args, tiles, sms, stream);
+  }
 #define QF_PH(bc, ns)           \
   if (BC == bc && nseg == ns)   \
     return try_launch<D, bc, ns, 4, 1, false, 0, true>(tq, tk, tv, args, tiles, sms, stream);

@@ -188,7 +188,8 @@ struct GroupBars {
   QF_DEV uint64_t* q_full(int b) const { return base + 2 * kMaxStages + b; }
   QF_DEV uint64_t* q_empty(int b) const { return base + 2 * kMaxStages + 2 + b; }
   QF_DEV uint64_t* s_full(int b) const { return base + 2 * kMaxStages + 4 + b; }
-  // p_full(1), alpha_full(b) and rel_full are used by the row-owner roles (CS = 1),
+  // p_full(1) and rel_full are used by the row-owner roles (CS = 1) (alpha_full: slot kept
+  // for the layout; the alpha hand-off uses named barriers),
   // where the softmax warpgroup may run one KV tile ahead of its consumers: the
   // double-buffered barriers (index it & 1, parity (it >> 1) & 1) never overrun.
   QF_DEV uint64_t* p_full(int b = 0) const { return base + 2 * kMaxStages + 4 + NUMS + b; }
@@ -962,9 +963,14 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
 }
 
 // ---------------------------------------------------------------- row-owner roles (CS = 1)
+// Named barriers of the alpha hand-off (softmax warpgroup -> correction warpgroup of
+// group g, double-buffered slot b), 128 + 128 threads each: ids 1..8 (0 = __syncthreads;
+// the column-split configurations use 1..8 for their max exchange instead).
+QF_DEV uint32_t rc_full_bar(int g, int b) { return 1u + 4u * g + b; }
+QF_DEV uint32_t rc_free_bar(int g, int b) { return 3u + 4u * g + b; }
 // Softmax warpgroup: thread = query row, all B_c key columns of every KV tile.
 // No cross-warpgroup max exchange; alpha goes to the correction warpgroup
-// through shared memory (alpha_full barrier), P (packed, contiguous per segment)
+// through shared memory (a pair of named barriers), P (packed, contiguous per segment)
 // over the S buffer once every S chunk of the row has been read.
 template <int D, int BC, int NSEG, int QT, bool FASTQ>
 __device__ __forceinline__ void softmax_rc_role(const AttnArgs& args, const IntParams& prm,
@@ -1019,9 +1025,11 @@ __device__ __forceinline__ void softmax_rc_role(const AttnArgs& args, const IntP
       const int32_t m_new = max(m, tmax);
       // (4) alpha = ShiftExp2(m_old - m_new), handed to the correction warpgroup
       const int32_t alpha = shift_exp2<FASTQ>(m - m_new, prm);
+      // slot it & 1: free once the correction warpgroup read it at iteration it - 2
+      // (named barriers, so that racecheck models both directions of the hand-off)
+      if (it >= 2) named_bar_sync(rc_free_bar(g, it & 1), 256);
       sts32(alpha_buf + static_cast<uint32_t>(((it & 1) * 128 + row) * 4), alpha);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(gb.alpha_full(it & 1));
+      named_bar_arrive(rc_full_bar(g, it & 1), 256);
       // (5)(6) P = Requant(ShiftExp2(S - m_new)), chunk by chunk (S reloaded)
       const uint32_t mu = static_cast<uint32_t>(m_new);
       const uint32_t nmu = static_cast<uint32_t>(-m_new);
@@ -1063,6 +1071,8 @@ __device__ __forceinline__ void softmax_rc_role(const AttnArgs& args, const IntP
     }
     it0 += Tc;
   }
+  // drain: the correction warpgroup's "consumed" arrivals of the last two iterations
+  for (int it = max(it0 - 2, 0); it < it0; ++it) named_bar_sync(rc_free_bar(g, it & 1), 256);
 }
 
 // Correction warpgroup: thread = query row.  Per KV tile j >= 1 it releases the
@@ -1099,8 +1109,9 @@ __device__ __forceinline__ void correction_role(const AttnArgs& args, const IntP
     const bool warp_live = quarter * 32 < ti.rows;
     for (int j = 0; j < Tc; ++j) {
       const int it = it0 + j;
-      corr_wait(gb.alpha_full(it & 1), (it >> 1) & 1);
+      named_bar_sync(rc_full_bar(g, it & 1), 256);  // alpha of iteration it published
       const int32_t alpha = lds32(alpha_buf + static_cast<uint32_t>(((it & 1) * 128 + row) * 4));
+      named_bar_arrive(rc_free_bar(g, it & 1), 256);  // slot it & 1 consumed
       if (j > 0) {
         corr_wait(gb.o_full(), (it - 1) & 1);
         tc_fence_after();
@@ -1500,7 +1511,6 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
       for (int b = 0; b < C::kNumS; ++b) mbar_init(gb.s_full(b), 1);
       for (int b = 0; b < 2; ++b) {
         mbar_init(gb.p_full(b), C::kGroupThreads / 32);
-        mbar_init(gb.alpha_full(b), 4);
       }
       mbar_init(gb.o_full(), 1);
       mbar_init(gb.rel_full(), 4);

@@ -41,7 +41,7 @@ cudaError_t launch_fused_d128(int BC, int nseg, int cfg, const CUtensorMap& tq, 
 cudaError_t launch_attention_var(int var, int D, int BC, const CUtensorMap& tq, const CUtensorMap& tk,
                                  const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
                                  cudaStream_t stream);
-cudaError_t launch_attention_ph(int D, int BC, int nseg, const CUtensorMap& tq,
+cudaError_t launch_attention_ph(int D, int BC, int nseg, int cfg, const CUtensorMap& tq,
                                 const CUtensorMap& tk, const CUtensorMap& tv,
                                 const AttnArgs& args, int64_t tiles, int sms,
                                 cudaStream_t stream);
@@ -348,6 +348,12 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
     for (int c : pref)
       if (cfg == 0 && qf::attention_supported(d, bc_eff, nseg, c)) cfg = c;
   }
+  // per-head constants: cfg 1 for multi-wave generic tiles with several KV tiles (the
+  // row-owner configurations have no per-head instantiation), else cfg 0
+  if (heads > 0 && tiles > sms && nseg == 1 && Tc_host > 1 && bc_eff <= 128 &&
+      qf::attention_supported(d, bc_eff, 1, 1))
+    cfg = 1;
+  if (heads > 0 && cfg_env >= 0) cfg = (cfg_env == 1 && nseg == 1 && bc_eff <= 128) ? 1 : 0;
   if (cfg_env >= 0 && heads == 0 && qf::attention_supported(d, bc_eff, nseg, cfg_env)) cfg = cfg_env;
   if (abl_var != 0) cfg = 0;
   if (!qf::attention_supported(d, bc_eff, nseg, cfg))
@@ -405,12 +411,12 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   cudaError_t e;
   if (abl_var != 0) {
     e = qf::launch_attention_var(abl_var, d, bc_eff, tq, tk, tv, args, tiles, sms, stream);
-  } else if (heads > 0) {  // per-head constants (configuration 0)
+  } else if (heads > 0) {  // per-head constants (configuration 0 or 1)
     args.head_prm = reinterpret_cast<const qf::IntParams*>(reinterpret_cast<const char*>(dev_prm) +
                                                           qf::kHeadPrmOffset);
     args.H = heads;
     args.h_magic = static_cast<uint32_t>(((1ull << 32) + heads - 1) / heads);
-    e = qf::launch_attention_ph(d, bc_eff, nseg, tq, tk, tv, args, tiles, sms, stream);
+    e = qf::launch_attention_ph(d, bc_eff, nseg, cfg, tq, tk, tv, args, tiles, sms, stream);
   } else {
     e = qf::launch_attention(d, bc_eff, nseg, cfg, tq, tk, tv, args, tiles, sms, dbg,
                              fin != nullptr, stream);

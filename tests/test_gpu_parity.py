@@ -751,3 +751,22 @@ def test_ablation_variants_accuracy(orc, name, batch):
     s4, s3, s2 = sqnr_db(ref, v4), sqnr_db(ref, y3), sqnr_db(ref, y2)
     assert s3 >= 29.0 and s2 >= 29.0 and s4 >= 29.0, (s4, s3, s2)
     assert np.abs(y3 - v4).max() <= 3.0 * sv
+
+
+@pytest.mark.parametrize("name,batch,H,cfg", [("L14", 2, 16, 1), ("L14", 2, 16, 0), ("A3", 8, 12, 1)])
+def test_per_head_configurations(orc, name, batch, H, cfg):
+    # the per-head attention in configuration 1 (two query tiles per SM, CS = 2) and 0,
+    # forced, bit-exact to the oracle's per-head composition
+    q, k, v = _head_spread(*gen_workload(name, batch, seed=8), H)
+    dq, dk, dv = _dev(q, k, v)
+    _lib.force_config(cfg)
+    try:
+        y, o, scales, ws = qf.qflash_forward_per_head(dq, dk, dv, H)
+        torch.cuda.synchronize()
+    finally:
+        _lib.force_config(-1)
+    qh, sq = orc.quantize_per_head(q, H)
+    kh, sk = orc.quantize_per_head(k, H)
+    vh, sv = orc.quantize_per_head(v, H)
+    o_ref = orc.attention_per_head(qh, kh, vh, sq, sk, H, nthreads=8)
+    assert np.array_equal(o.cpu().numpy(), o_ref)
