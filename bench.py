@@ -655,6 +655,8 @@ def main():
     if rank == 0:
         step_desc = ("qflash_amax_qkv + NCCL all_reduce(MAX, 3 floats) + qflash_forward_fused_amax"
                      if strong else
+                     "qflash_forward_fused_per_head (CUDA graph, 1 cooperative launch)"
+                     if (launches_per_step == 1 and per_head) else
                      "qflash_forward_fused (CUDA graph, 1 cooperative launch)" if launches_per_step == 1
                      else "per-head quantize + derive + attention + dequantize (CUDA graph)"
                      if per_head else "quantize_qkv_prepare + attention_dequant_prepared (CUDA graph)")

@@ -246,6 +246,23 @@ QFLASH_API qflash_status qflash_attention_int8_accum(const int8_t* q, const int8
                                                      float s_q, float s_k, const qflash_attn_shape* shape,
                                                      int8_t* o, int32_t* flags_dev, qflash_stream_t stream);
 
+/* The whole per-head step in ONE cooperative launch (per-head scales
+ * P:L221): fp32 q, k, v [P, N, d] (head = problem mod heads, heads <= 96,
+ * dividing P) -> per-(tensor, head) quantization in the kernel's prologue -> Algorithm 1
+ * with head h's constants -> y = fl32(s_V[h] O^).  scales_dev: device float[3 heads]
+ * (written: s_q[h], s_k[h], s_v[h]); q_q / k_q / v_q: int8 codes (written); workspace_dev:
+ * QFLASH_PH_FUSED_WORKSPACE_BYTES, ZERO-FILLED before its first use (the kernel keeps its
+ * per-(tensor, head) amax accumulators there and re-zeroes them at the end of every call;
+ * the status of the constant derivation is its first int32, the head table follows at 128).
+ * Bit-identical to qflash_quantize_per_head + qflash_attention_int8_per_head +
+ * qflash_dequantize_per_head.  block_kv <= 128. */
+#define QFLASH_PH_FUSED_WORKSPACE_BYTES 16384
+QFLASH_API qflash_status qflash_forward_fused_per_head(const float* q, const float* k, const float* v,
+                                                       int32_t heads, const qflash_attn_shape* shape,
+                                                       qflash_variant variant, int8_t* q_q, int8_t* k_q,
+                                                       int8_t* v_q, float* y, float* scales_dev,
+                                                       void* workspace_dev, qflash_stream_t stream);
+
 /* Ablation steps of the paper's Table on the same kernel
  * skeleton (int8 Q K^T and int8 P V on tcgen05, generic tiles, configuration 0):
  *   QFLASH_ABLATION_V3: integer ShiftExp2 + requant (the method's P bytes), but O and l

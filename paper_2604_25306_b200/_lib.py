@@ -25,6 +25,7 @@ QFLASH_ERR_UNSUPPORTED_DEVICE = 5
 QFLASH_F32, QFLASH_BF16, QFLASH_F16 = 0, 1, 2
 VARIANTS = {"auto": 0, "generic": 1, "packed": 2}
 DSCALE_WORKSPACE_BYTES = 8192
+PH_FUSED_WORKSPACE_BYTES = 16384
 
 EXPORTED = [
     "qflash_quantize_per_tensor", "qflash_quantize_qkv", "qflash_attention_int8",
@@ -35,7 +36,7 @@ EXPORTED = [
     "qflash_attention_dequant_prepared", "qflash_forward_fused",
     "qflash_quantize_per_head", "qflash_attention_int8_per_head", "qflash_dequantize_per_head",
     "qflash_amax_qkv", "qflash_forward_fused_amax", "qflash_attention_int8_accum",
-    "qflash_forward_fused_qkv", "qflash_attention_ablation",
+    "qflash_forward_fused_qkv", "qflash_attention_ablation", "qflash_forward_fused_per_head",
 ]
 
 
@@ -100,6 +101,9 @@ def lib():
     L.qflash_forward_fused_qkv.restype = st
     L.qflash_forward_fused_qkv.argtypes = [vp, i32, ctypes.POINTER(AttnShape), st, vp, vp, vp, vp, vp, vp,
                                            vp, vp]
+    L.qflash_forward_fused_per_head.restype = st
+    L.qflash_forward_fused_per_head.argtypes = [vp, vp, vp, i32, ctypes.POINTER(AttnShape), st, vp, vp, vp, vp,
+                                                vp, vp, vp]
     L.qflash_attention_ablation.restype = st
     L.qflash_attention_ablation.argtypes = [vp, vp, vp, f32, f32, f32, ctypes.POINTER(AttnShape), i32, vp, vp]
     L.qflash_attention_int8_accum.restype = st

@@ -416,28 +416,66 @@ def qflash_forward_per_head(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, h
     return y, o, scales, ws
 
 
+def qflash_forward_fused_per_head(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, heads: int,
+                                  block_kv: int = 128, variant: str = "auto", out: torch.Tensor | None = None,
+                                  codes=None, scales: torch.Tensor | None = None,
+                                  workspace: torch.Tensor | None = None, stream=None):
+    """The per-head step in ONE cooperative launch: fp32 Q, K, V [P, N, d] (head = problem
+    mod heads) -> per-(tensor, head) quantization -> integer attention -> fp32 y.  Returns
+    (y, scales float32[3 heads], workspace); the workspace must start zero-filled (a fresh
+    one is allocated when None) and is re-zeroed by every call."""
+    _check_qkv(q, k, v, torch.float32)
+    dev = q.device
+    out = torch.empty(q.shape, dtype=torch.float32, device=dev) if out is None else out
+    if codes is None:
+        codes = [torch.empty(q.shape, dtype=torch.int8, device=dev) for _ in range(3)]
+    scales = torch.empty(3 * heads, dtype=torch.float32, device=dev) if scales is None else scales
+    if workspace is None:
+        workspace = torch.zeros(_lib.PH_FUSED_WORKSPACE_BYTES // 4, dtype=torch.int32, device=dev)
+    _check_like(q, out, "out", torch.float32)
+    for i, t in enumerate(codes):
+        _check_like(q, t, "codes[%d]" % i, torch.int8)
+    _check_scales(scales, 3 * heads, dev)
+    _check_buffer(workspace, _lib.PH_FUSED_WORKSPACE_BYTES, "workspace", dev)
+    shape = _shape(q, block_kv)
+    check(lib().qflash_forward_fused_per_head(
+        _dev_ptr(q), _dev_ptr(k), _dev_ptr(v), heads, ctypes.byref(shape), _lib.VARIANTS[variant],
+        _dev_ptr(codes[0]), _dev_ptr(codes[1]), _dev_ptr(codes[2]), _dev_ptr(out), _dev_ptr(scales),
+        _dev_ptr(workspace), _stream(stream)))
+    return out, scales, workspace
+
+
 class QFlashPerHeadPipeline:
     """qflash_forward_per_head with preallocated buffers (graph-capturable): per-head
     quantize (amax + quantize), constant derivation + attention, dequantize."""
 
     def __init__(self, P: int, N: int, d: int, heads: int, block_kv: int = 128, device="cuda",
-                 variant: str = "auto"):
+                 variant: str = "auto", mode: str = "fused"):
+        assert mode in ("fused", "multi")
         dev = torch.device(device)
         self.shape, self.heads, self.block_kv, self.variant = (P, N, d), heads, block_kv, variant
+        self.mode = mode if block_kv <= 128 else "multi"  # the fused per-head step: block_kv <= 128
         self.codes = [torch.empty(self.shape, dtype=torch.int8, device=dev) for _ in range(3)]
         self.scales = torch.empty(3 * heads, dtype=torch.float32, device=dev)
         self.o_q = torch.empty(self.shape, dtype=torch.int8, device=dev)
-        self.workspace = torch.empty(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=dev)
+        # zero-filled: the fused step keeps its per-(tensor, head) amax accumulators here
+        self.workspace = torch.zeros(_lib.PH_FUSED_WORKSPACE_BYTES // 4, dtype=torch.int32, device=dev)
         self.out = torch.empty(self.shape, dtype=torch.float32, device=dev)
 
     def launches(self, dtype=torch.float32) -> int:
-        return 5  # amax, quantize, derive, attention, dequantize
+        # fused: one cooperative launch; multi: amax, quantize, derive, attention, dequantize
+        return 1 if self.mode == "fused" else 5
 
     def __call__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, stream=None):
         P, N, d = self.shape
         H = self.heads
         _check_qkv(q, k, v, torch.float32)
         _check_like(self.out, q, "q")
+        if self.mode == "fused":
+            qflash_forward_fused_per_head(q, k, v, H, self.block_kv, self.variant, out=self.out,
+                                          codes=self.codes, scales=self.scales, workspace=self.workspace,
+                                          stream=stream)
+            return self.out
         c = self.codes
         check(lib().qflash_quantize_per_head(_dev_ptr(q), _dev_ptr(k), _dev_ptr(v), P, N, d, H,
                                              _dev_ptr(c[0]), _dev_ptr(c[1]), _dev_ptr(c[2]),

@@ -12,7 +12,11 @@ template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ, bool PH = f
 cudaError_t try_launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const AttnArgs& args, int64_t tiles, int sms, cudaStream_t stream) {
   if constexpr (config_fits<D, BC, NSEG, CS, QT>()) {
-    return launch_attn_t<D, BC, NSEG, CS, QT, DBG, FQ, PH, VAR>(tq, tk, tv, args, tiles, sms, stream);
+    // the fused per-head step also keeps its head area in shared memory
+    if constexpr (FQ && PH && Cfg<D, BC, NSEG, CS, QT>::kAlloc + kHeadAreaBytes > 227 * 1024)
+      return cudaErrorNotSupported;
+    else
+      return launch_attn_t<D, BC, NSEG, CS, QT, DBG, FQ, PH, VAR>(tq, tk, tv, args, tiles, sms, stream);
   } else {
     return cudaErrorNotSupported;
   }
@@ -68,6 +72,26 @@ cudaError_t launch_attention_var_d(int BC, const CUtensorMap& tq, const CUtensor
                                    cudaStream_t stream) {
   if (BC == 64) return try_launch<D, 64, 1, 4, 1, false, 0, false, VAR>(tq, tk, tv, args, tiles, sms, stream);
   if (BC == 128) return try_launch<D, 128, 1, 4, 1, false, 0, false, VAR>(tq, tk, tv, args, tiles, sms, stream);
+  return cudaErrorNotSupported;
+}
+
+// Fused per-head step (FQ + PH): cfg 0 for every (B_c, NSEG) with B_c <= 128, cfg 1 for
+// generic tiles.
+template <int D>
+cudaError_t launch_fused_ph_d(int BC, int nseg, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
+                              const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
+                              cudaStream_t stream) {
+  if (cfg == 1 && nseg == 1) {
+    if (BC == 64) return try_launch<D, 64, 1, 2, 2, false, 1, true>(tq, tk, tv, args, tiles, sms, stream);
+    if (BC == 128) return try_launch<D, 128, 1, 2, 2, false, 1, true>(tq, tk, tv, args, tiles, sms, stream);
+  }
+#define QF_FPH(bc, ns)          \
+  if (BC == bc && nseg == ns)   \
+    return try_launch<D, bc, ns, 4, 1, false, 1, true>(tq, tk, tv, args, tiles, sms, stream);
+  QF_FPH(64, 1) QF_FPH(128, 1)
+  QF_FPH(64, 2) QF_FPH(128, 2)
+  QF_FPH(64, 4) QF_FPH(128, 4)
+#undef QF_FPH
   return cudaErrorNotSupported;
 }
 

@@ -443,11 +443,14 @@ QF_DEV RowConsts row_consts(const IntParams& prm, int Tc) {
   r.rel_lthr = t < 0 ? -1 : (t > 0x7FFFFFFF ? 0x7FFFFFFF : static_cast<int32_t>(t));
   return r;
 }
-QF_DEV IntParams head_params(const AttnArgs& a, int problem) {
-  // problem / H (H = 1: the 32-bit magic ceil(2^32 / 1) does not exist)
-  const int q = a.H == 1 ? problem : static_cast<int>(__umulhi(static_cast<uint32_t>(problem), a.h_magic));
-  const int h = problem - q * a.H;
-  return *reinterpret_cast<const IntParams*>(reinterpret_cast<const char*>(a.head_prm) + kHeadPrmStride * h);
+QF_DEV int head_of(const AttnArgs& a, uint32_t problem) {
+  // problem mod H (H = 1: the 32-bit magic ceil(2^32 / 1) does not exist)
+  const uint32_t q = a.H == 1 ? problem : __umulhi(problem, a.h_magic);
+  return static_cast<int>(problem - q * static_cast<uint32_t>(a.H));
+}
+QF_DEV IntParams head_params(const AttnArgs& a, const IntParams* table, int problem) {
+  return *reinterpret_cast<const IntParams*>(reinterpret_cast<const char*>(table) +
+                                             kHeadPrmStride * head_of(a, static_cast<uint32_t>(problem)));
 }
 
 // tcgen05.ld of W consecutive 32-bit TMEM columns of this warp's lanes (no wait).
@@ -572,9 +575,9 @@ QF_DEV void p_pack_fp(const uint32_t* sc, int hv, int32_t m_new, float s_f, uint
 // Step (11) for one row's OW output columns [c OW, c OW + OW): O = floor(O / l)
 // saturated to int8 (R14), stored as int8 and/or dequantized fp32 (DQ row) at
 // flattened output row `orow` (row-packed tiles included).
-template <int D, int OW>
+template <int D, int OW, bool FMUL = false>
 QF_DEV void normalize_store(const AttnArgs& args, int64_t orow, int c, const uint32_t* o, uint32_t lraw,
-                            const uint32_t* recip) {
+                            const uint32_t* recip, float sv = 0.f) {
   const Recip rc = make_recip(static_cast<int32_t>(lraw), recip);
   bool bad = false;
   uint32_t w[OW / 4];
@@ -613,18 +616,25 @@ QF_DEV void normalize_store(const AttnArgs& args, int64_t orow, int c, const uin
     for (int e = 0; e < OW / 4; ++e) {
       uint32_t y4[4];
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
-        y4[b] = static_cast<uint32_t>(lds32(dqt + ((((w[e] >> (8 * b)) & 0xFFu) ^ 0x80u) << 2)));
+      for (int b = 0; b < 4; ++b) {
+        if constexpr (FMUL) {  // per-head scales (fused per-head step): y = fl32(s_V[h] x^)
+          const int32_t x = static_cast<int32_t>(static_cast<int8_t>((w[e] >> (8 * b)) & 0xFFu));
+          y4[b] = __float_as_uint(__fmul_rn(sv, static_cast<float>(x)));
+        } else {
+          y4[b] = static_cast<uint32_t>(lds32(dqt + ((((w[e] >> (8 * b)) & 0xFFu) ^ 0x80u) << 2)));
+        }
+      }
       reinterpret_cast<uint4*>(ydst)[e] = make_uint4(y4[0], y4[1], y4[2], y4[3]);
     }
   }
 }
 
-template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FASTQ, bool PH = false, int VAR = 0>
+template <int D, int BC, int NSEG, int CS, int QT, bool DBG, bool FASTQ, bool PH = false, int VAR = 0,
+          int FQ_PH = 0>
 __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntParams& prm_k,
                                              uint32_t tmem_group, GroupBars<Cfg<D, BC, NSEG, CS, QT>::kNumS> gb,
                                              uint32_t red_group, const uint32_t* recip, int g,
-                                             int c, int quarter, int lane) {
+                                             int c, int quarter, int lane, const IntParams* head_tab = nullptr) {
   using C = Cfg<D, BC, NSEG, CS, QT>;
   constexpr int CW = C::kCW;
   constexpr int OW = C::kOW;
@@ -658,7 +668,7 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
     IntParams prm_t;
     RowConsts rct = rck;
     if constexpr (PH) {
-      prm_t = head_params(args, ti.problem + seg);
+      prm_t = head_params(args, head_tab, ti.problem + seg);
       rct = row_consts(prm_t, Tc);
     }
     const IntParams& prm = PH ? prm_t : prm_k;
@@ -952,8 +962,9 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
           if (c == 0) args.dbg_o[row * (D + 1) + D] = static_cast<int32_t>(lraw);
         }
       }
-      if (live) normalize_store<D, OW>(args, static_cast<int64_t>(ti.problem) * N + ti.off + row, c, o,
-                                       lraw, recip);
+      if (live)
+        normalize_store<D, OW, PH && (FQ_PH != 0)>(args, static_cast<int64_t>(ti.problem) * N + ti.off + row, c,
+                                                     o, lraw, recip, __int_as_float(prm.pad[0]));
     }
     if (dbg && ts_warp) QF_TS(101);
     // The O/l loads above completed (wait::ld) before this thread's next p_full
@@ -1463,6 +1474,152 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   QF_FQ_TS_AT(a, 10, 0, 32);
 }
 
+// ---------------------------------------------------------------- fused per-head prologue
+// Q0 with one scale per (tensor, head) for the
+// fused per-head step (FQ + PH): the same grid-stride share as the per-tensor prologue,
+// but each float4's amax goes to its head h = (vector / (N d/4)) mod H through shared-memory
+// atomics, then one global atomicMax per (tensor, head) and CTA; after the grid barrier every
+// CTA reads the 3H maxima, forms s = fl32(amax / 127) (R2, R3), derives the H constant sets
+// (thread h: derive_core, the fp64 expression of qflash_derive_params) into the shared head
+// table and quantizes with its head's scale.  After the second barrier CTA 0 re-zeroes the
+// global accumulators for the next launch (the workspace must be zero before the first one).
+// head area: [table 96 x 80 B][s 3 x 96][1/s 3 x 96][amax bits 3 x 96]
+template <int D>
+__device__ __forceinline__ void fused_quantize_prologue_ph(const AttnArgs& a, IntParams* sprm,
+                                                          uint8_t* head_area) {
+  constexpr int kVR = QF_KVR;
+  IntParams* tab = reinterpret_cast<IntParams*>(head_area);  // stride kHeadPrmStride
+  float* s_h = reinterpret_cast<float*>(head_area + kMaxHeads * kHeadPrmStride);
+  float* r_h = s_h + 3 * kMaxHeads;
+  uint32_t* am_h = reinterpret_cast<uint32_t*>(r_h + 3 * kMaxHeads);
+  __shared__ int ph_fast, ph_status;
+  const int H = a.H;
+  const int ndata_blk = static_cast<int>(blockDim.x) - 32;
+  const bool data_thread = threadIdx.x >= 32;
+  const int64_t nthr = static_cast<int64_t>(gridDim.x) * ndata_blk;
+  const int64_t gtid = data_thread ? static_cast<int64_t>(blockIdx.x) * ndata_blk + threadIdx.x - 32
+                                   : INT64_MAX / 2;
+  const int64_t nvec = a.numel >> 2;
+  const bool resident = nvec <= kVR * nthr;
+  auto head_vec = [&](int64_t i) {  // head of float4 vector i (i < 2^32)
+    const uint64_t p = a.vp_magic == 0 ? static_cast<uint64_t>(i) : __umul64hi(static_cast<uint64_t>(i), a.vp_magic);
+    return head_of(a, static_cast<uint32_t>(p));
+  };
+  for (int j = threadIdx.x; j < 3 * kMaxHeads; j += blockDim.x) am_h[j] = 0u;
+  if (threadIdx.x == 0) {
+    ph_fast = 1;
+    ph_status = 0;
+  }
+  __syncthreads();
+  float4 reg[3][kVR];
+  if (resident) {
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
+#pragma unroll
+      for (int u = 0; u < kVR; ++u) {
+        const int64_t i = gtid + u * nthr;
+        reg[t][u] = i < nvec ? ldg_stream(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+#pragma unroll
+      for (int u = 0; u < kVR; ++u) {
+        const int64_t i = gtid + u * nthr;
+        if (i < nvec) atomicMax(&am_h[t * kMaxHeads + head_vec(i)], __float_as_uint(amax4(0.f, reg[t][u])));
+      }
+  } else {
+    for (int64_t i = gtid; i < nvec; i += nthr) {
+      const int h = head_vec(i);
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+        atomicMax(&am_h[t * kMaxHeads + h],
+                  __float_as_uint(amax4(0.f, __ldg(reinterpret_cast<const float4*>(a.xin[t]) + i))));
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < 3 * H; j += blockDim.x) {
+    const int t = j / H, h = j - t * H;  // (3 H <= 288 entries, once per CTA)
+    const uint32_t v = am_h[t * kMaxHeads + h];
+    if (v != 0u) atomicMax(&a.ph_amax[j], v);
+  }
+  if (a.cluster_grid) cluster_sync_all();
+  else cooperative_groups::this_grid().sync();
+  // scales (every CTA, identical): s = fl32(amax / 127), R3 for an all-zero head
+  for (int j = threadIdx.x; j < 3 * H; j += blockDim.x) {
+    const int t = j / H, h = j - t * H;
+    float sc = __fdiv_rn(__uint_as_float(__ldcg(&a.ph_amax[j])), 127.0f);
+    if (sc == 0.0f) sc = 1.0f / 127.0f;
+    s_h[t * kMaxHeads + h] = sc;
+    r_h[t * kMaxHeads + h] = __frcp_rn(sc);
+    if (blockIdx.x == 0) a.scales_out[j] = sc;  // [3][H]: s_q[h], s_k[h], s_v[h]
+  }
+  __syncthreads();
+  // constants of head h (one thread each, in parallel with the quantization below), s_V in
+  // the spare word pad[0] for the epilogue's y = fl32(s_V[h] x^)
+  if (threadIdx.x < H) {
+    const int h = threadIdx.x;
+    IntParams p;
+    const int st = derive_core(s_h[h], s_h[kMaxHeads + h], D, &p, nullptr);
+    if (st != QFLASH_OK) {
+      memset(&p, 0, sizeof(p));
+      p.status = st;
+      atomicCAS(&ph_status, 0, st);
+    } else if (!(p.q_shift == 0 && static_cast<uint64_t>(p.s_inv) * static_cast<uint64_t>(p.m_p) < (1ull << 32))) {
+      atomicAnd(&ph_fast, 0);
+    }
+    p.pad[0] = __float_as_int(s_h[2 * kMaxHeads + h]);
+    *reinterpret_cast<IntParams*>(reinterpret_cast<char*>(tab) + kHeadPrmStride * h) = p;
+    if (blockIdx.x == 0)
+      *reinterpret_cast<IntParams*>(reinterpret_cast<char*>(a.prm_out) + kHeadPrmOffset + kHeadPrmStride * h) = p;
+  }
+  // quantize this thread's share with its heads' scales
+  if (resident) {
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      uint32_t* dst = reinterpret_cast<uint32_t*>(a.xq[t]);
+#pragma unroll
+      for (int u = 0; u < kVR; ++u) {
+        const int64_t i = gtid + u * nthr;
+        if (i < nvec) {
+          const int h = head_vec(i);
+          dst[i] = quant4(reg[t][u], s_h[t * kMaxHeads + h], r_h[t * kMaxHeads + h]);
+        }
+      }
+    }
+  } else {
+    for (int64_t i = gtid; i < nvec; i += nthr) {
+      const int h = head_vec(i);
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+        reinterpret_cast<uint32_t*>(a.xq[t])[i] =
+            quant4(__ldcg(reinterpret_cast<const float4*>(a.xin[t]) + i), s_h[t * kMaxHeads + h], r_h[t * kMaxHeads + h]);
+    }
+  }
+  __syncthreads();  // the head table and flags are complete
+  if (threadIdx.x == 0) {
+    // header: status, and whether EVERY head takes the fast quotient path (the kernel
+    // picks one softmax instantiation for all heads)
+    IntParams hdr;
+    memset(&hdr, 0, sizeof(hdr));
+    hdr.status = ph_status;
+    hdr.q_shift = ph_fast ? 0 : 1;
+    hdr.s_inv = 1;
+    hdr.m_p = 1;
+    hdr.one = 1;
+    *sprm = hdr;
+    if (blockIdx.x == 0) *a.prm_out = hdr;
+  }
+  fence_proxy_async_global();
+  if (a.cluster_grid) cluster_sync_all();
+  else cooperative_groups::this_grid().sync();
+  fence_proxy_async_global();
+  // every CTA read the accumulators before barrier 2: re-zero them for the next launch
+  if (blockIdx.x == 0)
+    for (int j = threadIdx.x; j < 3 * H; j += blockDim.x) a.ph_amax[j] = 0u;
+}
+
 // ---------------------------------------------------------------- the kernel
 template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ = 0, bool PH = false, int VAR = 0>
 __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
@@ -1538,7 +1695,10 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
   // dependent launch); every global access of this grid comes after the wait.
   griddep_wait();
   IntParams* sprm = reinterpret_cast<IntParams*>(smem + C::kPrm);
-  if constexpr (FQ) {
+  if constexpr (FQ && PH) {
+    fused_quantize_prologue_ph<D>(args, sprm, smem + C::kTotal);
+    __syncthreads();
+  } else if constexpr (FQ) {
     fused_quantize_prologue<D>(args, reinterpret_cast<float*>(smem + C::kScratch), sprm, recip + 1024);
     __syncthreads();
   }
@@ -1734,13 +1894,16 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
       const Bars gb{bars + g * C::kBarsPerGroup};
       const uint32_t red_group = smem_u32(smem + C::kRed) + static_cast<uint32_t>(g * 2 * CS * 128 * 4);
       const uint32_t tG = tmem_base + g * C::kGroupCols;
+      // per-head constants: the fused step derived them into shared memory, else the table
+      // qflash_attention_int8_per_head's derive kernel left in the workspace
+      const IntParams* head_tab = (FQ && PH) ? reinterpret_cast<const IntParams*>(smem + C::kTotal) : args.head_prm;
       // (PH: the header's q_shift / s_inv / m_p encode "every head takes the fast path")
       if (prm.q_shift == 0 && static_cast<uint64_t>(prm.s_inv) * static_cast<uint64_t>(prm.m_p) < (1ull << 32))
-        softmax_role<D, BC, NSEG, CS, QT, DBG, true, PH, VAR>(args, prm, tG, gb, red_group, recip, g, c, warp & 3,
-                                                              lane);
+        softmax_role<D, BC, NSEG, CS, QT, DBG, true, PH, VAR, FQ>(args, prm, tG, gb, red_group, recip, g, c,
+                                                                  warp & 3, lane, head_tab);
       else
-        softmax_role<D, BC, NSEG, CS, QT, DBG, false, PH, VAR>(args, prm, tG, gb, red_group, recip, g, c, warp & 3,
-                                                               lane);
+        softmax_role<D, BC, NSEG, CS, QT, DBG, false, PH, VAR, FQ>(args, prm, tG, gb, red_group, recip, g, c,
+                                                                   warp & 3, lane, head_tab);
       }
     }
   }
@@ -1766,11 +1929,11 @@ template <int D, int BC, int NSEG, int CS, int QT, bool DBG, int FQ = 0, bool PH
 cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                           AttnArgs args, int64_t tiles, int sms, cudaStream_t stream) {
   using C = Cfg<D, BC, NSEG, CS, QT>;
-  static_assert(C::kAlloc <= 227 * 1024, "shared memory budget");
+  static_assert(C::kAlloc + ((FQ && PH) ? kHeadAreaBytes : 0) <= 227 * 1024, "shared memory budget");
   static_assert(!PH || CS > 1, "per-head constants: column-split configurations only");
   static_assert(VAR == 0 || (CS > 1 && NSEG == 1 && !FQ && !PH), "ablation variants: cfg 0/1 generic tiles");
   auto kern = qflash_attn_kernel<D, BC, NSEG, CS, QT, DBG, FQ, PH, VAR>;
-  constexpr int kSmem = C::kAlloc;
+  constexpr int kSmem = C::kAlloc + ((FQ && PH) ? kHeadAreaBytes : 0);
   static int configured[16] = {0};
   int dev = 0;
   cudaGetDevice(&dev);

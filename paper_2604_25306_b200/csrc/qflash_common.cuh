@@ -37,6 +37,12 @@ static_assert(kWsMaxPartialCtas == 320, "partials must end before the dequant ta
 constexpr int kHeadPrmStride = 80;   // bytes per head in the per-head constant table
 constexpr int kHeadPrmOffset = 128;  // table offset in the per-head workspace
 constexpr int kMaxHeads = 96;        // 128 + 96 * 80 <= QFLASH_DSCALE_WORKSPACE_BYTES
+// Fused per-head step workspace (QFLASH_PH_FUSED_WORKSPACE_BYTES = 16384): header at 0,
+// per-head table at kHeadPrmOffset, per-(tensor, head) amax accumulators at 8192.
+constexpr int kWsPhAmaxOffset = 8192;
+// shared-memory head area of the fused per-head kernels: table [96] x 80 B, s[3][96],
+// 1/s[3][96], amax bits[3][96]
+constexpr int kHeadAreaBytes = kMaxHeads * kHeadPrmStride + 3 * 3 * kMaxHeads * 4;
 
 struct AttnArgs {
   int32_t N;        // sequence length
@@ -72,6 +78,10 @@ struct AttnArgs {
   float s_v;                  // V2 / V3 ablations: s_V for the fp32 output y = s_V O / l
   // fused step, packed QKV projection output: xin[0..2] all point at one
   // [P / H, N, 3, H, d] fp32 tensor; qkv_H = H (0: three separate [P, N, d] tensors)
+  // fused per-head step (FQ + PH): per-(tensor, head) amax accumulators
+  // (device uint32 [3][H], zero at launch start; the kernel re-zeroes them at its end)
+  uint32_t* ph_amax;
+  uint64_t vp_magic;          // ceil(2^64 / (N d / 4)): problem of a float4 index
   int32_t qkv_H;
   int32_t pad3;
   uint64_t qkv_n_magic;       // ceil(2^64 / N): floor(x / N) = umul64hi(x, magic), x < 2^32

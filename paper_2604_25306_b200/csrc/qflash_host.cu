@@ -41,6 +41,9 @@ cudaError_t launch_fused_d128(int BC, int nseg, int cfg, const CUtensorMap& tq, 
 cudaError_t launch_attention_var(int var, int D, int BC, const CUtensorMap& tq, const CUtensorMap& tk,
                                  const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
                                  cudaStream_t stream);
+cudaError_t launch_fused_ph(int D, int BC, int nseg, int cfg, const CUtensorMap& tq, const CUtensorMap& tk,
+                            const CUtensorMap& tv, const AttnArgs& args, int64_t tiles, int sms,
+                            cudaStream_t stream);
 cudaError_t launch_attention_ph(int D, int BC, int nseg, int cfg, const CUtensorMap& tq,
                                 const CUtensorMap& tk, const CUtensorMap& tv,
                                 const AttnArgs& args, int64_t tiles, int sms,
@@ -411,6 +414,14 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   cudaError_t e;
   if (abl_var != 0) {
     e = qf::launch_attention_var(abl_var, d, bc_eff, tq, tk, tv, args, tiles, sms, stream);
+  } else if (heads > 0 && fin != nullptr) {  // fused per-head step (one cooperative launch)
+    args.H = heads;
+    args.h_magic = static_cast<uint32_t>(((1ull << 32) + heads - 1) / heads);
+    const uint64_t vpp = static_cast<uint64_t>(N) * d / 4;
+    args.vp_magic = vpp == 1 ? 0ull : ~0ull / vpp + 1ull;  // ceil(2^64 / vpp)
+    args.ph_amax = reinterpret_cast<uint32_t*>(static_cast<char*>(fin->workspace) + qf::kWsPhAmaxOffset);
+    if (bc_eff > 128) return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "fused per-head step: block_kv <= 128");
+    e = qf::launch_fused_ph(d, bc_eff, nseg, cfg, tq, tk, tv, args, tiles, sms, stream);
   } else if (heads > 0) {  // per-head constants (configuration 0 or 1)
     args.head_prm = reinterpret_cast<const qf::IntParams*>(reinterpret_cast<const char*>(dev_prm) +
                                                           qf::kHeadPrmOffset);
@@ -421,6 +432,9 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
     e = qf::launch_attention(d, bc_eff, nseg, cfg, tq, tk, tv, args, tiles, sms, dbg,
                              fin != nullptr, stream);
   }
+  if (e == cudaErrorNotSupported)
+    return fail(QFLASH_ERR_UNSUPPORTED_SHAPE, "no kernel instantiation for d=%d block=%d nseg=%d cfg=%d", d,
+                bc_eff, nseg, cfg);
   if (e != cudaSuccess) return cuda_fail(e, "attention launch");
   return QFLASH_OK;
 }
@@ -675,6 +689,61 @@ qflash_status qflash_forward_fused(const float* q, const float* k, const float* 
                                    qflash_stream_t stream) {
   return qflash_forward_fused_amax(q, k, v, shape, variant, q_q, k_q, v_q, o, y, scales_dev,
                                    workspace_dev, nullptr, stream);
+}
+
+qflash_status qflash_forward_fused_per_head(const float* q, const float* k, const float* v, int32_t heads,
+                                           const qflash_attn_shape* shape, qflash_variant variant,
+                                           int8_t* q_q, int8_t* k_q, int8_t* v_q, float* y,
+                                           float* scales_dev, void* workspace_dev, qflash_stream_t stream) {
+  int bc = 0;
+  qflash_status st = validate_shape(shape, &bc);
+  if (st != QFLASH_OK) return st;
+  if (heads < 1 || heads > qf::kMaxHeads || shape->num_problems % heads != 0)
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "heads must be in [1, %d] and divide num_problems",
+                qf::kMaxHeads);
+  const int64_t n = static_cast<int64_t>(shape->num_problems) * shape->seq_len * shape->head_dim;
+  if (!q || !k || !v || !y || !scales_dev || !workspace_dev || !q_q || !k_q || !v_q)
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(y) || !aligned16(workspace_dev) ||
+      !aligned16(q_q) || !aligned16(k_q) || !aligned16(v_q))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "all buffers must be 16-byte aligned");
+  const void* ins[3] = {q, k, v};
+  const int8_t* codes[3] = {q_q, k_q, v_q};
+  const int8_t* yb = reinterpret_cast<const int8_t*>(y);
+  const int8_t* ws = static_cast<const int8_t*>(workspace_dev);
+  const int8_t* sc = reinterpret_cast<const int8_t*>(scales_dev);
+  for (int i = 0; i < 3; ++i) {
+    if (overlaps(yb, 4 * n, ins[i], 4 * n) || overlaps(yb, 4 * n, codes[i], n))
+      return fail(QFLASH_ERR_INVALID_ARGUMENT, "y aliases a tensor");
+    if (overlaps(ws, QFLASH_PH_FUSED_WORKSPACE_BYTES, ins[i], 4 * n) ||
+        overlaps(ws, QFLASH_PH_FUSED_WORKSPACE_BYTES, codes[i], n) ||
+        overlaps(sc, 12 * heads, ins[i], 4 * n) || overlaps(sc, 12 * heads, codes[i], n))
+      return fail(QFLASH_ERR_INVALID_ARGUMENT, "workspace / scales alias a tensor");
+    for (int j = 0; j < 3; ++j) {
+      if (overlaps(codes[i], n, ins[j], 4 * n))
+        return fail(QFLASH_ERR_INVALID_ARGUMENT, "int8 code buffer %d aliases input %d", i, j);
+      if (j != i && overlaps(codes[i], n, codes[j], n))
+        return fail(QFLASH_ERR_INVALID_ARGUMENT, "int8 code buffers %d and %d alias", i, j);
+    }
+  }
+  if (overlaps(ws, QFLASH_PH_FUSED_WORKSPACE_BYTES, sc, 12 * heads) ||
+      overlaps(ws, QFLASH_PH_FUSED_WORKSPACE_BYTES, yb, 4 * n) || overlaps(sc, 12 * heads, yb, 4 * n))
+    return fail(QFLASH_ERR_INVALID_ARGUMENT, "workspace, scales and y must be disjoint");
+  int dev = 0;
+  if ((st = check_device(&dev)) != QFLASH_OK) return st;
+  FusedIn fin;
+  fin.x[0] = q;
+  fin.x[1] = k;
+  fin.x[2] = v;
+  fin.xq[0] = q_q;
+  fin.xq[1] = k_q;
+  fin.xq[2] = v_q;
+  fin.scales = scales_dev;
+  fin.workspace = workspace_dev;
+  fin.amax_in = nullptr;
+  fin.qkv_heads = 0;
+  return launch_common(q_q, k_q, v_q, shape, bc, variant, nullptr, nullptr, nullptr,
+                       reinterpret_cast<cudaStream_t>(stream), y, &fin, heads);
 }
 
 qflash_status qflash_attention_int8_accum(const int8_t* q, const int8_t* k, const int8_t* v, float s_q,

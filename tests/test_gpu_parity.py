@@ -770,3 +770,37 @@ def test_per_head_configurations(orc, name, batch, H, cfg):
     vh, sv = orc.quantize_per_head(v, H)
     o_ref = orc.attention_per_head(qh, kh, vh, sq, sk, H, nthreads=8)
     assert np.array_equal(o.cpu().numpy(), o_ref)
+
+
+@pytest.mark.parametrize("name,batch,H", [("A1", 1, 3), ("A3", 8, 12), ("A4", 8, 3), ("SwinB-s3", 1, 16),
+                                          ("L14", 2, 16), ("A7", 8, 24)])
+def test_fused_per_head_step_bit_exact(orc, name, batch, H):
+    # the one-launch per-head step: codes, the 3H scales and y bit-exact to the oracle's
+    # per-head composition, also on the second call on the same workspace
+    q, k, v = _head_spread(*gen_workload(name, batch, seed=13), H)
+    dq, dk, dv = _dev(q, k, v)
+    codes = [torch.empty(q.shape, dtype=torch.int8, device="cuda") for _ in range(3)]
+    ws = torch.zeros(_lib.PH_FUSED_WORKSPACE_BYTES // 4, dtype=torch.int32, device="cuda")
+    qh, sq = orc.quantize_per_head(q, H)
+    kh, sk = orc.quantize_per_head(k, H)
+    vh, sv = orc.quantize_per_head(v, H)
+    ref = orc.dequantize_per_head(orc.attention_per_head(qh, kh, vh, sq, sk, H, nthreads=8), sv, H)
+    # call 1 on 4 Q (larger amax), call 2 on Q: stale accumulators would keep 4 amax(Q)
+    for rep, x in enumerate((dq * 4.0, dq)):
+        y, sc, ws = qf.qflash_forward_fused_per_head(x, dk, dv, H, codes=codes, workspace=ws)
+        torch.cuda.synchronize()
+        assert int(ws[0].item()) == 0
+    assert np.array_equal(sc.cpu().numpy(), np.concatenate([sq, sk, sv]))
+    for t, c in enumerate((qh, kh, vh)):
+        assert np.array_equal(codes[t].cpu().numpy(), c)
+    assert np.array_equal(y.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    assert not ws[8192 // 4: 8192 // 4 + 3 * H].any()  # re-zeroed for the next call
+
+
+def test_fused_per_head_one_head_equals_per_tensor():
+    q, k, v = gen_workload("A2", 1, seed=4)
+    dq, dk, dv = _dev(q, k, v)
+    y, _, _ = qf.qflash_forward_fused_per_head(dq, dk, dv, 1)
+    y_t = qf.qflash_forward(dq, dk, dv)
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(torch.int32), y_t.view(torch.int32))
