@@ -303,6 +303,39 @@ def capture(fn, stream):
     return g
 
 
+def table1_sweep(qfl, dev, stream, reps=400):
+    """SURVEY 8(d) metric set in the driver's run: every Table 1 workload (A1-A7)
+    at batch 1 and 8 -- the fused one-launch step and the integer attention alone on the
+    int8 codes, each CUDA-graph-replayed over rotating input sets that exceed 2x L2 (cold)."""
+    import torch
+    from paper_2604_25306_b200.inputs import gen_real_qkv_slab
+    out = {}
+    for name in ("A1", "A2", "A3", "A4", "A5", "A6", "A7"):
+        w = CATALOG[name]
+        for batch in (1, 8):
+            P, N, d = w.problems(batch), w.seq_len, w.head_dim
+            alg = algorithmic(P, N, d)
+            n_sets = int(min(64, max(2, np.ceil(2.0 * L2_BYTES / alg["step_bytes"]) + 1)))
+            q0, k0, v0 = gen_real_qkv_slab(P, N, d, 0, P, seed=0, family=w.family)
+            base = [torch.from_numpy(a).to(dev) for a in (q0, k0, v0)]
+            sets = [[(t * (-1.0 if i % 2 else 1.0)).roll(shifts=i, dims=1).contiguous() for t in base]
+                    for i in range(n_sets)]
+            pipes = [qfl.QFlashPipeline(P, N, d, device=dev) for _ in range(n_sets)]
+            g_step = [capture(lambda p=p, s=s: p(*s, stream=stream), stream) for p, s in zip(pipes, sets)]
+            t_step = graph_time(g_step, stream, reps)
+            g_att = [capture(lambda p=p: qfl.qflash_attention_int8_prepared(
+                p.qkv_q[0], p.qkv_q[1], p.qkv_q[2], p.workspace, out=p.o_q, stream=stream), stream)
+                for p in pipes]
+            t_att = graph_time(g_att, stream, reps)
+            out[f"{name} b{batch}"] = {
+                "problems": P, "seq_len": N, "head_dim": d,
+                "step_us": t_step * 1e3, "step_tops": alg["int8_ops"] / (t_step * 1e-3) / 1e12,
+                "attention_int8_us": t_att * 1e3,
+                "attention_int8_tops": alg["int8_ops"] / (t_att * 1e-3) / 1e12}
+            del g_step, g_att, pipes, sets, base
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -320,6 +353,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the per-stage timing set")
+    ap.add_argument("--no-table1", action="store_true",
+                    help="skip the A1-A7 batch 1/8 table (default run only: world 1, default workload)")
     ap.add_argument("--mode", default="fused", choices=["fused", "two", "three"],
                     help="step form: one cooperative launch (default), or 2 / 3 launches")
     ap.add_argument("--variant", default="auto", choices=["auto", "generic", "packed"],
@@ -651,6 +686,9 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(name, batch, w, args.block_kv)
+    table1 = None
+    if world == 1 and args.workload is None and not args.no_table1 and args.scales == "per-tensor":
+        table1 = table1_sweep(qfl, dev, stream)
 
     if rank == 0:
         step_desc = ("qflash_amax_qkv + NCCL all_reduce(MAX, 3 floats) + qflash_forward_fused_amax"
@@ -678,6 +716,7 @@ def main():
             "rank_ms_per_step": rank_ms,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks, "roofline": roofline, "stages": extra, "cpu_baseline": cpu, "e2e": e2e,
+            "table1": table1,
             "verify": verify,
         }
         print(json.dumps(line))

@@ -1339,16 +1339,20 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   } else {
     auto stream_amax = [&](auto packed) {
       constexpr bool PK = decltype(packed)::value;
-      for (int64_t i = gtid; i < nvec; i += 2 * nthr) {  // 6 16-B loads in flight
-        float4 v[3][2];
+      for (int64_t i = gtid; i < nvec; i += kVR * nthr) {  // 3 kVR 16-B loads in flight
+        float4 v[3][kVR];
 #pragma unroll
-        for (int t = 0; t < 3; ++t) {
-          const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
-          v[t][0] = __ldg(src + qkv_src_vec<D, PK>(a, t, i));
-          v[t][1] = i + nthr < nvec ? __ldg(src + qkv_src_vec<D, PK>(a, t, i + nthr)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < kVR; ++u) {
+          const int64_t iu = i + u * nthr;
+#pragma unroll
+          for (int t = 0; t < 3; ++t)
+            v[t][u] = iu < nvec ? ldg_stream(reinterpret_cast<const float4*>(a.xin[t]) + qkv_src_vec<D, PK>(a, t, iu))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int t = 0; t < 3; ++t) m[t] = amax4(amax4(m[t], v[t][0]), v[t][1]);
+        for (int t = 0; t < 3; ++t)
+#pragma unroll
+          for (int u = 0; u < kVR; ++u) m[t] = amax4(m[t], v[t][u]);
       }
     };
     if (a.qkv_H == 0) stream_amax(std::false_type{});
@@ -1484,6 +1488,19 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
 // table and quantizes with its head's scale.  After the second barrier CTA 0 re-zeroes the
 // global accumulators for the next launch (the workspace must be zero before the first one).
 // head area: [table 96 x 80 B][s 3 x 96][1/s 3 x 96][amax bits 3 x 96]
+// Shared-memory max of one float4's amax into its head's slot (h < 0: nothing), aggregated
+// over the warp when every lane has the same head (consecutive vectors of one problem): one
+// atomic per warp instead of 32.  Called by all 32 lanes.
+QF_DEV void ph_amax_add(uint32_t* slots, int h, float m) {
+  const int h0 = __shfl_sync(0xffffffffu, h, 0);
+  if (__all_sync(0xffffffffu, h == h0)) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && h0 >= 0) atomicMax(&slots[h0], __float_as_uint(m));
+  } else if (h >= 0) {
+    atomicMax(&slots[h], __float_as_uint(m));
+  }
+}
 template <int D>
 __device__ __forceinline__ void fused_quantize_prologue_ph(const AttnArgs& a, IntParams* sprm,
                                                           uint8_t* head_area) {
@@ -1523,19 +1540,33 @@ __device__ __forceinline__ void fused_quantize_prologue_ph(const AttnArgs& a, In
       }
     }
 #pragma unroll
-    for (int t = 0; t < 3; ++t)
+    for (int u = 0; u < kVR; ++u) {
+      const int64_t i = gtid + u * nthr;
+      const bool ok = i < nvec;
+      const int h = ok ? head_vec(i) : -1;
+#pragma unroll
+      for (int t = 0; t < 3; ++t) ph_amax_add(am_h + t * kMaxHeads, h, ok ? amax4(0.f, reg[t][u]) : 0.f);
+    }
+  } else {
+    // warp-uniform trip count (lanes hold consecutive vectors), so the aggregation's
+    // shuffles see the full warp; kVR steps of all three tensors' loads in flight at once
+    const int lane = threadIdx.x & 31;
+    for (int64_t i0 = gtid; i0 - lane < nvec; i0 += kVR * nthr) {
+      float4 v[3][kVR];
 #pragma unroll
       for (int u = 0; u < kVR; ++u) {
-        const int64_t i = gtid + u * nthr;
-        if (i < nvec) atomicMax(&am_h[t * kMaxHeads + head_vec(i)], __float_as_uint(amax4(0.f, reg[t][u])));
-      }
-  } else {
-    for (int64_t i = gtid; i < nvec; i += nthr) {
-      const int h = head_vec(i);
+        const int64_t i = i0 + u * nthr;
 #pragma unroll
-      for (int t = 0; t < 3; ++t)
-        atomicMax(&am_h[t * kMaxHeads + h],
-                  __float_as_uint(amax4(0.f, __ldg(reinterpret_cast<const float4*>(a.xin[t]) + i))));
+        for (int t = 0; t < 3; ++t)
+          v[t][u] = i < nvec ? __ldg(reinterpret_cast<const float4*>(a.xin[t]) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < kVR; ++u) {
+        const int64_t i = i0 + u * nthr;
+        const int h = i < nvec ? head_vec(i) : -1;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) ph_amax_add(am_h + t * kMaxHeads, h, amax4(0.f, v[t][u]));
+      }
     }
   }
   __syncthreads();
@@ -1589,12 +1620,21 @@ __device__ __forceinline__ void fused_quantize_prologue_ph(const AttnArgs& a, In
       }
     }
   } else {
-    for (int64_t i = gtid; i < nvec; i += nthr) {
-      const int h = head_vec(i);
+    for (int64_t i = gtid; i < nvec; i += 2 * nthr) {  // 6 16-B loads in flight
+      const bool two = i + nthr < nvec;
+      float4 v[3][2];
 #pragma unroll
-      for (int t = 0; t < 3; ++t)
-        reinterpret_cast<uint32_t*>(a.xq[t])[i] =
-            quant4(__ldcg(reinterpret_cast<const float4*>(a.xin[t]) + i), s_h[t * kMaxHeads + h], r_h[t * kMaxHeads + h]);
+      for (int t = 0; t < 3; ++t) {
+        v[t][0] = __ldcg(reinterpret_cast<const float4*>(a.xin[t]) + i);
+        v[t][1] = two ? __ldcg(reinterpret_cast<const float4*>(a.xin[t]) + i + nthr) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      const int h0 = head_vec(i), h1 = two ? head_vec(i + nthr) : 0;
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        uint32_t* dst = reinterpret_cast<uint32_t*>(a.xq[t]);
+        dst[i] = quant4(v[t][0], s_h[t * kMaxHeads + h0], r_h[t * kMaxHeads + h0]);
+        if (two) dst[i + nthr] = quant4(v[t][1], s_h[t * kMaxHeads + h1], r_h[t * kMaxHeads + h1]);
+      }
     }
   }
   __syncthreads();  // the head table and flags are complete
