@@ -1339,20 +1339,16 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   } else {
     auto stream_amax = [&](auto packed) {
       constexpr bool PK = decltype(packed)::value;
-      for (int64_t i = gtid; i < nvec; i += kVR * nthr) {  // 3 kVR 16-B loads in flight
-        float4 v[3][kVR];
+      for (int64_t i = gtid; i < nvec; i += 2 * nthr) {  // 6 16-B loads in flight
+        float4 v[3][2];
 #pragma unroll
-        for (int u = 0; u < kVR; ++u) {
-          const int64_t iu = i + u * nthr;
-#pragma unroll
-          for (int t = 0; t < 3; ++t)
-            v[t][u] = iu < nvec ? ldg_stream(reinterpret_cast<const float4*>(a.xin[t]) + qkv_src_vec<D, PK>(a, t, iu))
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int t = 0; t < 3; ++t) {
+          const float4* src = reinterpret_cast<const float4*>(a.xin[t]);
+          v[t][0] = __ldg(src + qkv_src_vec<D, PK>(a, t, i));
+          v[t][1] = i + nthr < nvec ? __ldg(src + qkv_src_vec<D, PK>(a, t, i + nthr)) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int t = 0; t < 3; ++t)
-#pragma unroll
-          for (int u = 0; u < kVR; ++u) m[t] = amax4(m[t], v[t][u]);
+        for (int t = 0; t < 3; ++t) m[t] = amax4(amax4(m[t], v[t][0]), v[t][1]);
       }
     };
     if (a.qkv_H == 0) stream_amax(std::false_type{});
