@@ -653,6 +653,9 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
   TileIter<NSEG> ti;
   ti.init(args, blockIdx.x + g * gridDim.x);
   int it0 = 0;  // KV iterations of this group so far
+  uint64_t* tables_bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(const_cast<uint32_t*>(recip)) -
+                                                     C::kRecip + C::kTmemSlot + 8);
+  bool tables_ready = false;
   for (; ti.valid(args); ti.next(args)) {
     const bool dbg = dbg_on && ti.i == 0;
     const bool live = row < ti.rows;  // padded rows of the last tile do no work
@@ -911,6 +914,10 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
     mbar_wait(gb.o_full(), itl & 1);
     tc_fence_after();
     if (dbg && ts_warp) QF_TS(100);
+    if (!tables_ready) {  // the step-(11) tables warp 3 loaded (complete long before)
+      mbar_wait(tables_bar, 0);
+      tables_ready = true;
+    }
     if constexpr (VAR >= 2) {
       acc_fold(alpha_prev, alpha_prev_f);
       if (warp_live && live) {  // y = s_V O / l in fp32 (the FP variants' natural output)
@@ -962,9 +969,9 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
           if (c == 0) args.dbg_o[row * (D + 1) + D] = static_cast<int32_t>(lraw);
         }
       }
-      if (live)
-        normalize_store<D, OW, PH && (FQ_PH != 0)>(args, static_cast<int64_t>(ti.problem) * N + ti.off + row, c,
-                                                     o, lraw, recip, __int_as_float(prm.pad[0]));
+      if (live)  // the fused step dequantizes with an FMUL by s_V (per head: s_V[h]) kept in pad[0]
+        normalize_store<D, OW, (FQ_PH != 0)>(args, static_cast<int64_t>(ti.problem) * N + ti.off + row, c,
+                                               o, lraw, recip, __int_as_float(prm.pad[0]));
     }
     if (dbg && ts_warp) QF_TS(101);
     // The O/l loads above completed (wait::ld) before this thread's next p_full
@@ -1112,6 +1119,9 @@ __device__ __forceinline__ void correction_role(const AttnArgs& args, const IntP
     const int64_t t = (static_cast<int64_t>(A) - static_cast<int64_t>(prm.s_inv)) / 384 - 2 * Tc;
     rel_lthr = t < 0 ? -1 : (t > 0x7FFFFFFF ? 0x7FFFFFFF : static_cast<int32_t>(t));
   }
+  uint64_t* tables_bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(const_cast<uint32_t*>(recip)) -
+                                                     C::kRecip + C::kTmemSlot + 8);
+  bool tables_ready = false;
   TileIter<NSEG> ti;
   ti.init(args, blockIdx.x + g * gridDim.x);
   int it0 = 0;
@@ -1174,11 +1184,14 @@ __device__ __forceinline__ void correction_role(const AttnArgs& args, const IntP
     // (11) O_i = floor(O / l), saturated (R14), stores
     mbar_wait(gb.o_full(), (it0 + Tc - 1) & 1);
     tc_fence_after();
+    if (!tables_ready) {
+      mbar_wait(tables_bar, 0);
+      tables_ready = true;
+    }
     if (warp_live) {
       uint32_t lraw;
       tmem_ld1(tO + D, lraw);
       tmem_wait_ld();
-      const Recip rc = make_recip(static_cast<int32_t>(lraw), recip);
       const int64_t orow = static_cast<int64_t>(ti.problem) * N + ti.off + row;
 #pragma unroll
       for (int h = 0; h < D / OH; ++h) {
@@ -1186,42 +1199,7 @@ __device__ __forceinline__ void correction_role(const AttnArgs& args, const IntP
         if constexpr (OH == 32) tmem_ld32(tO + OH * h, *reinterpret_cast<uint32_t(*)[32]>(o));
         else tmem_ld<OH>(tO + OH * h, o);
         tmem_wait_ld();
-        if (live) {
-          bool bad = false;
-          uint32_t w[OH / 4];
-#pragma unroll
-          for (int e = 0; e < OH; e += 4)
-            w[e / 4] = pack4_sat_s8(floor_div(static_cast<int32_t>(o[e]), rc, bad),
-                                    floor_div(static_cast<int32_t>(o[e + 1]), rc, bad),
-                                    floor_div(static_cast<int32_t>(o[e + 2]), rc, bad),
-                                    floor_div(static_cast<int32_t>(o[e + 3]), rc, bad));
-          if (bad) {
-#pragma unroll
-            for (int e = 0; e < OH; e += 4)
-              w[e / 4] = pack4_sat_s8(floor_div_exact(static_cast<int32_t>(o[e]), rc.l),
-                                      floor_div_exact(static_cast<int32_t>(o[e + 1]), rc.l),
-                                      floor_div_exact(static_cast<int32_t>(o[e + 2]), rc.l),
-                                      floor_div_exact(static_cast<int32_t>(o[e + 3]), rc.l));
-          }
-          if (args.out != nullptr) {
-            int8_t* dst = args.out + orow * D + OH * h;
-#pragma unroll
-            for (int e = 0; e < OH / 16; ++e)
-              reinterpret_cast<uint4*>(dst)[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
-          }
-          if (args.out_f32 != nullptr) {
-            const uint32_t dqt = smem_u32(recip + 1024);
-            uint32_t* ydst = reinterpret_cast<uint32_t*>(args.out_f32 + orow * D + OH * h);
-#pragma unroll
-            for (int e = 0; e < OH / 4; ++e) {
-              uint32_t y4[4];
-#pragma unroll
-              for (int b = 0; b < 4; ++b)
-                y4[b] = static_cast<uint32_t>(lds32(dqt + ((((w[e] >> (8 * b)) & 0xFFu) ^ 0x80u) << 2)));
-              reinterpret_cast<uint4*>(ydst)[e] = make_uint4(y4[0], y4[1], y4[2], y4[3]);
-            }
-          }
-        }
+        if (live) normalize_store<D, OH, (FQ != 0)>(args, orow, h, o, lraw, recip, __int_as_float(prm.pad[0]));
       }
     }
     it0 += Tc;
@@ -1411,6 +1389,7 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
       memset(&p, 0, sizeof(p));
       p.status = st;
     }
+    p.pad[0] = __float_as_int(s3[2]);  // s_V for the epilogue's y = fl32(s_V O^)
     *sprm = p;
     QF_FQ_TS(a, 3);
     if (blockIdx.x == 0) {
@@ -1709,15 +1688,13 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
       mbar_init(gb.rel_full(), 4);
       mbar_init(gb.s_empty(), C::kGroupThreads / 32);
     }
+    mbar_init(reinterpret_cast<uint64_t*>(smem + C::kTmemSlot + 8), 1);  // step-(11) tables loaded
     fence_barrier_init();
   }
   if (warp == 2) {
     tmem_alloc(tmem_slot, kTmemCols);
     tmem_relinquish();
   }
-  // reciprocal table of step (11) (a constant: loaded before the grid dependency wait)
-  for (int i = threadIdx.x; i < 256; i += C::kThreads)
-    reinterpret_cast<uint4*>(recip)[i] = reinterpret_cast<const uint4*>(g_recip.v)[i];
   // ones block of the extended V operand (any layout: every byte is 1)
   for (int i = threadIdx.x; i < BC * D / 16; i += C::kThreads)
     reinterpret_cast<uint4*>(sOnes)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
@@ -1738,15 +1715,6 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
     fused_quantize_prologue<D>(args, reinterpret_cast<float*>(smem + C::kScratch), sprm, recip + 1024);
     __syncthreads();
   }
-  if constexpr (!FQ && VAR < 2) {
-    if (args.out_f32 != nullptr) {  // fused dequantization table (256 fp32 bit patterns)
-      if (threadIdx.x < 64)
-        reinterpret_cast<uint4*>(recip + 1024)[threadIdx.x] = reinterpret_cast<const uint4*>(args.dq_table)[threadIdx.x];
-      __syncthreads();
-    }
-  }
-  // (the fused step's prologue built the dequant table before its final __syncthreads:
-  // every table the epilogue reads is in shared memory before the roles start)
   const IntParams* dprm = FQ ? sprm : args.dev_prm;  // constants in memory, or nullptr (by value)
 
   if (warp < 2) {
@@ -1820,6 +1788,21 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
     if (warp < 2) {
       // (producer role above)
     } else if (warp < 4) {
+      if (warp == 3) {
+        // tables of step (11) -> shared memory, off the critical path (the epilogue waits
+        // on the tables mbarrier, long complete by then): the reciprocal table, and for
+        // the two-launch form's fused dequantization the quantizer's 256 fp32 patterns
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          reinterpret_cast<uint4*>(recip)[lane + 32 * k] = reinterpret_cast<const uint4*>(g_recip.v)[lane + 32 * k];
+        if (!FQ && VAR < 2 && args.out_f32 != nullptr) {
+          const uint4* src = reinterpret_cast<const uint4*>(args.dq_table);
+          reinterpret_cast<uint4*>(recip + 1024)[lane] = src[lane];
+          reinterpret_cast<uint4*>(recip + 1024)[lane + 32] = src[lane + 32];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(reinterpret_cast<uint64_t*>(smem + C::kTmemSlot + 8));
+      }
       // ========================================================= MMA issuer of group `warp - 2`
       // Issue order within a tile (tcgen05.mma of one thread execute in order,
       // which also orders every TMEM WAR hazard between P V and a later Q K^T):
