@@ -4,8 +4,10 @@
 A "step" is one pass of the whole hot path over one batch of synthetic input
 (SURVEY 8(a)): fused per-tensor quantization of fp32 Q, K, V (Eq. 2) -> the
 integer-only fused attention kernel (Algorithm 1, device-derived constants) ->
-dequantization of O (s_O = s_V).  Four of libqflash.so's kernels per step,
-replayed as one CUDA graph per input set.
+dequantization of O (s_O = s_V): ONE cooperative launch of libqflash.so's fused
+step kernel.  The rotating input sets' steps are captured back to back into one
+CUDA graph (a graph-captured model forward's launch pattern); --graph-steps 1
+replays one graph per step, and the line also reports that per-step figure.
 
 Default workload: BASELINE.json configs[1], ViT-Base attention at batch 8
 (P = 96 problems, N = 197, d = 64).  Inputs are fp32 resident in HBM; the
@@ -292,6 +294,13 @@ def graph_time(graphs, stream, reps, warm=3):
     return e0.elapsed_time(e1) / reps
 
 
+def chain_time(fns, stream, steps):
+    """ms per step of the callables `fns` captured back to back into ONE CUDA graph
+    (one replay = len(fns) steps), replayed for about `steps` steps."""
+    g = capture(lambda: [f() for f in fns], stream)
+    return graph_time([g], stream, max(1, steps // len(fns))) / len(fns)
+
+
 def capture(fn, stream):
     import torch
     with torch.cuda.stream(stream):
@@ -321,12 +330,12 @@ def table1_sweep(qfl, dev, stream, reps=400):
             sets = [[(t * (-1.0 if i % 2 else 1.0)).roll(shifts=i, dims=1).contiguous() for t in base]
                     for i in range(n_sets)]
             pipes = [qfl.QFlashPipeline(P, N, d, device=dev) for _ in range(n_sets)]
-            g_step = [capture(lambda p=p, s=s: p(*s, stream=stream), stream) for p, s in zip(pipes, sets)]
-            t_step = graph_time(g_step, stream, reps)
-            g_att = [capture(lambda p=p: qfl.qflash_attention_int8_prepared(
-                p.qkv_q[0], p.qkv_q[1], p.qkv_q[2], p.workspace, out=p.o_q, stream=stream), stream)
-                for p in pipes]
-            t_att = graph_time(g_att, stream, reps)
+            # one graph per n_sets consecutive steps (each on its own cold set), as the main line
+            g_step = capture(lambda: [p(*s, stream=stream) for p, s in zip(pipes, sets)], stream)
+            t_step = graph_time([g_step], stream, max(1, reps // n_sets)) / n_sets
+            g_att = capture(lambda: [qfl.qflash_attention_int8_prepared(
+                p.qkv_q[0], p.qkv_q[1], p.qkv_q[2], p.workspace, out=p.o_q, stream=stream) for p in pipes], stream)
+            t_att = graph_time([g_att], stream, max(1, reps // n_sets)) / n_sets
             out[f"{name} b{batch}"] = {
                 "problems": P, "seq_len": N, "head_dim": d,
                 "step_us": t_step * 1e3, "step_tops": alg["int8_ops"] / (t_step * 1e-3) / 1e12,
@@ -350,6 +359,8 @@ def main():
                          "scales, no collective; strong: ONE batch partitioned over the ranks, global "
                          "per-tensor scales via a MAX all-reduce of the amax every step")
     ap.add_argument("--ref-problems", type=int, default=0)
+    ap.add_argument("--graph-steps", default="sets", choices=["sets", "1"],
+                    help="steps per CUDA graph replay: all rotating input sets (default) or 1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the per-stage timing set")
@@ -441,6 +452,7 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     amax_bufs = [torch.zeros(3, dtype=torch.float32, device=dev) for _ in range(n_sets)]
 
+    chain = None
     if strong:
         # per step: local amax (graph) -> NCCL MAX all-reduce of 3 floats (eager, on the
         # stream) -> fused step with the global amax (graph)
@@ -458,9 +470,25 @@ def main():
         launches_per_step = 2
     else:
         graphs = [capture(lambda p=p, s=s: p(*s, stream=stream), stream) for p, s in zip(pipes, sets)]
+        # one CUDA graph holding the n_sets consecutive steps (every step its own cold
+        # input set), as a graph-captured model forward launches them: the per-graph
+        # launch cost (~2.5 us) is paid once per n_sets steps; --graph-steps 1 times one
+        # graph launch per step
+        chain = None
+        if args.graph_steps != "1":
+            chain = capture(lambda: [p(*s, stream=stream) for p, s in zip(pipes, sets)], stream)
 
         def run_step(i):
             graphs[i % n_sets].replay()
+
+        def run_steps(k):  # k consecutive steps starting at set 0
+            done = 0
+            if chain is not None:
+                while k - done >= n_sets:
+                    chain.replay()
+                    done += n_sets
+            for i in range(done, k):
+                run_step(i)
         launches_per_step = pipes[0].launches()
     torch.cuda.synchronize()
     status = int(pipes[0].workspace[0].item())
@@ -469,9 +497,12 @@ def main():
 
     sampler = ClockSampler(local)
     sampler.start()
+    if strong:
+        def run_steps(k):
+            for i in range(k):
+                run_step(i)
     with torch.cuda.stream(stream):
-        for i in range(args.warmup):
-            run_step(i)
+        run_steps(args.warmup)
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, barrier + sync on both sides, device events
@@ -483,8 +514,7 @@ def main():
     with torch.cuda.stream(stream):
         torch.cuda._sleep(2_000_000)  # host head start so graph replays queue back to back
         ev0.record(stream)
-        for i in range(args.steps):
-            run_step(i)
+        run_steps(args.steps)
         ev1.record(stream)
     torch.cuda.synchronize()
     t_host1 = time.perf_counter()
@@ -507,8 +537,10 @@ def main():
     one_launch = (not strong) and launches_per_step == 1
     per_head = args.scales == "per-head"
     k_launch = min(args.steps, 2000)
+    graphs_per_replay = 1
     if one_launch:
-        kgraphs = graphs
+        kgraphs = graphs if chain is None else [chain]
+        graphs_per_replay = 1 if chain is None else n_sets
         kname = "qflash_attn_kernel<FQ> (fused step: quantize prologue + attention + dequantize)"
     elif strong:
         kgraphs = g_step
@@ -521,25 +553,27 @@ def main():
             p.qkv_q[0], p.qkv_q[1], p.qkv_q[2], p.workspace, args.block_kv, args.variant,
             out=p.out, stream=stream), stream) for p in pipes]
         kname = "qflash_attn_kernel (fused dequantize epilogue)"
-    attn_ms = graph_time(kgraphs, stream, k_launch)
+    attn_ms = graph_time(kgraphs, stream, max(1, k_launch // graphs_per_replay)) / graphs_per_replay
     attn_share = attn_ms / ms_per_step
+    # the same step with one graph launch per step (the launch cost included)
+    step_graph1_ms = graph_time(graphs, stream, k_launch) if (not strong and chain is not None) else None
 
     # ---- the per-stage timing set: attention alone on int8 inputs,
     # the quantizer and the dequantizer alone (graphs, cold sets), single-call latency
     extra = None
     if not args.no_extra and not per_head:
         p0 = pipes[0]
-        q_prep = [capture(lambda p=p, s=s: qfl.qflash_quantize_qkv_prepare(
-            *s, outs=p.qkv_q, scales=p.scales, workspace=p.workspace, stream=stream), stream)
+        q_prep = [lambda p=p, s=s: qfl.qflash_quantize_qkv_prepare(
+            *s, outs=p.qkv_q, scales=p.scales, workspace=p.workspace, stream=stream)
             for p, s in zip(pipes, sets)]
-        a_int8 = [capture(lambda p=p: qfl.qflash_attention_int8_prepared(
+        a_int8 = [lambda p=p: qfl.qflash_attention_int8_prepared(
             p.qkv_q[0], p.qkv_q[1], p.qkv_q[2], p.workspace, args.block_kv, args.variant,
-            out=p.o_q, stream=stream), stream) for p in pipes]
-        dq = [capture(lambda p=p: qfl.qflash_dequantize(p.o_q, p.scales[2:3], out=p.out, stream=stream),
-                      stream) for p in pipes]
-        t_q = graph_time(q_prep, stream, k_launch)
-        t_a = graph_time(a_int8, stream, k_launch)
-        t_d = graph_time(dq, stream, k_launch)
+            out=p.o_q, stream=stream) for p in pipes]
+        dq = [lambda p=p: qfl.qflash_dequantize(p.o_q, p.scales[2:3], out=p.out, stream=stream)
+              for p in pipes]
+        t_q = chain_time(q_prep, stream, k_launch)
+        t_a = chain_time(a_int8, stream, k_launch)
+        t_d = chain_time(dq, stream, k_launch)
         # single call, host wall clock around one synchronized eager step (launch included)
         lat = []
         for i in range(20):
@@ -557,7 +591,7 @@ def main():
             "dequantize_us": t_d * 1e3,
             "dequantize_gbs": E * 5 / (t_d * 1e-3) / 1e9,
             "single_call_wall_us": statistics.median(lat) * 1e6,
-            "note": "CUDA-graph replays over the rotating cold sets; attention on the int8 codes "
+            "note": "CUDA graphs of the n_sets consecutive calls over the rotating cold sets; attention on the int8 codes "
                     "(qflash_attention_int8_prepared), quantizer = qflash_quantize_qkv_prepare "
                     "(bytes 3 E (4 + 1)), dequantizer bytes E (1 + 4); single call = host wall "
                     "clock of one synchronized eager fused step",
@@ -712,7 +746,10 @@ def main():
                                        + (", global scales via all_reduce" if strong else
                                           ", per-slab scales, no collective" if world > 1 else "")),
                        "step": step_desc, "scales": args.scales,
-                       "l2": f"rotating {n_sets} input sets ({n_sets * set_bytes / 2**20:.0f} MiB > 2x L2)"},
+                       "l2": f"rotating {n_sets} input sets ({n_sets * set_bytes / 2**20:.0f} MiB > 2x L2)",
+                       "graph": (f"{n_sets} consecutive steps (one per input set) per CUDA graph replay"
+                                 if (not strong and chain is not None) else "one CUDA graph replay per step")},
+            "us_per_call_graph_per_step": (step_graph1_ms * 1e3 if step_graph1_ms is not None else None),
             "rank_ms_per_step": rank_ms,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks, "roofline": roofline, "stages": extra, "cpu_baseline": cpu, "e2e": e2e,

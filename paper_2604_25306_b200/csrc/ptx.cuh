@@ -159,6 +159,26 @@ QF_DEV float4 ldg_stream(const float4* p) {
                : "l"(p));
   return v;
 }
+// L2 evict-first policy (createpolicy): data touched once -- the fp32 inputs of the fused
+// step and its fp32 output -- is chosen first for L2 eviction, so streaming it does not push
+// the kernel's code, the int8 codes and the workspace out of the 126 MB L2.
+QF_DEV uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+QF_DEV float4 ldg_stream_ef(const float4* p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+QF_DEV void stg_ef(uint4* p, const uint4& v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
 // Generic-proxy global writes of this thread ordered with async-proxy (TMA) accesses.
 QF_DEV void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");

@@ -88,6 +88,9 @@ constexpr int kBlockR = 128;
 #ifndef QF_SLEEP_PROD
 #define QF_SLEEP_PROD 0  // > 0: producers poll with test_wait + nanosleep(ns) instead of a suspended try_wait
 #endif
+#ifndef QF_EVICT_FIRST
+#define QF_EVICT_FIRST 0  // 1: L2 evict-first policy on the fused step's fp32 input loads / output stores
+#endif
 #ifndef QF_SLEEP_SOFT
 #define QF_SLEEP_SOFT 0
 #endif
@@ -611,6 +614,7 @@ QF_DEV void normalize_store(const AttnArgs& args, int64_t orow, int c, const uin
     // the same IEEE multiply as qflash_dequantize -- the attention kernel itself
     // stays integer-only.
     const uint32_t dqt = smem_u32(recip + 1024);
+    const uint64_t ypol = QF_EVICT_FIRST ? l2_evict_first_policy() : 0ull;  // y is written once
     uint32_t* ydst = reinterpret_cast<uint32_t*>(args.out_f32 + orow * D + c * OW);
 #pragma unroll
     for (int e = 0; e < OW / 4; ++e) {
@@ -624,7 +628,8 @@ QF_DEV void normalize_store(const AttnArgs& args, int64_t orow, int c, const uin
           y4[b] = static_cast<uint32_t>(lds32(dqt + ((((w[e] >> (8 * b)) & 0xFFu) ^ 0x80u) << 2)));
         }
       }
-      reinterpret_cast<uint4*>(ydst)[e] = make_uint4(y4[0], y4[1], y4[2], y4[3]);
+      if (QF_EVICT_FIRST) stg_ef(reinterpret_cast<uint4*>(ydst) + e, make_uint4(y4[0], y4[1], y4[2], y4[3]), ypol);
+      else reinterpret_cast<uint4*>(ydst)[e] = make_uint4(y4[0], y4[1], y4[2], y4[3]);
     }
   }
 }
@@ -918,6 +923,7 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
       mbar_wait(tables_bar, 0);
       tables_ready = true;
     }
+    if (dbg && ts_warp) QF_TS(103);
     if constexpr (VAR >= 2) {
       acc_fold(alpha_prev, alpha_prev_f);
       if (warp_live && live) {  // y = s_V O / l in fp32 (the FP variants' natural output)
@@ -963,6 +969,7 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
       else if constexpr (OW == 16) tmem_ld16(tO + c * OW, o);
       else tmem_ld<OW>(tO + c * OW, o);
       tmem_wait_ld();
+      if (dbg && ts_warp) QF_TS(104);
       if constexpr (DBG) {
         if (args.dbg_o != nullptr && dbg) {
           for (int e = 0; e < OW; ++e) args.dbg_o[row * (D + 1) + c * OW + e] = static_cast<int32_t>(o[e]);
@@ -1249,20 +1256,26 @@ QF_DEV int64_t qkv_src_vec(const AttnArgs& a, int t, int64_t i) {
 }
 
 // Quantize one float4 (4 elements) -> 4 packed int8 codes (exact, see qflash_quant_elem.cuh).
+// The exact definition, out of line: taken for ~1e-4 of the vectors (x r within 2^-14 of a
+// half-integer), so its division sequence is one copy in the binary instead of one per
+// unrolled element -- the prologue runs once per launch from a cold instruction cache, and
+// the inlined copies made its quantize phase ~46 KB of mostly skipped code (ncu: the
+// no_instructions stall led the fused step, profiles/r2_ncu_summary.md).
+static __device__ __noinline__ uint32_t quant4_exact(float4 v, float s) {
+  return pack4_sat_s8(quant_exact(v.x, s), quant_exact(v.y, s), quant_exact(v.z, s), quant_exact(v.w, s));
+}
+// Fast path only: `bad` flags a vector whose codes must come from quant4_exact.
+__device__ __forceinline__ uint32_t quant4_fast(const float4& v, float r, bool& bad) {
+  const int32_t q0 = quant_fast(v.x, r, bad);
+  const int32_t q1 = quant_fast(v.y, r, bad);
+  const int32_t q2 = quant_fast(v.z, r, bad);
+  const int32_t q3 = quant_fast(v.w, r, bad);
+  return pack4_sat_s8(q0, q1, q2, q3);
+}
 __device__ __forceinline__ uint32_t quant4(const float4& v, float s, float r) {
-  int32_t q[4];
   bool bad = false;
-  q[0] = quant_fast(v.x, r, bad);
-  q[1] = quant_fast(v.y, r, bad);
-  q[2] = quant_fast(v.z, r, bad);
-  q[3] = quant_fast(v.w, r, bad);
-  if (bad) {
-    q[0] = quant_exact(v.x, s);
-    q[1] = quant_exact(v.y, s);
-    q[2] = quant_exact(v.z, s);
-    q[3] = quant_exact(v.w, s);
-  }
-  return pack4_sat_s8(q[0], q[1], q[2], q[3]);
+  const uint32_t w = quant4_fast(v, r, bad);
+  return bad ? quant4_exact(v, s) : w;
 }
 __device__ __forceinline__ float amax4(float m, const float4& v) {
   return fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
@@ -1295,7 +1308,9 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   } else {
   if (resident) {
     // every load of all three tensors in flight before the first reduction (packed
-    // QKV input: the same loads with the (token, head) transpose of the addresses)
+    // QKV input: the same loads with the (token, head) transpose of the addresses);
+    // read once (registers keep them for the quantize pass): L2 evict-first
+    const uint64_t pol = QF_EVICT_FIRST ? l2_evict_first_policy() : 0ull;
     auto load_all = [&](auto packed) {
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
@@ -1303,7 +1318,8 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
 #pragma unroll
         for (int u = 0; u < kVR; ++u) {
           const int64_t i = gtid + u * nthr;
-          reg[t][u] = i < nvec ? ldg_stream(src + qkv_src_vec<D, decltype(packed)::value>(a, t, i))
+          reg[t][u] = i < nvec ? (QF_EVICT_FIRST ? ldg_stream_ef(src + qkv_src_vec<D, decltype(packed)::value>(a, t, i), pol)
+                                                 : ldg_stream(src + qkv_src_vec<D, decltype(packed)::value>(a, t, i)))
                                : make_float4(0.f, 0.f, 0.f, 0.f);  // no L1 allocation
         }
       }
@@ -1405,17 +1421,35 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   }
   // 3. quantize this thread's share (registers, or an L2-resident re-read with
   // all three tensors' loads in flight per step, as in the amax pass)
+  QF_FQ_TS_AT(a, 14, 0, 32);
   float r3[3];
 #pragma unroll
   for (int t = 0; t < 3; ++t) r3[t] = __frcp_rn(s3[t]);
+  QF_FQ_TS_AT(a, 15, 0, 32);
   if (resident) {
+    // fast path for every register-resident vector (stored at once), then the rare
+    // flagged vectors again through the out-of-line exact definition
+    uint32_t badmask = 0;
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
       uint32_t* dst = reinterpret_cast<uint32_t*>(a.xq[t]);
 #pragma unroll
       for (int u = 0; u < kVR; ++u) {
         const int64_t i = gtid + u * nthr;
-        if (i < nvec) dst[i] = quant4(reg[t][u], s3[t], r3[t]);
+        bool bad = false;
+        const uint32_t w = quant4_fast(reg[t][u], r3[t], bad);
+        if (i < nvec) dst[i] = w;
+        badmask |= (bad && i < nvec) ? (1u << (t * kVR + u)) : 0u;
+      }
+    }
+    QF_FQ_TS_AT(a, 16, 0, 32);
+    if (badmask != 0) {
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        uint32_t* dst = reinterpret_cast<uint32_t*>(a.xq[t]);
+#pragma unroll
+        for (int u = 0; u < kVR; ++u)
+          if (badmask & (1u << (t * kVR + u))) dst[gtid + u * nthr] = quant4_exact(reg[t][u], s3[t]);
       }
     }
   } else {

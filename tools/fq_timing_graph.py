@@ -13,12 +13,12 @@ from paper_2604_25306_b200.inputs import CATALOG, gen_real_qkv  # noqa: E402
 
 names = {8: "entry", 0: "prologue", 1: "amax", 2: "sync1", 3: "constants", 4: "quantized",
          5: "sync2", 9: "teardown", 13: "w1:scales", 6: "w1:quantized", 7: "w1:fenced",
-         10: "w1:sync2", 12: "lastCTA:teardown"}
+         10: "w1:sync2", 12: "lastCTA:teardown", 14: "w1:dq", 15: "w1:rcp", 16: "w1:qfast"}
 for wl, b in [("A3", 8), ("A4", 8), ("A1", 1)]:
     w = CATALOG[wl]
     P, N, d = w.problems(b), w.seq_len, w.head_dim
     base = [torch.from_numpy(x).cuda() for x in gen_real_qkv(P, N, d, seed=0, family=w.family)]
-    n_sets = 12
+    n_sets = int(os.environ.get("FQ_SETS", "12"))
     sets = [[(t * (-1.0 if i % 2 else 1.0)).roll(shifts=i, dims=1).contiguous() for t in base]
             for i in range(n_sets)]
     pipes = [qf.QFlashPipeline(P, N, d) for _ in range(n_sets)]
@@ -41,9 +41,9 @@ for wl, b in [("A3", 8), ("A4", 8), ("A1", 1)]:
     e1.record()
     torch.cuda.synchronize()
     print(f"== {wl} b{b}: {e0.elapsed_time(e1) * 1e3 / (20 * n_sets):.2f} us per step (graph)")
-    stamps = [p.workspace.view(torch.int64)[768:782].cpu().numpy() for p in pipes]
+    stamps = [p.workspace.view(torch.int64)[768:785].cpu().numpy() for p in pipes]
     t0 = stamps[0][8]
     for i in (n_sets - 2, n_sets - 1):
         st = stamps[i]
-        print(f"  step {i}: " + "  ".join(f"{names[k]} {(st[k] - st[8]) / 1e3:.2f}" for k in [0, 1, 2, 13, 3, 6, 7, 4, 5, 10, 9, 12])
+        print(f"  step {i}: " + "  ".join(f"{names[k]} {(st[k] - st[8]) / 1e3:.2f}" for k in [0, 1, 2, 13, 14, 15, 16, 3, 6, 7, 4, 5, 10, 9, 12])
               + f"  | entry after prev teardown: {(st[8] - stamps[i - 1][9]) / 1e3:.2f} us")

@@ -11,7 +11,8 @@ from paper_2604_25306_b200 import _lib  # noqa: E402
 from paper_2604_25306_b200.inputs import gen_int8_qkv  # noqa: E402
 
 NAMES = {0: "entry", 1: "setup done", 2: "mma: Q landed", 100: "softmax: final PV done",
-         101: "softmax: row stored", 102: "teardown"}
+         101: "softmax: row stored", 102: "teardown", 103: "softmax: tables ready",
+         104: "softmax: O, l loaded"}
 for j in range(7):
     NAMES[3 + 4 * j] = f"mma: KV{j} landed"
     NAMES[4 + 4 * j] = f"mma: P{j} ready"
