@@ -1740,6 +1740,8 @@ __global__ void __launch_bounds__(Cfg<D, BC, NSEG, CS, QT>::kThreads, 1)
   if (threadIdx.x == 0 && blockIdx.x == 0) QF_TS(1);
   // Everything above overlaps the tail of the previous kernel (programmatic
   // dependent launch); every global access of this grid comes after the wait.
+  // (Moving this setup behind the fused prologue's load issue instead was measured
+  // 0.4 us slower per step, profiles/r2_experiments.md.)
   griddep_wait();
   IntParams* sprm = reinterpret_cast<IntParams*>(smem + C::kPrm);
   if constexpr (FQ && PH) {

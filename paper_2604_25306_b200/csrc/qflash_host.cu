@@ -342,12 +342,14 @@ qflash_status launch_common(const int8_t* q, const int8_t* k, const int8_t* v,
   // shared memory; else cfg 0 (one tile, 4 column splits: lowest latency per
   // tile).  QFLASH_ATTN_CFG=0..3 overrides.
   const int cfg_env = forced_config();
-  // Measured (profiles/r1_cfg_ab.txt): multi-wave with several KV tiles -> cfg 1
-  // (L14 b64: 848 vs 938 us for cfg 2); one KV tile (Swin windows) -> cfg 2.
+  // Measured: multi-wave with several KV tiles -> cfg 1 (profiles/r1_cfg_ab.txt, L14 b64:
+  // 848 vs 938 us for cfg 2); multi-wave with one KV tile (Swin windows) -> cfg 1 as well
+  // since round 2 (profiles/r2b_cfg_ab.txt, chained graphs: A4 b8 25.7 vs 26.6 us for cfg 2,
+  // Swin-B s1 b8 32.3 vs 33.2 us); cfg 2 where cfg 1 does not fit.
   const int Tc_host = (N + bc_eff - 1) / bc_eff;
   int cfg = 0;
   if (tiles > sms && heads == 0) {
-    const int pref[2] = {Tc_host == 1 ? 2 : 1, Tc_host == 1 ? 1 : 2};
+    const int pref[2] = {1, 2};
     for (int c : pref)
       if (cfg == 0 && qf::attention_supported(d, bc_eff, nseg, c)) cfg = c;
   }
