@@ -475,8 +475,12 @@ def main():
         # launch cost (~2.5 us) is paid once per n_sets steps; --graph-steps 1 times one
         # graph launch per step
         chain = None
+        # the chain cycles the input sets until it holds >= 48 steps (the sets already
+        # exceed 2x L2, so every step still reads cold inputs)
+        chain_len = n_sets * (max(1, -(-48 // n_sets)) if set_bytes < (64 << 20) else 1)
         if args.graph_steps != "1":
-            chain = capture(lambda: [p(*s, stream=stream) for p, s in zip(pipes, sets)], stream)
+            chain = capture(lambda: [pipes[i % n_sets](*sets[i % n_sets], stream=stream)
+                                     for i in range(chain_len)], stream)
 
         def run_step(i):
             graphs[i % n_sets].replay()
@@ -484,9 +488,9 @@ def main():
         def run_steps(k):  # k consecutive steps starting at set 0
             done = 0
             if chain is not None:
-                while k - done >= n_sets:
+                while k - done >= chain_len:
                     chain.replay()
-                    done += n_sets
+                    done += chain_len
             for i in range(done, k):
                 run_step(i)
         launches_per_step = pipes[0].launches()
@@ -540,7 +544,7 @@ def main():
     graphs_per_replay = 1
     if one_launch:
         kgraphs = graphs if chain is None else [chain]
-        graphs_per_replay = 1 if chain is None else n_sets
+        graphs_per_replay = 1 if chain is None else chain_len
         kname = "qflash_attn_kernel<FQ> (fused step: quantize prologue + attention + dequantize)"
     elif strong:
         kgraphs = g_step
@@ -747,7 +751,7 @@ def main():
                                           ", per-slab scales, no collective" if world > 1 else "")),
                        "step": step_desc, "scales": args.scales,
                        "l2": f"rotating {n_sets} input sets ({n_sets * set_bytes / 2**20:.0f} MiB > 2x L2)",
-                       "graph": (f"{n_sets} consecutive steps (one per input set) per CUDA graph replay"
+                       "graph": (f"{chain_len} consecutive steps (cycling the {n_sets} input sets) per CUDA graph replay"
                                  if (not strong and chain is not None) else "one CUDA graph replay per step")},
             "us_per_call_graph_per_step": (step_graph1_ms * 1e3 if step_graph1_ms is not None else None),
             "rank_ms_per_step": rank_ms,

@@ -88,6 +88,9 @@ constexpr int kBlockR = 128;
 #ifndef QF_SLEEP_PROD
 #define QF_SLEEP_PROD 0  // > 0: producers poll with test_wait + nanosleep(ns) instead of a suspended try_wait
 #endif
+#ifndef QF_NO_CODE_STORE
+#define QF_NO_CODE_STORE 0  // timing experiment only: quantize without storing the codes (wrong output)
+#endif
 #ifndef QF_EVICT_FIRST
 #define QF_EVICT_FIRST 0  // 1: L2 evict-first policy on the fused step's fp32 input loads / output stores
 #endif
@@ -1237,6 +1240,19 @@ __device__ __forceinline__ void correction_role(const AttnArgs& args, const IntP
   } while (0)
 #endif
 #define QF_FQ_TS(a, k) QF_FQ_TS_AT(a, k, 0, 0)
+// per-CTA event ev (1..3) of the timing build: low 32 bits of globaltimer at bytes 6400..8176 (thread 0)
+#ifdef QF_FQ_TIMING
+#define QF_FQ_CTA(a, ev)                                                                                \
+  do {                                                                                                  \
+    if (threadIdx.x == 0 && blockIdx.x < 148)                                                           \
+      reinterpret_cast<uint32_t*>(reinterpret_cast<char*>((a).prm_out) + 6400)[3 * blockIdx.x + (ev) - 1] = \
+          static_cast<uint32_t>(globaltimer_ns());                                                      \
+  } while (0)
+#else
+#define QF_FQ_CTA(a, ev) \
+  do {                  \
+  } while (0)
+#endif
 // Source float4 of output vector i (the [P, N, d] layout of tensor t) in the fused step's
 // input: the same index for three separate tensors; for a packed QKV projection output
 // [P / H, N, 3, H, d] (N2, dynamic quantization of the projection P:L703) the (n, h)
@@ -1422,6 +1438,10 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   // 3. quantize this thread's share (registers, or an L2-resident re-read with
   // all three tensors' loads in flight per step, as in the amax pass)
   QF_FQ_TS_AT(a, 14, 0, 32);
+  // Warp 0 holds no data (its lane 0 derived the constants): a warp-uniform skip, so it
+  // reaches the second barrier without issuing the ~540 predicated-off instructions of
+  // the unrolled quantize pass after the derivation.
+  if (data_thread) {
   float r3[3];
 #pragma unroll
   for (int t = 0; t < 3; ++t) r3[t] = __frcp_rn(s3[t]);
@@ -1438,7 +1458,7 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
         const int64_t i = gtid + u * nthr;
         bool bad = false;
         const uint32_t w = quant4_fast(reg[t][u], r3[t], bad);
-        if (i < nvec) dst[i] = w;
+        if (i < nvec && !QF_NO_CODE_STORE) dst[i] = w;
         badmask |= (bad && i < nvec) ? (1u << (t * kVR + u)) : 0u;
       }
     }
@@ -1475,15 +1495,22 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
     if (a.qkv_H == 0) stream_quant(std::false_type{});
     else stream_quant(std::true_type{});
   }
+  }  // data_thread
   // int8 codes (generic-proxy stores) -> TMA loads of other CTAs after the barrier
   QF_FQ_TS(a, 4);
   QF_FQ_TS_AT(a, 6, 0, 32);
   fence_proxy_async_global();
   QF_FQ_TS_AT(a, 7, 0, 32);
+#ifdef QF_FQ_TIMING
+  __syncthreads();  // timing build: the stamp marks the CTA's last thread done
+#endif
+  QF_FQ_CTA(a, 1);
   if (a.cluster_grid) cluster_sync_all();
   else cooperative_groups::this_grid().sync();
+  QF_FQ_CTA(a, 2);
   fence_proxy_async_global();
   QF_FQ_TS(a, 5);
+  QF_FQ_CTA(a, 3);
   QF_FQ_TS_AT(a, 10, 0, 32);
 }
 
