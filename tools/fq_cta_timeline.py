@@ -15,7 +15,7 @@ for wl, b in [("A3", 8), ("A1", 1), ("A4", 8)]:
     w = CATALOG[wl]
     P, N, d = w.problems(b), w.seq_len, w.head_dim
     base = [torch.from_numpy(x).cuda() for x in gen_real_qkv(P, N, d, seed=0, family=w.family)]
-    n_sets = 12
+    n_sets = int(os.environ.get('FQ_SETS', '12'))
     sets = [[(t * (-1.0 if i % 2 else 1.0)).roll(shifts=i, dims=1).contiguous() for t in base] for i in range(n_sets)]
     pipes = [qf.QFlashPipeline(P, N, d) for _ in range(n_sets)]
     s = torch.cuda.Stream()
@@ -37,7 +37,7 @@ for wl, b in [("A3", 8), ("A1", 1), ("A4", 8)]:
         st = st.astype(np.float64) / 1e3
         G = st.shape[0]
         print(f"== {wl} b{b}: {G} CTAs (us from the first barrier-2 arrival)")
-        for k, name in enumerate(["barrier-2 arrive", "barrier-2 exit", "proxy fence done"]):
+        for k, name in enumerate(os.environ.get("CTA_EVENTS", "barrier-2 arrive,barrier-2 exit,proxy fence done").split(",")):
             c = st[:, k]
             print(f"  {name:18s} min {c.min():6.2f}  median {np.median(c):6.2f}  p90 {np.percentile(c, 90):6.2f}  max {c.max():6.2f}  argmax CTA {int(c.argmax())}")
         q = st[:, 1] - st[:, 0]
