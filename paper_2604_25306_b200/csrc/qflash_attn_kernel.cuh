@@ -1274,6 +1274,13 @@ QF_DEV int64_t qkv_src_vec(const AttnArgs& a, int t, int64_t i) {
   return static_cast<int64_t>(((b * a.N + n) * 3 + t) * (static_cast<uint64_t>(a.qkv_H) * R) + h * R + k4);
 }
 
+// The fused prologue's grid barrier: hardware cluster barrier for a one-cluster grid, else the
+// cooperative-groups grid barrier (an out-of-line copy shared by both call sites was measured
+// slower, profiles/r2_experiments.md §11).
+static __device__ __forceinline__ void fused_grid_barrier(int cluster_grid) {
+  if (cluster_grid) cluster_sync_all();
+  else cooperative_groups::this_grid().sync();
+}
 // Code store of the fused prologue.
 __device__ __forceinline__ void stg_code(uint32_t* p, uint32_t w) { *p = w; }
 // Quantize one float4 (4 elements) -> 4 packed int8 codes (exact, see qflash_quant_elem.cuh).
@@ -1392,8 +1399,7 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   // fences saved ~1 us of the A3 step (profiles/r1_cfg_ab.txt).  A flag barrier
   // (per-CTA tagged slots polled by every CTA, no atomics) was measured slower:
   // 2.8 us vs 1.3 us -- the polling traffic competes with the stragglers' loads.
-  if (a.cluster_grid) cluster_sync_all();
-  else cooperative_groups::this_grid().sync();
+  fused_grid_barrier(a.cluster_grid);
   QF_FQ_TS(a, 2);
 #ifdef QF_FQ_TIMING_B1
   QF_FQ_CTA(a, 2);
@@ -1526,8 +1532,7 @@ __device__ __forceinline__ void fused_quantize_prologue(const AttnArgs& a, float
   __syncthreads();  // timing build: the stamp marks the CTA's last thread done
   QF_FQ_CTA(a, 1);
 #endif
-  if (a.cluster_grid) cluster_sync_all();
-  else cooperative_groups::this_grid().sync();
+  fused_grid_barrier(a.cluster_grid);
 #ifndef QF_FQ_TIMING_B1
   QF_FQ_CTA(a, 2);
 #endif
