@@ -359,6 +359,25 @@ class QFlashPipeline:
         self.o_q = torch.empty(self.shape, dtype=torch.int8, device=dev)
         self.workspace = torch.zeros(_lib.DSCALE_WORKSPACE_BYTES // 4, dtype=torch.int32, device=dev)
         self.out = torch.empty(self.shape, dtype=torch.float32, device=dev)
+        self.device = self.out.device
+        # the fused call's fixed arguments (buffers owned and sized here), marshalled once:
+        # a call then checks and converts only q, k, v and the stream
+        self._fused_shape = AttnShape(P, N, d, block_kv)
+        self._fused_fixed = (ctypes.byref(self._fused_shape), _lib.VARIANTS[variant],
+                             _dev_ptr(self.qkv_q[0]), _dev_ptr(self.qkv_q[1]), _dev_ptr(self.qkv_q[2]),
+                             None, _dev_ptr(self.out), _dev_ptr(self.scales), _dev_ptr(self.workspace), None)
+
+    def _fused_call(self, q, k, v, stream):
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            if t.shape != self.out.shape or t.dtype != torch.float32 or t.device != self.device \
+                    or not t.is_contiguous():
+                raise ValueError("%s: expected a contiguous float32 %s tensor on %s, got %s %s on %s"
+                                 % (name, tuple(self.shape), self.device, t.dtype, tuple(t.shape), t.device))
+        f = self._fused_fixed
+        check(lib().qflash_forward_fused_amax(
+            ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(k.data_ptr()), ctypes.c_void_p(v.data_ptr()),
+            f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7], f[8], f[9], _stream(stream)))
+        return self.out
 
     def launches(self, dtype=torch.float32) -> int:
         """Kernel launches per call (bench.py's gpu_launches)."""
@@ -369,11 +388,9 @@ class QFlashPipeline:
         return quant + (1 if self.mode == "two" else 2)
 
     def __call__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, stream=None):
-        _check_like(self.out, q, "q", q.dtype)   # the buffers were sized for self.shape
         if self.mode == "fused" and q.dtype == torch.float32:
-            return qflash_forward_fused(q, k, v, self.block_kv, self.variant, out=self.out,
-                                        codes=self.qkv_q, scales=self.scales,
-                                        workspace=self.workspace, stream=stream)
+            return self._fused_call(q, k, v, stream)
+        _check_like(self.out, q, "q", q.dtype)   # the buffers were sized for self.shape
         qflash_quantize_qkv_prepare(q, k, v, outs=self.qkv_q, scales=self.scales,
                                     workspace=self.workspace, stream=stream)
         if self.mode != "three":

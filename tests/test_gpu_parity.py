@@ -804,3 +804,26 @@ def test_fused_per_head_one_head_equals_per_tensor():
     y_t = qf.qflash_forward(dq, dk, dv)
     torch.cuda.synchronize()
     assert torch.equal(y.view(torch.int32), y_t.view(torch.int32))
+
+
+@pytest.mark.gpu
+def test_pipeline_fused_fast_path_matches_and_checks():
+    # QFlashPipeline's fused call marshals its own buffers once at construction; the
+    # per-call path checks q, k, v itself: same bytes as qflash_forward_fused, and the
+    # same rejections before anything reaches the C ABI
+    w = CATALOG["A3"]
+    P, N, d = w.problems(1), w.seq_len, w.head_dim
+    q, k, v = _dev(*gen_real_qkv(P, N, d, seed=3))
+    pipe = qf.QFlashPipeline(P, N, d, mode="fused")
+    y1 = pipe(q, k, v).clone()
+    y2 = qf.qflash_forward_fused(q, k, v)
+    torch.cuda.synchronize()
+    assert torch.equal(y1.view(torch.int32), y2.view(torch.int32))
+    with pytest.raises(ValueError):
+        pipe(q, k[:, :-1].contiguous(), v)                    # wrong shape
+    with pytest.raises(ValueError):
+        pipe(q, k, v.transpose(1, 2).contiguous().transpose(1, 2))  # not contiguous
+    with pytest.raises(ValueError):
+        pipe(q, k.to(torch.float16), v)                       # wrong dtype
+    with pytest.raises(ValueError):
+        pipe(q, k.cpu(), v)                                   # wrong device
