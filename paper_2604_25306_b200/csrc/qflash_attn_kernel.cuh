@@ -471,13 +471,34 @@ QF_DEV void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
   else tmem_ld<W>(taddr, r);
 }
 
+// Max of N int32 values as a tree of 3-input maxima (VIMNMX3): dependency depth
+// ceil(log3 N) instead of the N / 2 of a running max (a 16-deep chain for 32 columns).
+template <int N>
+QF_DEV int32_t tree_max(const int32_t* v) {
+  if constexpr (N == 1) {
+    return v[0];
+  } else if constexpr (N == 2) {
+    return max(v[0], v[1]);
+  } else {
+    constexpr int M = (N + 2) / 3;
+    int32_t t[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      const int32_t a = v[3 * i];
+      const int32_t b = 3 * i + 1 < N ? v[3 * i + 1] : a;
+      const int32_t c = 3 * i + 2 < N ? v[3 * i + 2] : a;
+      t[i] = max(a, max(b, c));
+    }
+    return tree_max<M>(t);
+  }
+}
+
 // Row max over the first `valid` of W columns (valid warp-uniform; <= 0: none).
 template <int W>
 QF_DEV int32_t row_max_masked(const uint32_t* s, int valid) {
   int32_t t = INT32_MIN;
   if (valid >= W) {
-#pragma unroll
-    for (int e = 0; e < W; ++e) t = max(t, static_cast<int32_t>(s[e]));
+    t = tree_max<W>(reinterpret_cast<const int32_t*>(s));
   } else {
 #pragma unroll
     for (int k = 0; k < W / 8; ++k) {
@@ -761,11 +782,13 @@ __device__ __forceinline__ void softmax_role(const AttnArgs& args, const IntPara
           for (int h = 0; h < NH; ++h) tmem_ld32(tS + c0 + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(s + 32 * h));
         }
         tmem_wait_ld();
+        if (dbg && ts_warp && j < 7) QF_TS(60 + j);
         if constexpr (DBG) {
           if (args.dbg_s != nullptr && dbg && j == 0)
             for (int e = 0; e < CW; ++e) args.dbg_s[row * BC + c0 + e] = static_cast<int32_t>(s[e]);
         }
         tmax = row_max_masked<CW>(s, valid);
+        if (dbg && ts_warp && j < 7) QF_TS(70 + j);
       }
       // (2)(3) combine the partial maxima of the group's CS warpgroups
       if constexpr (CS > 1) {

@@ -27,6 +27,8 @@ for j in range(7):
     NAMES[47 + 8 * j] = f"softmax: release{j} stored"
     NAMES[110 + j] = f"softmax: wait_st{j} done"
     NAMES[43 + 8 * j] = f"softmax: P{j} arrived"
+    NAMES[60 + j] = f"softmax: S{j} loaded (tcgen05.ld done)"
+    NAMES[70 + j] = f"softmax: S{j} row max done"
 
 for (P, N, d, variant, label) in [(96, 197, 64, 0, "A3 b8"), (1536, 49, 32, 0, "A4 b8"),
                                   (1024, 1025, 64, 0, "L14 b64")]:
