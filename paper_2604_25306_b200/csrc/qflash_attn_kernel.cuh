@@ -2115,18 +2115,28 @@ cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CU
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)
           nonportable[dev] = 1;
       }
-      cudaLaunchAttribute ca[1];
+      cudaLaunchAttribute ca[2];
       ca[0].id = cudaLaunchAttributeClusterDimension;
       ca[0].val.clusterDim.x = static_cast<unsigned>(G);
       ca[0].val.clusterDim.y = 1;
       ca[0].val.clusterDim.z = 1;
+      // programmatic serialization as for the cooperative form: the next step's setup
+      // overlaps this one's tail (griddep_wait precedes every global access)
+      ca[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      ca[1].val.programmaticStreamSerializationAllowed = 1;
       cudaLaunchConfig_t ccfg = cfg;
       ccfg.attrs = ca;
-      ccfg.numAttrs = 1;
+      ccfg.numAttrs = (pdl_mask() & 8) ? 2 : 1;
       AttnArgs cargs = args;
       cargs.cluster_grid = 1;
       if (cudaLaunchKernelEx(&ccfg, kern, tq, tk, tv, cargs) == cudaSuccess) return cudaSuccess;
-      (void)cudaGetLastError();  // cluster shape not schedulable here: cooperative launch
+      (void)cudaGetLastError();
+      if (ccfg.numAttrs == 2) {  // without PDL
+        ccfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&ccfg, kern, tq, tk, tv, cargs) == cudaSuccess) return cudaSuccess;
+        (void)cudaGetLastError();
+      }
+      // cluster shape not schedulable here: cooperative launch
     }
     // fused step: grid barriers in the quantize prologue need every CTA resident;
     // programmatic serialization lets the next step's grid be launched (and run its
