@@ -43,6 +43,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include <cooperative_groups.h>
@@ -2129,8 +2131,18 @@ cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CU
       ccfg.numAttrs = (pdl_mask() & 8) ? 2 : 1;
       AttnArgs cargs = args;
       cargs.cluster_grid = 1;
-      if (cudaLaunchKernelEx(&ccfg, kern, tq, tk, tv, cargs) == cudaSuccess) return cudaSuccess;
+      const cudaError_t ce = cudaLaunchKernelEx(&ccfg, kern, tq, tk, tv, cargs);
+      if (ce == cudaSuccess) return cudaSuccess;
       (void)cudaGetLastError();
+      if (getenv("QFLASH_DEBUG_LAUNCH") != nullptr) {
+        int nclusters = -1;
+        ccfg.numAttrs = 1;
+        cudaOccupancyMaxActiveClusters(&nclusters, kern, &ccfg);
+        (void)cudaGetLastError();
+        fprintf(stderr, "qflash: %d-CTA cluster launch failed (%s); max active clusters %d\n",
+                static_cast<int>(G), cudaGetErrorString(ce), nclusters);
+        ccfg.numAttrs = (pdl_mask() & 8) ? 2 : 1;
+      }
       if (ccfg.numAttrs == 2) {  // without PDL
         ccfg.numAttrs = 1;
         if (cudaLaunchKernelEx(&ccfg, kern, tq, tk, tv, cargs) == cudaSuccess) return cudaSuccess;
