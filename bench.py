@@ -331,11 +331,13 @@ def table1_sweep(qfl, dev, stream, reps=400):
                     for i in range(n_sets)]
             pipes = [qfl.QFlashPipeline(P, N, d, device=dev) for _ in range(n_sets)]
             # one graph per n_sets consecutive steps (each on its own cold set), as the main line
-            g_step = capture(lambda: [p(*s, stream=stream) for p, s in zip(pipes, sets)], stream)
-            t_step = graph_time([g_step], stream, max(1, reps // n_sets)) / n_sets
+            L = n_sets * max(1, -(-48 // n_sets))  # >= 48 steps per graph, as the main line
+            g_step = capture(lambda: [pipes[i % n_sets](*sets[i % n_sets], stream=stream) for i in range(L)], stream)
+            t_step = graph_time([g_step], stream, max(1, reps // L)) / L
             g_att = capture(lambda: [qfl.qflash_attention_int8_prepared(
-                p.qkv_q[0], p.qkv_q[1], p.qkv_q[2], p.workspace, out=p.o_q, stream=stream) for p in pipes], stream)
-            t_att = graph_time([g_att], stream, max(1, reps // n_sets)) / n_sets
+                pipes[i % n_sets].qkv_q[0], pipes[i % n_sets].qkv_q[1], pipes[i % n_sets].qkv_q[2],
+                pipes[i % n_sets].workspace, out=pipes[i % n_sets].o_q, stream=stream) for i in range(L)], stream)
+            t_att = graph_time([g_att], stream, max(1, reps // L)) / L
             out[f"{name} b{batch}"] = {
                 "problems": P, "seq_len": N, "head_dim": d,
                 "step_us": t_step * 1e3, "step_tops": alg["int8_ops"] / (t_step * 1e-3) / 1e12,
