@@ -469,7 +469,8 @@ def test_pipeline_end_to_end_bit_exact(orc):
     assert np.array_equal(out.numpy().view(np.uint32), ref.view(np.uint32))
 
 
-@pytest.mark.parametrize("name,batch", [("A1", 1), ("A3", 8), ("A4", 8), ("A7", 1), ("SwinB-s3", 8)])
+@pytest.mark.parametrize("name,batch", [("A1", 1), ("A3", 8), ("A4", 8), ("A7", 1), ("SwinB-s3", 8),
+                                        ("SwinB-s2", 8), ("SwinB-s1", 8)])
 def test_fused_step_and_dequant_epilogue_bit_exact(orc, name, batch):
     # quantize_prepare -> attention with the DQ step fused into the epilogue (fp32 bits from
     # the quantizer's table) == oracle dequantize(attention(quantize)) == the 3-stage path
